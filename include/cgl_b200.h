@@ -1,0 +1,178 @@
+/*
+ * cgl_b200.h — C ABI of the B200-native CGL time-integration hot path.
+ *
+ * Drop-in boundary for the reference package `cglsolve` (arXiv 2403.02816,
+ * /root/reference/pkg/src/cglsolve).  The reference has no FFI: its seam is
+ * the Python operator protocol (operators.py:106-208) and the stepper bodies
+ * (integrators.py:130-227).  Each entry point below replaces the numpy call
+ * site named in its comment; the Python package `paper_2403_02816_b200`
+ * binds them with ctypes behind the same Python API.
+ *
+ * Conventions (all entry points):
+ *   - complex128 data = interleaved (re, im) doubles, C-contiguous tensors of
+ *     shape (n_1, ..., n_d) (last axis fastest), device pointers;
+ *   - `stream` is a cudaStream_t passed as void*; work is enqueued, never
+ *     synchronised;
+ *   - return 0 on success, a negative CGL_E* code on argument errors, or a
+ *     positive cudaError_t; cgl_last_error() has the message;
+ *   - `flag`/`pos` implement the sticky divergence record (may be NULL/0):
+ *     a kernel at position pos skips when an earlier position diverged.
+ */
+#ifndef CGL_B200_H
+#define CGL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGL_ABI_VERSION 1
+
+#define CGL_EINVAL (-1)
+#define CGL_ESHAPE (-2)
+#define CGL_ECUFFT (-3)
+
+/* Sticky divergence record in device memory (8 bytes, init all-ones).
+ * key = (step << 24) | (seq << 8) | reason, atomically min-reduced, so it
+ * holds the first (step, call) that failed; mirrors DivergenceError(reason)
+ * + diverged_at of integrators.py:264-278 and flows.py:32-39,95-132. */
+typedef struct cgl_flag_t { unsigned long long key; } cgl_flag_t;
+
+enum cgl_reason {
+  CGL_BLOWUP_CUBIC = 0,      /* flows.py:95-96  "finite-time blow-up in cubic flow" */
+  CGL_NONFINITE_CUBIC = 1,   /* flows.py:99-100 "non-finite cubic flow output" */
+  CGL_BLOWUP_QUINTIC = 2,    /* flows.py:111-112 */
+  CGL_NONFINITE_QUINTIC = 3, /* flows.py:114-115 */
+  CGL_NONFINITE_RK4 = 4,     /* flows.py:131-132 "non-finite RK4 flow output" */
+  CGL_NONFINITE_STATE = 5    /* integrators.py:274-278 "non-finite state" */
+};
+
+/* Nonlinearity (flows.py:42-78). kind: 0 cubic, 1 cubic_quintic,
+ * 2 coupled_cubic_quintic (two components). */
+typedef struct cgl_nonlinear_t {
+  double alpha3, beta3, alpha4, beta4, alpha5;
+  int kind;
+} cgl_nonlinear_t;
+
+const char* cgl_version(void);
+const char* cgl_last_error(void);
+int cgl_abi_version(void);
+
+/* Number of kernels this library has launched in this process (evidence
+ * counter for benchmarks; cuFFT's own kernels are not counted). */
+unsigned long long cgl_launch_count(void);
+
+/* FP64 tensor-pipe probe: a register-resident DMMA.8x8x4 loop on all SMs;
+ * returns the flops one launch performs (time it with events on `stream`).
+ * Used to report mu-mode-product rooflines against a measured FP64 peak. */
+double cgl_probe_dmma(void* stream, int iters);
+
+/* ---- dense complex-FP64 contractions (DMMA tensor cores) ---------------- */
+
+/* Batched complex GEMM, row-major:
+ *   C_b[m,n] = alpha * sum_k A_b[m,k] B_b[k,n] + beta * Y_b[m,n]
+ * A_b = A + b*sA (element (m,k) at m*lda+k), likewise B, C, Y (Y may be NULL,
+ * may alias C).  Strides/leading dims are in complex elements.
+ * Replaces the zgemm under np.tensordot (tensors.py:59). */
+int cgl_zgemm(void* stream, int64_t M, int64_t N, int64_t K,
+              const double* A, int64_t lda, int64_t sA,
+              const double* B, int64_t ldb, int64_t sB,
+              double* C, int64_t ldc, int64_t sC, int64_t batch,
+              double alpha_re, double alpha_im,
+              const double* Y, int64_t ldy, int64_t sY, double beta,
+              const cgl_flag_t* flag, uint64_t pos);
+
+/* mu-mode product out = u x_axis mat (tensors.py:38-59), plus optional
+ * out = alpha*(...) + beta*y.  mat is m_out x shape[axis] row-major; mat_t is
+ * its transpose (shape[axis] x m_out row-major), used when axis is the
+ * contiguous (last) axis. */
+int cgl_mode_product(void* stream, int ndim, const int64_t* shape, int axis,
+                     const double* mat, const double* mat_t, int64_t m_out,
+                     const double* in, double* out,
+                     double alpha, const double* y, double beta,
+                     const cgl_flag_t* flag, uint64_t pos);
+
+/* The same for nfields fields with per-field matrices in ONE GEMM launch
+ * (mats/mats_t/ins/outs/ys: arrays of nfields pointers, ys may be NULL). */
+int cgl_mode_product_batch(void* stream, int ndim, const int64_t* shape, int axis,
+                           int nfields, const double* const* mats,
+                           const double* const* mats_t, int64_t m_out,
+                           const double* const* ins, double* const* outs,
+                           double alpha, const double* const* ys, double beta,
+                           const cgl_flag_t* flag, uint64_t pos);
+
+/* Tucker chain out_f = in_f x_1 M_{f,1} ... x_d M_{f,d} for nfields fields
+ * in one launch per mode (tensors.py:62-69 / operators.py:134-139).
+ * mats/mats_t: nfields*ndim square matrices (field-major); work: nfields
+ * scratch fields (may be NULL when ndim == 1). in may not alias out. */
+int cgl_tucker(void* stream, int ndim, const int64_t* shape, int nfields,
+               const double* const* mats, const double* const* mats_t,
+               const double* const* in, double* const* out,
+               double* const* work, const cgl_flag_t* flag, uint64_t pos);
+
+/* ---- pointwise kernels (HBM-bound) --------------------------------------- */
+
+/* out = sum_i coef[i] * x[i] (nterms <= 6, real coefficients) —
+ * integrators.py:130-143 (_axpy/_add/_scale). out may alias an x[i]. */
+int cgl_lincomb(void* stream, int64_t n, int nterms, const double* coef,
+                const double* const* x, double* out,
+                const cgl_flag_t* flag, uint64_t pos);
+
+/* out_c = g_c(in_scale * in) per component (flows.py:62-78). */
+int cgl_eval_g(void* stream, int64_t n, const cgl_nonlinear_t* nl, int nfields,
+               const double* const* in, double in_scale, double* const* out,
+               const cgl_flag_t* flag, uint64_t pos);
+
+/* Exact cubic / quintic flows over time t of in_scale*in (flows.py:87-115);
+ * raise CGL_BLOWUP_* / CGL_NONFINITE_* at pos. */
+int cgl_cubic_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl,
+                   const double* in, double in_scale, double* out,
+                   cgl_flag_t* flag, uint64_t pos);
+int cgl_quintic_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl,
+                     const double* in, double in_scale, double* out,
+                     cgl_flag_t* flag, uint64_t pos);
+
+/* One fused RK4 step of size t on u' = g(u) (flows.py:118-133): one read and
+ * one write per component, all four stages in registers. */
+int cgl_rk4_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl,
+                 int nfields, const double* const* in, double in_scale,
+                 double* const* out, cgl_flag_t* flag, uint64_t pos);
+
+/* Raise CGL_NONFINITE_STATE at pos if any value of any field is NaN/Inf
+ * (integrators.py:274-278). */
+int cgl_check_finite(void* stream, int64_t n, int nfields,
+                     const double* const* x, cgl_flag_t* flag, uint64_t pos);
+
+int cgl_flag_reset(void* stream, cgl_flag_t* flag);
+
+/* Hadamard product out = factor .* in (spectral.py:123-129). */
+int cgl_pointwise_mul(void* stream, int64_t n, const double* factor,
+                      const double* in, double* out,
+                      const cgl_flag_t* flag, uint64_t pos);
+
+/* out = exp(s * symbol) elementwise (spectral.py:116-120). */
+int cgl_symbol_exp(void* stream, int64_t n, double s, const double* symbol,
+                   double* out);
+
+/* Separable Fourier multiplier: out[j] = in_scale * prod_mu table_mu[j_mu] * in[j],
+ * the factorised exp(f tau symbol) of spectral.py:89-120 (never reads an
+ * N-sized E). tables: ndim device arrays of shape[mu] complex values. */
+int cgl_separable_mul(void* stream, int ndim, const int64_t* shape,
+                      const double* const* tables, double in_scale,
+                      const double* in, double* out,
+                      const cgl_flag_t* flag, uint64_t pos);
+
+/* ---- FFT (cuFFT Z2Z) — spectral.py:79-86 --------------------------------- */
+/* Forward is unnormalised; "inverse" here is the unnormalised backward
+ * transform: callers fold the 1/N of dft_inverse into the next kernel's
+ * in_scale. */
+int cgl_fft_plan(int ndim, const int64_t* shape, void** plan);
+int cgl_fft_exec(void* plan, void* stream, const double* in, double* out, int inverse);
+int cgl_fft_destroy(void* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CGL_B200_H */

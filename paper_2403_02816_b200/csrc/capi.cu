@@ -1,0 +1,256 @@
+// extern "C" boundary (include/cgl_b200.h): argument validation, layout
+// mapping of mu-mode products onto the batched GEMM, and error plumbing.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "cgl_common.cuh"
+#include "cgl_internal.h"
+
+namespace cgl {
+
+// launchers from pointwise.cu / fft.cu
+int pw_lincomb(cudaStream_t, int64_t, int, const double*, const double* const*, double*, const cgl_flag_t*, uint64_t);
+int pw_eval_g(cudaStream_t, int64_t, const cgl_nonlinear_t*, int, const double* const*, double, double* const*,
+              const cgl_flag_t*, uint64_t);
+int pw_exact_flow(cudaStream_t, int, int64_t, double, const cgl_nonlinear_t*, const double*, double, double*,
+                  cgl_flag_t*, uint64_t);
+int pw_rk4_flow(cudaStream_t, int64_t, double, const cgl_nonlinear_t*, int, const double* const*, double,
+                double* const*, cgl_flag_t*, uint64_t);
+int pw_check_finite(cudaStream_t, int64_t, int, const double* const*, cgl_flag_t*, uint64_t);
+int pw_flag_reset(cudaStream_t, cgl_flag_t*);
+int pw_mul(cudaStream_t, int64_t, const double*, const double*, double*, const cgl_flag_t*, uint64_t);
+int pw_symexp(cudaStream_t, int64_t, double, const double*, double*);
+int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double, const double*, double*,
+                 const cgl_flag_t*, uint64_t);
+int fft_plan(int, const int64_t*, void**);
+int fft_exec(void*, cudaStream_t, const double*, double*, int);
+int fft_destroy(void*);
+
+static thread_local std::string g_err;
+static unsigned long long g_launches = 0;
+
+__global__ void dmma_probe_kernel(double* sink, int iters) {
+  double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+  double c[8][2] = {};
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double r = 0;
+  for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+  if (r == 1234.5) *sink = r;
+}
+
+int set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+int set_cuda_error(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return (int)e;
+}
+int check_launch(const char* name) {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, name);
+  return 0;
+}
+
+// Map out_f = alpha * (in_f x_axis mat_f) + beta * y_f onto one batched GEMM
+// launch over nitems fields.  shape is the input shape; out replaces
+// shape[axis] by m_out.
+static int mode_product_multi(cudaStream_t st, int ndim, const int64_t* shape, int axis, int64_t m_out, int nitems,
+                              const double* const* mats, const double* const* mats_t, const double* const* ins,
+                              double* const* outs, double alpha, const double* const* ys, double beta,
+                              const cgl_flag_t* flag, uint64_t pos) {
+  if (ndim < 1 || ndim > 8) return set_error(CGL_ESHAPE, "mode_product: ndim must be 1..8");
+  if (axis < 0 || axis >= ndim) return set_error(CGL_ESHAPE, "mode_product: axis out of range");
+  if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "mode_product: 1..8 fields per launch");
+  int64_t P = 1, Q = 1;
+  for (int d = 0; d < axis; ++d) P *= shape[d];
+  for (int d = axis + 1; d < ndim; ++d) Q *= shape[d];
+  const int64_t n = shape[axis];
+  for (int d = 0; d < ndim; ++d)
+    if (shape[d] < 0) return set_error(CGL_ESHAPE, "mode_product: negative extent");
+  if (m_out < 0) return set_error(CGL_ESHAPE, "mode_product: negative m_out");
+  GemmArgs a{};
+  a.alpha = make_double2(alpha, 0.0);
+  a.beta = beta;
+  a.flag = flag;
+  a.pos = pos;
+  bool have_y = false;
+  for (int f = 0; f < nitems; ++f) {
+    if (ins[f] == outs[f] && n > 0) return set_error(CGL_EINVAL, "mode_product: in and out must not alias");
+    have_y |= (ys && ys[f]);
+  }
+  if (Q == 1) {
+    // contiguous axis: Out (P x m) = In (P x n) * M^T
+    a.M = P; a.N = m_out; a.K = n;
+    a.lda = n; a.ldb = m_out; a.ldc = m_out; a.ldy = m_out;
+    a.sA = a.sB = a.sC = a.sY = 0;
+    a.batch = 1;
+    a.m_fastest = 0;
+    for (int f = 0; f < nitems; ++f) {
+      if (!mats_t || !mats_t[f]) return set_error(CGL_EINVAL, "mode_product: last-axis product needs mat_t");
+      a.items[f] = GemmItem{ins[f], mats_t[f], outs[f], have_y ? ys[f] : nullptr};
+    }
+  } else {
+    // Out_p (m x Q) = M (m x n) * In_p (n x Q), batched over the P leading slabs
+    a.M = m_out; a.N = Q; a.K = n;
+    a.lda = n; a.ldb = Q; a.ldc = Q; a.ldy = Q;
+    a.sA = 0; a.sB = n * Q; a.sC = m_out * Q; a.sY = m_out * Q;
+    a.batch = P;
+    a.m_fastest = 1;
+    for (int f = 0; f < nitems; ++f) {
+      if (!mats || !mats[f]) return set_error(CGL_EINVAL, "mode_product: null matrix");
+      a.items[f] = GemmItem{mats[f], ins[f], outs[f], have_y ? ys[f] : nullptr};
+    }
+  }
+  if (a.batch == 0) return 0;
+  return zgemm_launch(a, nitems, st);
+}
+
+}  // namespace cgl
+
+using namespace cgl;
+
+extern "C" {
+
+const char* cgl_version(void) { return "cgl_b200 1.0 (sm_100a, DMMA complex-FP64)"; }
+const char* cgl_last_error(void) { return g_err.c_str(); }
+int cgl_abi_version(void) { return CGL_ABI_VERSION; }
+unsigned long long cgl_launch_count(void) { return g_launches; }
+
+double cgl_probe_dmma(void* stream, int iters) {
+  static double* sink = nullptr;
+  if (!sink && cudaMalloc(&sink, sizeof(double)) != cudaSuccess) return -1.0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int blocks = sms * 4, threads = 256;
+  dmma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(sink, iters);
+  if (check_launch("dmma_probe")) return -1.0;
+  // 8 DMMA.8x8x4 per iteration per warp, 2*8*8*4 flops each
+  return (double)blocks * (threads / 32) * iters * 8.0 * 512.0;
+}
+
+int cgl_zgemm(void* stream, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA, const double* B,
+              int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC, int64_t batch, double alpha_re,
+              double alpha_im, const double* Y, int64_t ldy, int64_t sY, double beta, const cgl_flag_t* flag,
+              uint64_t pos) {
+  if (M < 0 || N < 0 || K < 0 || batch < 0) return set_error(CGL_ESHAPE, "zgemm: negative size");
+  if (lda < K || ldb < N || ldc < N || (Y && ldy < N)) return set_error(CGL_ESHAPE, "zgemm: leading dimension too small");
+  GemmArgs a{};
+  a.M = M; a.N = N; a.K = K;
+  a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.ldy = ldy;
+  a.sA = sA; a.sB = sB; a.sC = sC; a.sY = sY;
+  a.batch = batch;
+  a.alpha = make_double2(alpha_re, alpha_im);
+  a.beta = beta;
+  a.m_fastest = 1;
+  a.flag = flag;
+  a.pos = pos;
+  a.items[0] = GemmItem{A, B, C, Y};
+  if (batch == 0) return 0;
+  return zgemm_launch(a, 1, (cudaStream_t)stream);
+}
+
+int cgl_mode_product(void* stream, int ndim, const int64_t* shape, int axis, const double* mat, const double* mat_t,
+                     int64_t m_out, const double* in, double* out, double alpha, const double* y, double beta,
+                     const cgl_flag_t* flag, uint64_t pos) {
+  const double* ys[1] = {y};
+  return mode_product_multi((cudaStream_t)stream, ndim, shape, axis, m_out, 1, &mat, &mat_t, &in, &out, alpha,
+                            y ? ys : nullptr, beta, flag, pos);
+}
+
+int cgl_mode_product_batch(void* stream, int ndim, const int64_t* shape, int axis, int nfields,
+                           const double* const* mats, const double* const* mats_t, int64_t m_out,
+                           const double* const* ins, double* const* outs, double alpha, const double* const* ys,
+                           double beta, const cgl_flag_t* flag, uint64_t pos) {
+  return mode_product_multi((cudaStream_t)stream, ndim, shape, axis, m_out, nfields, mats, mats_t, ins, outs, alpha,
+                            ys, beta, flag, pos);
+}
+
+int cgl_tucker(void* stream, int ndim, const int64_t* shape, int nfields, const double* const* mats,
+               const double* const* mats_t, const double* const* in, double* const* out, double* const* work,
+               const cgl_flag_t* flag, uint64_t pos) {
+  if (nfields < 1 || nfields > kMaxItems) return set_error(CGL_EINVAL, "tucker: 1..8 fields per launch");
+  if (ndim < 1 || ndim > 8) return set_error(CGL_ESHAPE, "tucker: ndim must be 1..8");
+  if (ndim > 1 && !work) return set_error(CGL_EINVAL, "tucker: work buffers required for ndim > 1");
+  const double* src[kMaxItems];
+  double* dst[kMaxItems];
+  const double* m[kMaxItems];
+  const double* mt[kMaxItems];
+  for (int f = 0; f < nfields; ++f) {
+    if (in[f] == out[f]) return set_error(CGL_EINVAL, "tucker: in and out must not alias");
+    src[f] = in[f];
+  }
+  for (int axis = 0; axis < ndim; ++axis) {
+    const bool to_out = ((ndim - axis) % 2) == 1;  // the last product lands in out
+    for (int f = 0; f < nfields; ++f) {
+      dst[f] = to_out ? out[f] : work[f];
+      m[f] = mats[f * ndim + axis];
+      mt[f] = mats_t ? mats_t[f * ndim + axis] : nullptr;
+    }
+    int r = mode_product_multi((cudaStream_t)stream, ndim, shape, axis, shape[axis], nfields, m, mt, src, dst, 1.0,
+                               nullptr, 0.0, flag, pos);
+    if (r) return r;
+    for (int f = 0; f < nfields; ++f) src[f] = dst[f];
+  }
+  return 0;
+}
+
+int cgl_lincomb(void* stream, int64_t n, int nterms, const double* coef, const double* const* x, double* out,
+                const cgl_flag_t* flag, uint64_t pos) {
+  return pw_lincomb((cudaStream_t)stream, n, nterms, coef, x, out, flag, pos);
+}
+
+int cgl_eval_g(void* stream, int64_t n, const cgl_nonlinear_t* nl, int nfields, const double* const* in,
+               double in_scale, double* const* out, const cgl_flag_t* flag, uint64_t pos) {
+  return pw_eval_g((cudaStream_t)stream, n, nl, nfields, in, in_scale, out, flag, pos);
+}
+
+int cgl_cubic_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl, const double* in, double in_scale,
+                   double* out, cgl_flag_t* flag, uint64_t pos) {
+  return pw_exact_flow((cudaStream_t)stream, 0, n, t, nl, in, in_scale, out, flag, pos);
+}
+
+int cgl_quintic_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl, const double* in, double in_scale,
+                     double* out, cgl_flag_t* flag, uint64_t pos) {
+  return pw_exact_flow((cudaStream_t)stream, 1, n, t, nl, in, in_scale, out, flag, pos);
+}
+
+int cgl_rk4_flow(void* stream, int64_t n, double t, const cgl_nonlinear_t* nl, int nfields, const double* const* in,
+                 double in_scale, double* const* out, cgl_flag_t* flag, uint64_t pos) {
+  return pw_rk4_flow((cudaStream_t)stream, n, t, nl, nfields, in, in_scale, out, flag, pos);
+}
+
+int cgl_check_finite(void* stream, int64_t n, int nfields, const double* const* x, cgl_flag_t* flag, uint64_t pos) {
+  return pw_check_finite((cudaStream_t)stream, n, nfields, x, flag, pos);
+}
+
+int cgl_flag_reset(void* stream, cgl_flag_t* flag) { return pw_flag_reset((cudaStream_t)stream, flag); }
+
+int cgl_pointwise_mul(void* stream, int64_t n, const double* factor, const double* in, double* out,
+                      const cgl_flag_t* flag, uint64_t pos) {
+  return pw_mul((cudaStream_t)stream, n, factor, in, out, flag, pos);
+}
+
+int cgl_symbol_exp(void* stream, int64_t n, double s, const double* symbol, double* out) {
+  return pw_symexp((cudaStream_t)stream, n, s, symbol, out);
+}
+
+int cgl_separable_mul(void* stream, int ndim, const int64_t* shape, const double* const* tables, double in_scale,
+                      const double* in, double* out, const cgl_flag_t* flag, uint64_t pos) {
+  return pw_separable((cudaStream_t)stream, ndim, shape, tables, in_scale, in, out, flag, pos);
+}
+
+int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }
+int cgl_fft_exec(void* plan, void* stream, const double* in, double* out, int inverse) {
+  return fft_exec(plan, (cudaStream_t)stream, in, out, inverse);
+}
+int cgl_fft_destroy(void* plan) { return fft_destroy(plan); }
+
+}  // extern "C"

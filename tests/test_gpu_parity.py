@@ -1,0 +1,197 @@
+"""GPU parity: the sm_100a path against the reference's golden outputs (and
+the oracle), through the package's public API / the C ABI.
+
+Tolerances: single contractions <= 1e-13 relative max (test_tensors.py:53-97
+uses the same bar); full integrations <= 1e-10 relative L2 (BASELINE
+north_star); divergence step index and reason must match exactly.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from cases import gpu_problem, inputs
+from conftest import GOLDEN, rel_l2, rel_max
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(7,), (16,), (3, 5), (8, 6), (2, 9), (4, 4, 4), (3, 4, 5), (6, 2, 7), (2, 3, 2, 4), (3, 2, 2, 2)]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2403_02816_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("i", range(len(SHAPES)))
+def test_mode_product_tucker_kronsum(P, unit_golden, i):
+    from paper_2403_02816_b200 import tensors
+    g = unit_golden
+    u = g[f"mp{i}_u"]
+    for axis in range(u.ndim):
+        got = tensors.mu_mode_product(u, g[f"mp{i}_a{axis}_m"], axis)
+        assert got.shape == g[f"mp{i}_a{axis}_out"].shape
+        assert rel_max(got, g[f"mp{i}_a{axis}_out"]) <= 1e-13
+    mats = [g[f"tk{i}_m{a}"] for a in range(u.ndim)]
+    assert rel_max(tensors.tucker_apply(u, mats), g[f"tk{i}_out"]) <= 1e-13
+    assert rel_max(tensors.kron_sum_apply(u, mats), g[f"ks{i}_out"]) <= 1e-13
+
+
+def test_identity_factors_exact(P):
+    from paper_2403_02816_b200 import tensors
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((5, 6, 7)) + 1j * rng.standard_normal((5, 6, 7))
+    out = tensors.tucker_apply(u, [np.eye(5), np.eye(6), np.eye(7)])
+    assert np.array_equal(out, u)
+
+
+@pytest.mark.parametrize("m,n,k,batch", [(1, 1, 1, 1), (33, 17, 65, 3), (64, 64, 16, 1), (130, 70, 200, 2),
+                                         (512, 512, 512, 1), (5, 1000, 7, 4)])
+def test_zgemm_against_torch(P, m, n, k, batch):
+    """The DMMA GEMM vs a torch complex128 matmul (cuBLAS zgemm) with
+    alpha/beta epilogue, odd sizes exercising every tile edge."""
+    from paper_2403_02816_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(batch, m, k, dtype=torch.complex128, device="cuda", generator=g)
+    B = torch.randn(batch, k, n, dtype=torch.complex128, device="cuda", generator=g)
+    Y = torch.randn(batch, m, n, dtype=torch.complex128, device="cuda", generator=g)
+    C = torch.empty_like(Y)
+    al = 0.7 - 0.3j
+    rc = _lib.load().cgl_zgemm(_lib.stream(), m, n, k, _lib.ptr(A), k, m * k, _lib.ptr(B), n, k * n, _lib.ptr(C),
+                               n, m * n, batch, al.real, al.imag, _lib.ptr(Y), n, m * n, -0.5, None, 0)
+    _lib.check(rc, "zgemm")
+    want = al * (A @ B) - 0.5 * Y
+    err = (C - want).abs().max().item() / want.abs().max().item()
+    assert err <= 1e-14
+
+
+def test_flows_and_g(P, unit_golden):
+    from paper_2403_02816_b200 import flows
+    g = unit_golden
+    pts = g["flow_pts"]
+    CUBIC = P.CglParameters(alpha1=1.0, beta1=2.0, alpha2=1.0, alpha3=-1.0, beta3=0.2)
+    CQ = P.CglParameters(alpha1=0.5, beta1=0.5, alpha2=-0.5, alpha3=2.52, beta3=1.0, alpha4=-1.0, beta4=-0.11)
+    CP = P.CglParameters(alpha1=0.125, beta1=0.5, alpha2=-0.9, alpha0=-0.4, alpha3=1.0, beta3=0.8, alpha4=-0.1,
+                         beta4=-0.6, alpha5=0.5)
+    assert rel_max(flows.cubic_flow(pts, 0.3, CUBIC), g["cubic_flow"]) <= 1e-14
+    assert rel_max(flows.cubic_flow(pts, 0.02, CQ), g["cubic_flow_pos"]) <= 1e-14
+    assert rel_max(flows.quintic_flow(pts, 0.2, CQ), g["quintic_flow"]) <= 1e-14
+    assert rel_max(flows.eval_g(P.NonlinearSpec("cubic", CUBIC), (pts,))[0], g["g_cubic"]) <= 1e-14
+    assert rel_max(flows.eval_g(P.NonlinearSpec("cubic_quintic", CQ), (pts,))[0], g["g_cq"]) <= 1e-14
+    spec = P.NonlinearSpec("coupled_cubic_quintic", CP)
+    a, b = flows.eval_g(spec, (pts, pts[::-1].copy()))
+    assert rel_max(a, g["g_coupled_0"]) <= 1e-14 and rel_max(b, g["g_coupled_1"]) <= 1e-14
+    a, b = flows.rk4_flow(spec, (pts, pts[::-1].copy()), 0.1)
+    assert rel_max(a, g["rk4_coupled_0"]) <= 1e-14 and rel_max(b, g["rk4_coupled_1"]) <= 1e-14
+    assert rel_max(flows.rk4_flow(P.NonlinearSpec("cubic_quintic", CQ), (pts,), 0.05)[0], g["rk4_cq"]) <= 1e-14
+    with pytest.raises(P.DivergenceError) as e:
+        flows.cubic_flow(np.array([2.0 + 1.0j]), 0.1, CQ)
+    assert e.value.reason == "finite-time blow-up in cubic flow"
+    with pytest.raises(P.DivergenceError):
+        flows.quintic_flow(np.array([2.0 + 1.0j]), 1.0, P.CglParameters(alpha1=1.0, alpha4=1.0))
+    # alpha3 = 0 branch is a pure phase rotation (flows.py:92-93)
+    rot = flows.cubic_flow(pts, 0.4, P.CglParameters(alpha1=1.0, beta3=0.7))
+    assert rel_max(rot, pts * np.exp(1j * 0.7 * np.abs(pts) ** 2 * 0.4)) <= 1e-14
+
+
+def test_fft_conventions(P, unit_golden):
+    from paper_2403_02816_b200 import spectral
+    g = unit_golden
+    assert rel_max(spectral.dft_forward(g["fft_u"]), g["fft_out"]) <= 1e-14
+    assert rel_max(spectral.dft_inverse(g["fft_u"]), g["ifft_out"]) <= 1e-14
+
+
+def test_operator_protocol(P):
+    p = P.CglParameters(alpha1=1.0, beta1=2.0, alpha2=1.0)
+    op = P.build_fd_operator(p, (7, 6), (5.0, 4.0), "dirichlet")
+    u = np.random.default_rng(71).standard_normal((7, 6)) + 0j
+    with pytest.raises(RuntimeError):
+        op.exp_apply(1, u)
+    with pytest.raises(ValueError):
+        op.prepare(-1.0, [1])
+    with pytest.raises(ValueError):
+        op.prepare(0.1, [0])
+    op.prepare(0.08, [1, 0.5])
+    from cglsolve_free_kron import dense_expm_action
+    want = dense_expm_action(op.matrices, 0.08, u)
+    assert rel_max(op.exp_apply(1, u), want) <= 1e-11
+    half = op.exp_apply(0.5, op.exp_apply(0.5, u))
+    assert rel_max(half, op.exp_apply(1, u)) <= 1e-11
+
+
+def test_all_stepper_cases(P, stepper_golden):
+    meta, arrays = stepper_golden
+    for case in meta:
+        ic, want = inputs(case, arrays)
+        res = P.integrate(gpu_problem(case), case["scheme"], ic, case["t_final"], case["steps"])
+        assert res.diverged == case["diverged"], case["name"]
+        assert res.diverged_at == case["diverged_at"], case["name"]
+        assert res.reason == case["reason"], case["name"]
+        for got, w in zip(res.fields, want):
+            fin = np.isfinite(w)
+            assert np.array_equal(np.isfinite(got), fin), case["name"]
+            if fin.any():
+                assert rel_l2(got[fin], w[fin]) <= 1e-10, case["name"]
+
+
+def test_device_tensors_in_device_tensors_out(P, stepper_golden):
+    meta, arrays = stepper_golden
+    case = next(c for c in meta if c["name"] == "fd2d_dir4_cubic_if4")
+    ic, want = inputs(case, arrays)
+    res = P.integrate(gpu_problem(case), "if4", [torch.from_numpy(x).cuda() for x in ic], case["t_final"],
+                      case["steps"])
+    assert isinstance(res.fields[0], torch.Tensor) and res.fields[0].is_cuda
+    assert rel_l2(res.fields[0].cpu().numpy(), want[0]) <= 1e-10
+
+
+def test_snapshots_and_determinism(P, stepper_golden):
+    meta, arrays = stepper_golden
+    case = next(c for c in meta if c["name"] == "four2d_cubic_strang")
+    ic, _ = inputs(case, arrays)
+    seen = []
+    a = P.integrate(gpu_problem(case), "strang", ic, 1.0, 10, snapshot_steps=(3, 7, 10),
+                    on_snapshot=lambda k, t, f: seen.append((k, t)))
+    assert [k for k, _ in seen] == [3, 7, 10]
+    assert seen[-1][1] == pytest.approx(1.0, abs=1e-12)
+    b = P.integrate(gpu_problem(case), "strang", ic, 1.0, 10)
+    assert np.array_equal(a.fields[0], b.fields[0])
+
+
+def _workload_run(P, tag, meta):
+    from paper_2403_02816_b200 import workloads as W
+    m = meta[tag]
+    w = W.CONFIGS[m["workload"].split("-")[0]]
+    if "@" in m["workload"]:
+        w = w.scaled(m["extents"][0], m["steps"])
+    prob = W.build_problem(w)
+    x0 = W.state_for_problem(w, W.initial_state(w))
+    return P.integrate(prob, m["scheme"], (x0,), w.t_final, w.steps), m
+
+
+@pytest.mark.parametrize("tag", ["C0_strang", "C1s64_if4", "C1s64_rk4", "C2s24_split4", "C3s32_if4",
+                                 "C3s32_strang", "C4s24_if4"])
+def test_baseline_config_cases(P, config_golden, tag):
+    meta, arrays = config_golden
+    res, m = _workload_run(P, tag, meta)
+    assert res.diverged == m["diverged"] and res.diverged_at == m["diverged_at"]
+    assert rel_l2(res.fields[0], arrays[f"{tag}_out"]) <= 1e-10
+
+
+@pytest.mark.parametrize("scheme", ["if4", "strang", "rk4"])
+def test_c1_full_size(P, config_golden, scheme):
+    """BASELINE config 1 at full size (512^2, 400 steps) vs the reference."""
+    tag = f"C1_{scheme}"
+    path = os.path.join(GOLDEN, f"{tag}_out.npy")
+    meta, _ = config_golden
+    if tag not in meta or not os.path.exists(path):
+        pytest.skip("C1 fixtures not generated")
+    want = np.load(path)
+    res, m = _workload_run(P, tag, meta)
+    assert res.diverged == m["diverged"] and res.diverged_at == m["diverged_at"] and res.reason == m["reason"]
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(res.fields[0]), fin)
+    assert rel_l2(res.fields[0][fin], want[fin]) <= 1e-10
