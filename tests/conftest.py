@@ -57,9 +57,12 @@ def config_golden():
 
 
 def rel_l2(a, b):
-    a = np.asarray(a)
-    b = np.asarray(b)
-    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+    """||a - b||_2 / ||b||_2, scaled first so huge-but-finite states do not overflow."""
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    s = float(np.max(np.abs(b))) if b.size else 1.0
+    s = s if s > 0 and np.isfinite(s) else 1.0
+    return float(np.linalg.norm(a / s - b / s) / np.linalg.norm(b / s))
 
 
 def rel_max(a, b):

@@ -194,4 +194,5 @@ def test_c1_full_size(P, config_golden, scheme):
     assert res.diverged == m["diverged"] and res.diverged_at == m["diverged_at"] and res.reason == m["reason"]
     fin = np.isfinite(want)
     assert np.array_equal(np.isfinite(res.fields[0]), fin)
-    assert rel_l2(res.fields[0][fin], want[fin]) <= 1e-10
+    if fin.any():
+        assert rel_l2(res.fields[0][fin], want[fin]) <= 1e-10
