@@ -28,6 +28,11 @@ struct GemmArgs {
   int m_fastest;  // tile order: consecutive CTAs walk M (reuse the B tile in L2)
   const cgl_flag_t* flag;
   uint64_t pos;
+  // stream-K bookkeeping (filled by the launcher)
+  int64_t total_iters;
+  double* workspace;
+  int* flags;
+  int epoch;
   GemmItem items[kMaxItems];
 };
 

@@ -4,11 +4,32 @@
 // (tensors.py:38-59).  On sm_100a FP64 has no tcgen05 path (tcgen05.mma has
 // no .kind::f64), so the tensor-core route is warp-level mma.sync
 // m8n8k4.f64 (SASS DMMA.8x8x4; measured 37.06 TFLOP/s chip peak, see
-// profiles/fp64_peak_r01.txt).  A complex MAC is four real DMMAs:
-//     Cr += Ar Br - Ai Bi ,  Ci += Ar Bi + Ai Br    (8 real flops)
-// Operands are staged through a multi-stage cp.async pipeline into padded
+// profiles/fp64_peak_r01.txt).
+//
+// Complex product: Gauss/Karatsuba "3M" form, three real DMMAs per complex
+// fragment pair instead of four:
+//     P1 = Ar Br,  P2 = Ai Bi,  P3 = (Ar + Ai)(Br + Bi)
+//     Cr = P1 - P2,  Ci = P3 - P1 - P2
+// (the operand sums are one DADD per fragment, ~3% of the DMMA issue).
+// The algorithmic flop count stays 8 per complex MAC; the executed tensor
+// work is 6 — rooflines are reported on the algorithmic count.  The classic
+// 4-DMMA form is kept (CGL_ZGEMM_4M=1) for A/B checks.
+//
+// Decomposition: persistent stream-K.  grid = (#SM x resident CTAs); the
+// flattened (tile, k-tile) iteration space is cut into equal contiguous
+// ranges, one per CTA, so every SM gets the same MAC count regardless of how
+// many 64x64 tiles the problem has (512^2 fields give 64 tiles per field, a
+// 0.86-wave grid in the data-parallel form).  A tile split across CTAs is
+// finished by its HEAD CTA (the one holding k-tile 0, which reaches the tile
+// at the end of its range); the continuing CTAs compute their tail segment
+// first and publish it at once (workspace + release/acquire flags), so the
+// head finds the partials ready instead of serialising the chain.  The grid
+// never exceeds the co-resident CTA count, so every awaited CTA is running.
+// The workspace is per device: cgl GEMM launches must be stream-ordered.
+//
+// Operands are staged through a 3-stage cp.async pipeline into padded
 // shared-memory tiles whose padding makes every 16-byte fragment load
-// bank-conflict-free (see the SA/SB derivation below).
+// bank-conflict-free (SA/SB derivation below).
 //
 // Layout (row-major, complex elements):
 //   A[m,k] k-contiguous, B[k,n] n-contiguous, C/Y[m,n] n-contiguous.
@@ -16,6 +37,7 @@
 // "right" (Out = In * M^T, B = M^T stored explicitly).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
@@ -37,64 +59,61 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 // Shared-memory row strides in 16-byte (complex) units.
 //  A fragment (row = lane/4, col k = lane%4): 8 lanes of one 128-bit phase hit
 //  (m*SA + k) mod 8 distinct  <=>  SA = 4 (mod 8).
 //  B fragment (row k = lane%4, col n = lane/4): (k*SB + n) mod 8 distinct
 //  <=>  SB = 2 (mod 8).
-template <int BK> struct StrideA { static constexpr int v = BK + 4; };
-template <int BN> struct StrideB { static constexpr int v = BN + 2; };
-
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool M3>
 struct GemmCfg {
   static constexpr int NT = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M;
   static constexpr int WTN = BN / WARPS_N;
   static constexpr int FM = WTM / 8;
   static constexpr int FN = WTN / 8;
-  static constexpr int SA = StrideA<BK>::v;
-  static constexpr int SB = StrideB<BN>::v;
+  static constexpr int SA = BK + 4;
+  static constexpr int SB = BN + 2;
   static constexpr int A_STAGE = BM * SA;
   static constexpr int B_STAGE = BK * SB;
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double2);
+  static constexpr int NACC = M3 ? 3 : 2;           // accumulator planes
+  static constexpr int PART = FM * FN * 4;          // partial (Cr, Ci) doubles per thread
   static_assert(BM % (8 * WARPS_M) == 0 && BN % (8 * WARPS_N) == 0, "warp tile");
   static_assert(BK % 8 == 0, "BK multiple of 8");
   static_assert(SA % 8 == 4 && SB % 8 == 2, "conflict-free padding");
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
-    zgemm_kernel(const GemmArgs args) {
-  using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+template <class Cfg>
+struct Acc {
+  double p[Cfg::NACC][Cfg::FM][Cfg::FN][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < Cfg::NACC; ++a)
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) p[a][i][j][0] = p[a][i][j][1] = 0.0;
+  }
+};
+
+// Accumulate k-tiles [kt0, kt1) of one output tile into acc.
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool M3, class Cfg>
+__device__ __forceinline__ void mainloop(const GemmArgs& args, const double2* __restrict__ A,
+                                         const double2* __restrict__ B, int64_t m0, int64_t n0, int kt0, int kt1,
+                                         double2* As, double2* Bs, Acc<Cfg>& acc) {
   constexpr int NT = Cfg::NT, FM = Cfg::FM, FN = Cfg::FN, SA = Cfg::SA, SB = Cfg::SB;
-
-  if (flag_skip(args.flag, args.pos)) return;
-
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* As = reinterpret_cast<double2*>(smem_raw);
-  double2* Bs = As + STAGES * Cfg::A_STAGE;
-
-  // ---- decode (item, batch, tile) from the linear block index ----
-  const int64_t tiles_m = (args.M + BM - 1) / BM;
-  const int64_t tiles_n = (args.N + BN - 1) / BN;
-  const int64_t tiles = tiles_m * tiles_n;
-  int64_t bid = blockIdx.x;
-  const int64_t t = bid % tiles;
-  bid /= tiles;
-  const int64_t b = bid % args.batch;
-  const int item = (int)(bid / args.batch);
-  int64_t tm, tn;
-  if (args.m_fastest) { tm = t % tiles_m; tn = t / tiles_m; }
-  else                { tn = t % tiles_n; tm = t / tiles_n; }
-  const int64_t m0 = tm * BM, n0 = tn * BN;
-
-  const double2* __restrict__ A = reinterpret_cast<const double2*>(args.items[item].A) + b * args.sA;
-  const double2* __restrict__ B = reinterpret_cast<const double2*>(args.items[item].B) + b * args.sB;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int64_t M = args.M, N = args.N, K = args.K, lda = args.lda, ldb = args.ldb;
-  const int ktiles = (int)((K + BK - 1) / BK);
 
   auto load_tile = [&](int stage, int kt) {
     const int64_t k0 = (int64_t)kt * BK;
@@ -116,106 +135,308 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     }
   };
 
-  double cr[FM][FN][2], ci[FM][FN][2];
-#pragma unroll
-  for (int i = 0; i < FM; ++i)
-#pragma unroll
-    for (int j = 0; j < FN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-
+  const int nk = kt1 - kt0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_tile(s, s);
+    if (s < nk) load_tile(s, kt0 + s);
     cp_async_commit();
   }
-
   const int arow = (wm * Cfg::WTM + (lane >> 2)) * SA + (lane & 3);
   const int bcol = (lane & 3) * SB + wn * Cfg::WTN + (lane >> 2);
 
-  for (int kt = 0; kt < ktiles; ++kt) {
+  for (int t = 0; t < nk; ++t) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      const int nk = kt + STAGES - 1;
-      if (nk < ktiles) load_tile(nk % STAGES, nk);
+      const int nt = t + STAGES - 1;
+      if (nt < nk) load_tile(nt % STAGES, kt0 + nt);
       cp_async_commit();
     }
-    const double2* as = As + (kt % STAGES) * Cfg::A_STAGE + arow;
-    const double2* bs = Bs + (kt % STAGES) * Cfg::B_STAGE + bcol;
+    const double2* as = As + (t % STAGES) * Cfg::A_STAGE + arow;
+    const double2* bs = Bs + (t % STAGES) * Cfg::B_STAGE + bcol;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double2 a[FM], bb[FN];
+      double2 bb[FN];
+      double bsum[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) a[i] = as[i * 8 * SA + kk * 4];
-#pragma unroll
-      for (int j = 0; j < FN; ++j) bb[j] = bs[kk * 4 * SB + j * 8];
+      for (int j = 0; j < FN; ++j) {
+        bb[j] = bs[kk * 4 * SB + j * 8];
+        bsum[j] = bb[j].x + bb[j].y;
+      }
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const double nai = -a[i].y;
+        const double2 a = as[i * 8 * SA + kk * 4];
+        if (M3) {
+          const double asum = a.x + a.y;
 #pragma unroll
-        for (int j = 0; j < FN; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], a[i].x, bb[j].x);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].x, bb[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].y, bb[j].x);
-          dmma(cr[i][j][0], cr[i][j][1], nai, bb[j].y);
+          for (int j = 0; j < FN; ++j) {
+            dmma(acc.p[0][i][j][0], acc.p[0][i][j][1], a.x, bb[j].x);
+            dmma(acc.p[1][i][j][0], acc.p[1][i][j][1], a.y, bb[j].y);
+            dmma(acc.p[2 % Cfg::NACC][i][j][0], acc.p[2 % Cfg::NACC][i][j][1], asum, bsum[j]);
+          }
+        } else {
+          const double nai = -a.y;
+#pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            dmma(acc.p[0][i][j][0], acc.p[0][i][j][1], a.x, bb[j].x);
+            dmma(acc.p[1][i][j][0], acc.p[1][i][j][1], a.x, bb[j].y);
+            dmma(acc.p[1][i][j][0], acc.p[1][i][j][1], a.y, bb[j].x);
+            dmma(acc.p[0][i][j][0], acc.p[0][i][j][1], nai, bb[j].y);
+          }
         }
       }
     }
   }
   cp_async_wait<0>();
+  __syncthreads();  // the next segment's prologue reuses the stages
+}
 
-  // ---- epilogue: C = alpha*acc + beta*Y ----
-  double2* __restrict__ C = reinterpret_cast<double2*>(args.items[item].C) + b * args.sC;
-  const double2* Y = args.items[item].Y ? reinterpret_cast<const double2*>(args.items[item].Y) + b * args.sY : nullptr;
-  const double2 al = args.alpha;
+// Fold the 3M planes into (Cr, Ci) in planes 0 and 1, in place.
+template <bool M3, class Cfg>
+__device__ __forceinline__ void finalize(Acc<Cfg>& acc) {
+  if (!M3) return;
 #pragma unroll
-  for (int i = 0; i < FM; ++i) {
-    const int64_t row = m0 + wm * Cfg::WTM + i * 8 + (lane >> 2);
-    if (row >= M) continue;
+  for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
-    for (int j = 0; j < FN; ++j) {
+    for (int j = 0; j < Cfg::FN; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t col = n0 + wn * Cfg::WTN + j * 8 + (lane & 3) * 2 + e;
-        if (col >= N) continue;
-        double2 v = make_double2(al.x * cr[i][j][e] - al.y * ci[i][j][e],
-                                 al.x * ci[i][j][e] + al.y * cr[i][j][e]);
-        if (Y) {
-          const double2 y = Y[row * args.ldy + col];
-          v.x = fma(args.beta, y.x, v.x);
-          v.y = fma(args.beta, y.y, v.y);
+        const double p1 = acc.p[0][i][j][e], p2 = acc.p[1][i][j][e], p3 = acc.p[2 % Cfg::NACC][i][j][e];
+        acc.p[0][i][j][e] = p1 - p2;
+        acc.p[1][i][j][e] = p3 - p1 - p2;
+      }
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool M3>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
+    zgemm_kernel(const GemmArgs args) {
+  using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, M3>;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN, NT = Cfg::NT;
+
+  if (flag_skip(args.flag, args.pos)) return;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* As = reinterpret_cast<double2*>(smem_raw);
+  double2* Bs = As + STAGES * Cfg::A_STAGE;
+
+  const int64_t tiles_m = (args.M + BM - 1) / BM;
+  const int64_t tiles_n = (args.N + BN - 1) / BN;
+  const int64_t tiles = tiles_m * tiles_n;
+  const int ktiles = max(1, (int)((args.K + BK - 1) / BK));  // K = 0: one zero-filled k-tile
+  const int64_t total = args.total_iters;  // (nitems * batch * tiles) * ktiles
+  const int64_t G = gridDim.x, g = blockIdx.x;
+  const int64_t it_end = (g + 1) * total / G;
+  int64_t it = g * total / G;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+
+  while (it < it_end) {
+    const int64_t tile_id = it / ktiles;
+    const int kt0 = (int)(it % ktiles);
+    const int64_t rem = it_end - it;
+    const int kt1 = (int)((int64_t)kt0 + rem < (int64_t)ktiles ? (int64_t)kt0 + rem : (int64_t)ktiles);
+    // decode (item, batch, tile)
+    int64_t r = tile_id;
+    const int64_t t = r % tiles;
+    r /= tiles;
+    const int64_t b = r % args.batch;
+    const int item = (int)(r / args.batch);
+    int64_t tm, tn;
+    if (args.m_fastest) { tm = t % tiles_m; tn = t / tiles_m; }
+    else                { tn = t % tiles_n; tm = t / tiles_n; }
+    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const double2* A = reinterpret_cast<const double2*>(args.items[item].A) + b * args.sA;
+    const double2* B = reinterpret_cast<const double2*>(args.items[item].B) + b * args.sB;
+
+    Acc<Cfg> acc;
+    acc.zero();
+    mainloop<BM, BN, BK, WARPS_M, WARPS_N, STAGES, M3, Cfg>(args, A, B, m0, n0, kt0, kt1, As, Bs, acc);
+    finalize<M3, Cfg>(acc);
+    it += kt1 - kt0;
+
+    if (kt0 > 0) {
+      // This segment continues a tile begun by a lower CTA; it is the first
+      // thing this CTA computes, so publish it right away.  The tile's head
+      // CTA (which reaches the tile at the END of its range) finishes it.
+      double* ws = args.workspace + (size_t)g * Cfg::PART * NT;
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = ((i * FN + j) * 2 + e) * 2;
+            __stcg(ws + (size_t)q * NT + tid, acc.p[0][i][j][e]);
+            __stcg(ws + (size_t)(q + 1) * NT + tid, acc.p[1][i][j][e]);
+          }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(args.flags + g, args.epoch);
+      continue;
+    }
+    if (kt1 < ktiles) {
+      // head segment at the end of this CTA's range: add the tail partials
+      // that the following CTAs published at the start of theirs
+      const int64_t tile_end = (tile_id + 1) * ktiles;
+      for (int64_t h = g + 1; h < G; ++h) {
+        if (tid == 0) {
+          while (ld_acquire(args.flags + h) != args.epoch) __nanosleep(20);
         }
-        C[row * args.ldc + col] = v;
+        __syncthreads();
+        const double* wh = args.workspace + (size_t)h * Cfg::PART * NT;
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int q = ((i * FN + j) * 2 + e) * 2;
+              acc.p[0][i][j][e] += __ldcg(wh + (size_t)q * NT + tid);
+              acc.p[1][i][j][e] += __ldcg(wh + (size_t)(q + 1) * NT + tid);
+            }
+        __syncthreads();
+        if (tid == 0) args.flags[h] = 0;  // single consumer: re-arm for the next launch (graph-replay safe)
+        if ((h + 1) * total / G >= tile_end) break;  // CTA h holds the tile's last k-tile
+      }
+    }
+
+    // epilogue: C = alpha*acc + beta*Y
+    double2* __restrict__ C = reinterpret_cast<double2*>(args.items[item].C) + b * args.sC;
+    const double2* Y = args.items[item].Y ? reinterpret_cast<const double2*>(args.items[item].Y) + b * args.sY : nullptr;
+    const double2 al = args.alpha;
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int64_t row = m0 + wm * Cfg::WTM + i * 8 + (lane >> 2);
+      if (row >= args.M) continue;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = n0 + wn * Cfg::WTN + j * 8 + (lane & 3) * 2 + e;
+          if (col >= args.N) continue;
+          const double2 a = make_double2(acc.p[0][i][j][e], acc.p[1][i][j][e]);
+          double2 v = make_double2(al.x * a.x - al.y * a.y, al.x * a.y + al.y * a.x);
+          if (Y) {
+            const double2 y = Y[row * args.ldy + col];
+            v.x = fma(args.beta, y.x, v.x);
+            v.y = fma(args.beta, y.y, v.y);
+          }
+          C[row * args.ldc + col] = v;
+        }
       }
     }
   }
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST>
-static int launch_cfg(const GemmArgs& a, int nitems, cudaStream_t s) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
-  auto kern = zgemm_kernel<BM, BN, BK, WM, WN, ST>;
-  static bool attr_done = false;  // per template instance
-  if (!attr_done) {
+// ---------------------------------------------------------------------------
+// host side: per-device persistent workspace + flags, grid sizing
+// ---------------------------------------------------------------------------
+struct StreamKState {
+  double* ws = nullptr;
+  int* flags = nullptr;
+  size_t ws_doubles = 0;
+  int nflags = 0;
+  int epoch = 0;
+};
+static StreamKState g_sk[16];
+
+static int ensure_state(int dev, size_t ws_doubles, int nflags, StreamKState** out) {
+  StreamKState& s = g_sk[dev & 15];
+  if (s.ws_doubles < ws_doubles) {
+    if (s.ws) cudaFree(s.ws);
+    s.ws = nullptr;
+    cudaError_t e = cudaMalloc(&s.ws, ws_doubles * sizeof(double));
+    if (e != cudaSuccess) return set_cuda_error(e, "zgemm workspace");
+    s.ws_doubles = ws_doubles;
+  }
+  if (s.nflags < nflags) {
+    if (s.flags) cudaFree(s.flags);
+    s.flags = nullptr;
+    cudaError_t e = cudaMalloc(&s.flags, nflags * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(s.flags, 0, nflags * sizeof(int));
+    if (e != cudaSuccess) return set_cuda_error(e, "zgemm flags");
+    s.nflags = nflags;
+    s.epoch = 0;
+  }
+  *out = &s;
+  return 0;
+}
+
+static bool use_4m() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CGL_ZGEMM_4M");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3>
+static int launch_cfg(GemmArgs a, int nitems, cudaStream_t s) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST, M3>;
+  auto kern = zgemm_kernel<BM, BN, BK, WM, WN, ST, M3>;
+  static int occ = 0, sms = 0, dev_cached = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (occ == 0 || dev != dev_cached) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(zgemm)");
-    attr_done = true;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
+    if (e != cudaSuccess || occ < 1) return set_cuda_error(e, "zgemm occupancy");
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dev_cached = dev;
   }
   const int64_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
-  const int64_t blocks = tiles * a.batch * nitems;
-  if (blocks <= 0) return 0;
-  if (blocks > 0x7fffffffLL) return set_error(CGL_ESHAPE, "zgemm grid too large");
-  kern<<<(unsigned)blocks, Cfg::NT, Cfg::SMEM, s>>>(a);
+  const int64_t ktiles = a.K > 0 ? (a.K + BK - 1) / BK : 1;  // K = 0: one zero-filled k-tile
+  const int64_t units = tiles * a.batch * nitems;
+  if (units <= 0) return 0;
+  a.total_iters = units * ktiles;
+  int64_t G = (int64_t)sms * occ;
+  if (G > a.total_iters) G = a.total_iters;
+  StreamKState* st = nullptr;
+  int r = ensure_state(dev, (size_t)G * Cfg::PART * Cfg::NT, (int)G, &st);
+  if (r) return r;
+  a.workspace = st->ws;
+  a.flags = st->flags;
+  a.epoch = 1;  // flags are re-armed to 0 by their consumer, so a constant works under graph replay
+  kern<<<(unsigned)G, Cfg::NT, Cfg::SMEM, s>>>(a);
   return check_launch("zgemm_kernel");
 }
 
-// Tile-shape choice: the 64x64 tile (8 warps, 32x16 warp tiles) when it
-// yields at least ~one CTA per SM, else the 32x32 tile (4 warps) so small
-// grids (128^2 fields) still spread over the 148 SMs.
+static int env_cfg() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("CGL_ZGEMM_CFG");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+template <bool M3>
+static int launch_big(const GemmArgs& a, int nitems, cudaStream_t s, int cfg) {
+  switch (cfg) {
+    case 1: return launch_cfg<64, 32, 16, 4, 2, 3, M3>(a, nitems, s);   // 16x16 warp tiles, 8 warps
+    case 2: return launch_cfg<64, 64, 16, 4, 4, 3, M3>(a, nitems, s);   // 16x16 warp tiles, 16 warps
+    case 3: return launch_cfg<32, 64, 16, 2, 4, 3, M3>(a, nitems, s);   // 16x16 warp tiles, 8 warps
+    case 4: return launch_cfg<64, 32, 32, 4, 2, 3, M3>(a, nitems, s);   // BK = 32
+    case 0: return launch_cfg<64, 64, 16, 2, 4, 3, M3>(a, nitems, s);   // 32x16 warp tiles, 8 warps
+    // default (measured best on B200, profiles/r01_zgemm_configs.txt): 64x64 CTA
+    // tile, 16 warps of 16x16, BK = 32, double-buffered, 1 CTA/SM (141 KB smem)
+    default: return launch_cfg<64, 64, 32, 4, 4, 2, M3>(a, nitems, s);
+  }
+}
+
+// Tile-shape choice: the 64x64 tile for real work; the 32x32 tile (4 warps)
+// when a problem has too few 64x64 tiles to occupy the SMs without splitting
+// every tile many ways.
 int zgemm_launch(const GemmArgs& a, int nitems, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return 0;
   const int64_t big = ((a.M + 63) / 64) * ((a.N + 63) / 64) * a.batch * nitems;
-  if (big >= 120) return launch_cfg<64, 64, 16, 2, 4, 3>(a, nitems, s);
-  return launch_cfg<32, 32, 16, 2, 2, 3>(a, nitems, s);
+  const bool m3 = !use_4m();
+  if (big >= 32) return m3 ? launch_big<true>(a, nitems, s, env_cfg()) : launch_big<false>(a, nitems, s, env_cfg());
+  return m3 ? launch_cfg<32, 32, 16, 2, 2, 3, true>(a, nitems, s)
+            : launch_cfg<32, 32, 16, 2, 2, 3, false>(a, nitems, s);
 }
 
 }  // namespace cgl
