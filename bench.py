@@ -233,9 +233,13 @@ def gemm_roofline(torch, w, scheme_fields=4):
     flops = sum(f for f, _ in res.values())
     dt = sum(t for _, t in res.values())
     achieved = flops / dt / 1e12
+    m3 = os.environ.get("CGL_ZGEMM_4M", "0") != "1"
     return {"bound": "tensor", "achieved": achieved, "peak": best, "unit": "TFLOP/s", "frac": achieved / best,
             "traffic": None,
-            "kernel": "zgemm_kernel<64,64,16> (DMMA.8x8x4), 4-field batched mode products of the if4 step",
+            "kernel": "zgemm_kernel<64,64,32,4,4,2,3M> (DMMA.8x8x4, stream-K), 4-field batched mode products "
+                      "of the if4 step (M=N=K=512 per field)",
+            "complex_product": "3M (3 DMMA per complex MAC)" if m3 else "4M",
+            "executed_dmma_frac": achieved * (0.75 if m3 else 1.0) / best,
             "per_launch_ms": {f"mode{a + 1}": 1e3 * t for a, (_, t) in res.items()},
             "algorithmic_flops_per_launch": {f"mode{a + 1}": f for a, (f, _) in res.items()},
             "peak_source": f"cgl_probe_dmma live in this run (recorded {FP64_PEAK_RECORDED} TFLOP/s, "
