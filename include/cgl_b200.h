@@ -33,11 +33,22 @@ extern "C" {
 #define CGL_ESHAPE (-2)
 #define CGL_ECUFFT (-3)
 
-/* Sticky divergence record in device memory (8 bytes, init all-ones).
+/* Sticky divergence record + device step counter (24 bytes, device memory).
  * key = (step << 24) | (seq << 8) | reason, atomically min-reduced, so it
  * holds the first (step, call) that failed; mirrors DivergenceError(reason)
- * + diverged_at of integrators.py:264-278 and flows.py:32-39,95-132. */
-typedef struct cgl_flag_t { unsigned long long key; } cgl_flag_t;
+ * + diverged_at of integrators.py:264-278 and flows.py:32-39,95-132.
+ * Init: key = all ones, step = first step number, done = 0.
+ * A `pos` argument with CGL_POS_DEVICE set takes its step from `step`
+ * (low 24 bits = seq << 8), so a captured CUDA graph of a step can replay;
+ * "end-of-step" stage kernels advance `step` once all their CTAs are done. */
+typedef struct cgl_flag_t {
+  unsigned long long key;
+  unsigned long long step;
+  unsigned int done;
+  unsigned int reserved;
+} cgl_flag_t;
+
+#define CGL_POS_DEVICE (1ull << 63)
 
 enum cgl_reason {
   CGL_BLOWUP_CUBIC = 0,      /* flows.py:95-96  "finite-time blow-up in cubic flow" */
@@ -145,6 +156,30 @@ int cgl_check_finite(void* stream, int64_t n, int nfields,
                      const double* const* x, cgl_flag_t* flag, uint64_t pos);
 
 int cgl_flag_reset(void* stream, cgl_flag_t* flag);
+
+/* ---- fused per-scheme stage kernels (csrc/stages.cu) -------------------- */
+enum cgl_stage_program {
+  CGL_STAGE_IF4_PRE = 0,    /* in u            -> out X1, X5           */
+  CGL_STAGE_IF4_MID = 1,    /* in u2, a        -> out g3, s            */
+  CGL_STAGE_IF4_END = 2,    /* in b, c, d, e   -> out u', X1', X5'     */
+  CGL_STAGE_FLOW1 = 3,      /* in u            -> out v                */
+  CGL_STAGE_FLOW2 = 4,      /* in u            -> out v, f             */
+  CGL_STAGE_SPLIT4_MID = 5, /* in v, f         -> out c, f'            */
+  CGL_STAGE_SPLIT4_END = 6, /* in f, c         -> out u', v', f'       */
+  CGL_STAGE_STRANG_END = 7, /* in w            -> out u', v'           */
+  CGL_STAGE_IF2_PRE = 8,    /* in u            -> out X, Y             */
+  CGL_STAGE_IF2_END = 9     /* in u2, o        -> out u', X', Y'       */
+};
+/* One fused pass of a step body (integrators.py:146-215): see the program
+ * table in csrc/stages.cu.  in/out: (#operands x nfields) pointers, operand
+ * major.  *_END programs check finiteness, run the next step's prologue and
+ * advance flag->step; positions come from flag->step when pos has
+ * CGL_POS_DEVICE set (CUDA-graph replay), else from pos >> 24.  in/out may
+ * alias elementwise (each point is read before it is written). */
+int cgl_stage(void* stream, int program, int nfields, int64_t n,
+              const cgl_nonlinear_t* nl, double tau, double in_scale,
+              const double* const* in, double* const* out,
+              cgl_flag_t* flag, uint64_t pos);
 
 /* Hadamard product out = factor .* in (spectral.py:123-129). */
 int cgl_pointwise_mul(void* stream, int64_t n, const double* factor,

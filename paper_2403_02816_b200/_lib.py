@@ -34,6 +34,18 @@ REASONS = {
 }
 NONFINITE_STATE = 5
 NO_DIVERGENCE = (1 << 64) - 1
+POS_DEVICE = 1 << 63
+
+STAGE = {"if4_pre": 0, "if4_mid": 1, "if4_end": 2, "flow1": 3, "flow2": 4, "split4_mid": 5,
+         "split4_end": 6, "strang_end": 7, "if2_pre": 8, "if2_end": 9}
+
+
+def new_flag(first_step=1):
+    """Device flag record (cgl_flag_t): key = all ones, step, done = 0."""
+    f = torch.zeros(3, dtype=torch.int64, device="cuda")
+    f[0] = -1
+    f[1] = first_step
+    return f
 
 KIND_CODES = {"cubic": 0, "cubic_quintic": 1, "coupled_cubic_quintic": 2}
 
@@ -64,6 +76,7 @@ _SIGS = {
     "cgl_rk4_flow": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_int, c_ptr, c_dbl, c_ptr, c_ptr, c_u64]),
     "cgl_check_finite": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr, c_u64]),
     "cgl_flag_reset": (c_int, [c_ptr, c_ptr]),
+    "cgl_stage": (c_int, [c_ptr, c_int, c_int, c_i64, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_pointwise_mul": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_symbol_exp": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr]),
     "cgl_separable_mul": (c_int, [c_ptr, c_int, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),

@@ -26,6 +26,8 @@ int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double
 int fft_plan(int, const int64_t*, void**);
 int fft_exec(void*, cudaStream_t, const double*, double*, int);
 int fft_destroy(void*);
+int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
+                 double* const*, cgl_flag_t*, uint64_t);
 
 static thread_local std::string g_err;
 static unsigned long long g_launches = 0;
@@ -245,6 +247,11 @@ int cgl_symbol_exp(void* stream, int64_t n, double s, const double* symbol, doub
 int cgl_separable_mul(void* stream, int ndim, const int64_t* shape, const double* const* tables, double in_scale,
                       const double* in, double* out, const cgl_flag_t* flag, uint64_t pos) {
   return pw_separable((cudaStream_t)stream, ndim, shape, tables, in_scale, in, out, flag, pos);
+}
+
+int cgl_stage(void* stream, int program, int nfields, int64_t n, const cgl_nonlinear_t* nl, double tau,
+              double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
+  return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos);
 }
 
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }

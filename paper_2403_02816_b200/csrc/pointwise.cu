@@ -55,6 +55,7 @@ struct LinArgs {
 };
 
 __global__ void lincomb_kernel(int64_t n, LinArgs a, double2* out, const cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double2 acc = cscale(a.c[0], ld2(a.x[0] + i));
@@ -66,6 +67,7 @@ __global__ void lincomb_kernel(int64_t n, LinArgs a, double2* out, const cgl_fla
 template <int NF>
 __global__ void eval_g_kernel(int64_t n, NL p, const double2* in0, const double2* in1, double s,
                               double2* out0, double2* out1, const cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double2 u[NF], g[NF];
@@ -82,6 +84,7 @@ __global__ void eval_g_kernel(int64_t n, NL p, const double2* in0, const double2
 template <int Q>
 __global__ void exact_flow_kernel(int64_t n, double t, double a, double b, const double2* in, double s,
                                   double2* out, cgl_flag_t* flag, uint64_t pos, unsigned r_blow, unsigned r_nonfinite) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool blow = false, bad = false;
   const bool phase_only = fabs(a) < kRealCoeffFloor;
@@ -112,6 +115,7 @@ __global__ void exact_flow_kernel(int64_t n, double t, double a, double b, const
 template <int NF>
 __global__ void rk4_flow_kernel(int64_t n, double t, NL p, const double2* in0, const double2* in1, double s,
                                 double2* out0, double2* out1, cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool bad = false;
   const double h = 0.5 * t, t6 = t / 6.0;
@@ -143,6 +147,7 @@ __global__ void rk4_flow_kernel(int64_t n, double t, NL p, const double2* in0, c
 struct FinArgs { const double2* x[4]; int nf; };
 
 __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -153,6 +158,7 @@ __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint
 __global__ void flag_reset_kernel(cgl_flag_t* f) { f->key = ~0ull; }
 
 __global__ void mul_kernel(int64_t n, const double2* f, const double2* in, double2* out, const cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = cmul(ld2(f + i), ld2(in + i));
@@ -174,6 +180,7 @@ struct SepArgs {
 // out[j] = s * prod_mu tab_mu[j_mu] * in[j] (C order: last axis fastest)
 __global__ void separable_kernel(int64_t n, SepArgs a, double s, const double2* in, double2* out,
                                  const cgl_flag_t* flag, uint64_t pos) {
+  pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i;

@@ -1,0 +1,293 @@
+// Fused per-scheme stage kernels: every pointwise piece of a time step
+// between two exponential (Tucker / Fourier-multiplier) applications runs as
+// ONE pass over the grid, reading each operand once and writing each result
+// once, with the nonlinearity, the exact / RK4 substep flows, the stage
+// combination, the end-of-step finiteness check and the next step's
+// prologue all in registers.  Step bodies restated (integrators.py):
+//
+//   if4   (:205-215)  PRE:  g1 = g(u); X1 = u + t/2 g1; X5 = u + t/6 g1
+//                     [u2, a, b, c] = expk([1/2, 1/2, 1, 1], [X1, u, u, X5])
+//                     MID:  g2 = g(u2); u3 = a + t/2 g2; g3 = g(u3); s = g2 + g3
+//                     [d, e] = expk(1/2, [g3, s])
+//                     END:  u4 = b + t d; g4 = g(u4); out = c + t/3 e + t/6 g4
+//                           check(out); PRE(out) for the next step
+//   strang (:161-164) FLOW1: v = flow(u, t/2)          expk(1, v) -> w
+//                     END:  out = flow(w, t/2); check; v' = flow(out, t/2)
+//   split4 (:167-175) FLOW2: v = flow(u, t/2) [seq 0], f = flow(u, t/4) [seq 2]
+//                     [v, f] = expk([1, 1/2], [v, f])
+//                     MID:  c = flow(v, t/2) [seq 1]; f = flow(f, t/2) [seq 3]
+//                     f = expk(1/2, f)
+//                     END:  fine = flow(f, t/4) [seq 4]; out = 4/3 fine - 1/3 c;
+//                           check; FLOW2(out) for the next step
+//   if2   (:198-202)  PRE:  g1 = g(u); X = u + t g1; Y = u + t/2 g1
+//                     [u2, o] = expk(1, [X, Y])
+//                     END:  out = o + t/2 g(u2); check; PRE(out)
+//
+// "flow" is the exact cubic flow for the cubic kind and one RK4 substep on
+// g otherwise (integrators.py:103-110).  Flow seq numbers follow the
+// reference's call order (one per component for the exact flow), so the
+// recorded first failure is the one the reference would raise.  A kernel
+// skips if a failure was recorded before its FIRST flow position.
+#include <cstdint>
+
+#include "cgl_common.cuh"
+#include "cgl_internal.h"
+
+namespace cgl {
+
+constexpr int kStageThreads = 256;
+
+struct StageNL {
+  double a3, b3, a4, b4, a5;
+  int kind;  // 0 cubic (exact flow), 1 cubic_quintic, 2 coupled
+};
+
+template <int NF>
+struct V {
+  double2 c[NF];
+};
+
+template <int NF>
+__device__ __forceinline__ V<NF> load(const double2* const* p, int base, int64_t i, double s) {
+  V<NF> v;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) v.c[c] = cscale(s, ld2(p[base + c] + i));
+  return v;
+}
+template <int NF>
+__device__ __forceinline__ void store(double2* const* p, int base, int64_t i, const V<NF>& v) {
+#pragma unroll
+  for (int c = 0; c < NF; ++c) p[base + c][i] = v.c[c];
+}
+template <int NF>
+__device__ __forceinline__ V<NF> axpy(double s, const V<NF>& x, const V<NF>& y) {  // s*x + y
+  V<NF> r;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) r.c[c] = cadd(cscale(s, x.c[c]), y.c[c]);
+  return r;
+}
+
+template <int NF>
+__device__ __forceinline__ V<NF> gfun(const StageNL& p, const V<NF>& u) {
+  double m[NF];
+#pragma unroll
+  for (int c = 0; c < NF; ++c) m[c] = cabs2(u.c[c]);
+  V<NF> g;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) {
+    double2 r = cmul(make_double2(p.a3 * m[c], p.b3 * m[c]), u.c[c]);
+    if (p.kind != 0) r = cadd(r, cmul(make_double2(p.a4 * (m[c] * m[c]), p.b4 * (m[c] * m[c])), u.c[c]));
+    if (p.kind == 2 && NF == 2) r = cadd(r, cscale(p.a5 * m[1 - c], u.c[c]));
+    g.c[c] = r;
+  }
+  return g;
+}
+
+__device__ __forceinline__ void note(uint64_t& key, uint64_t pos, unsigned reason) {
+  const uint64_t k = pos | reason;
+  if (k < key) key = k;
+}
+
+// exact cubic flow (flows.py:87-100) of one component at position pos
+__device__ __forceinline__ double2 cubic_exact(const StageNL& p, double2 u, double t, uint64_t pos, uint64_t& key) {
+  const double m = cabs2(u);
+  if (fabs(p.a3) < 1e-14) {
+    double sn, cs;
+    sincos(p.b3 * m * t, &sn, &cs);
+    return cmul(u, make_double2(cs, sn));
+  }
+  const double y = 2.0 * p.a3 * m * t;
+  if (y >= 1.0) note(key, pos, CGL_BLOWUP_CUBIC);
+  const double L = log1p(-y);
+  const double2 v = cmul(u, cexp(make_double2(-0.5 * L, (-p.b3 / (2.0 * p.a3)) * L)));
+  if (!cfinite(v)) note(key, pos, CGL_NONFINITE_CUBIC);
+  return v;
+}
+
+// one flow call of the scheme: seq positions seq0, seq0+1, ... (exact) or seq0 (rk4)
+template <int NF>
+__device__ __forceinline__ V<NF> flow(const StageNL& p, const V<NF>& u, double t, uint64_t step, int seq0,
+                                      uint64_t& key) {
+  V<NF> r;
+  if (p.kind == 0) {
+#pragma unroll
+    for (int c = 0; c < NF; ++c) r.c[c] = cubic_exact(p, u.c[c], t, (step << 24) | ((uint64_t)(seq0 + c) << 8), key);
+    return r;
+  }
+  const double h = 0.5 * t, t6 = t / 6.0;
+  const V<NF> k1 = gfun<NF>(p, u);
+  const V<NF> k2 = gfun<NF>(p, axpy<NF>(h, k1, u));
+  const V<NF> k3 = gfun<NF>(p, axpy<NF>(h, k2, u));
+  const V<NF> k4 = gfun<NF>(p, axpy<NF>(t, k3, u));
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) {
+    const double2 acc = cadd(cadd(cadd(k1.c[c], cscale(2.0, k2.c[c])), cscale(2.0, k3.c[c])), k4.c[c]);
+    r.c[c] = cadd(u.c[c], cscale(t6, acc));
+    bad |= !cfinite(r.c[c]);
+  }
+  if (bad) note(key, (step << 24) | ((uint64_t)seq0 << 8), CGL_NONFINITE_RK4);
+  return r;
+}
+
+template <int NF>
+__device__ __forceinline__ bool finite_all(const V<NF>& v) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) ok &= cfinite(v.c[c]);
+  return ok;
+}
+
+struct StageArgs {
+  const double2* in[8];
+  double2* out[8];
+  int64_t n;
+  double tau;
+  double in_scale;
+  StageNL nl;
+  cgl_flag_t* flag;
+  uint64_t pos;  // CGL_POS_DEVICE form allowed; low bits ignored (each program knows its seqs)
+  int fw;        // flow width: calls per flow() = NF for the exact cubic flow, 1 for RK4
+};
+
+__device__ __forceinline__ void raise_min(cgl_flag_t* f, uint64_t key) {
+  // warp-min then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other < key ? other : key;
+  }
+  if ((threadIdx.x & 31) == 0 && key != ~0ull && f) atomicMin(reinterpret_cast<unsigned long long*>(&f->key),
+                                                              (unsigned long long)key);
+}
+
+#define STAGE_LOOP for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; \
+                        i += (int64_t)gridDim.x * blockDim.x)
+
+enum Prog {
+  P_IF4_PRE = 0, P_IF4_MID, P_IF4_END, P_FLOW1, P_FLOW2, P_SPLIT4_MID, P_SPLIT4_END, P_STRANG_END,
+  P_IF2_PRE, P_IF2_END, P_NPROG
+};
+
+template <int NF, int PROG>
+__global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a) {
+  const cgl_flag_t* cf = a.flag;
+  const uint64_t step = resolve_pos(cf, a.pos) >> 24;
+  // first flow seq of the program (skip position); non-flow programs: 0
+  int first = 0;
+  if (PROG == P_SPLIT4_MID) first = a.fw;           // seq w (coarse second flow)
+  if (PROG == P_SPLIT4_END) first = 4 * a.fw;       // seq 4w
+  if (PROG == P_STRANG_END) first = a.fw;           // seq w
+  const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END);
+  if (flag_skip(cf, (step << 24) | ((uint64_t)first << 8))) return;  // all CTAs agree (key only grows later)
+
+  uint64_t key = ~0ull;
+  const double t = a.tau, s = a.in_scale;
+  const uint64_t check_pos = (step << 24) | (255ull << 8);
+  STAGE_LOOP {
+    if (PROG == P_IF4_PRE || PROG == P_IF2_PRE) {
+      const V<NF> u = load<NF>(a.in, 0, i, s);
+      const V<NF> g1 = gfun<NF>(a.nl, u);
+      store<NF>(a.out, 0, i, axpy<NF>(PROG == P_IF4_PRE ? 0.5 * t : t, g1, u));
+      store<NF>(a.out, NF, i, axpy<NF>(PROG == P_IF4_PRE ? t / 6.0 : 0.5 * t, g1, u));
+    } else if (PROG == P_IF4_MID) {
+      const V<NF> u2 = load<NF>(a.in, 0, i, s), av = load<NF>(a.in, NF, i, s);
+      const V<NF> g2 = gfun<NF>(a.nl, u2);
+      const V<NF> g3 = gfun<NF>(a.nl, axpy<NF>(0.5 * t, g2, av));
+      store<NF>(a.out, 0, i, g3);
+      store<NF>(a.out, NF, i, axpy<NF>(1.0, g2, g3));
+    } else if (PROG == P_IF4_END) {
+      const V<NF> b = load<NF>(a.in, 0, i, s), c = load<NF>(a.in, NF, i, s);
+      const V<NF> d = load<NF>(a.in, 2 * NF, i, s), e = load<NF>(a.in, 3 * NF, i, s);
+      const V<NF> g4 = gfun<NF>(a.nl, axpy<NF>(t, d, b));
+      const V<NF> out = axpy<NF>(t / 6.0, g4, axpy<NF>(t / 3.0, e, c));
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      const V<NF> g1 = gfun<NF>(a.nl, out);
+      store<NF>(a.out, NF, i, axpy<NF>(0.5 * t, g1, out));
+      store<NF>(a.out, 2 * NF, i, axpy<NF>(t / 6.0, g1, out));
+    } else if (PROG == P_FLOW1) {
+      // strang prologue: v = flow(u, t/2) at seq 0 of `step`
+      const V<NF> u = load<NF>(a.in, 0, i, s);
+      store<NF>(a.out, 0, i, flow<NF>(a.nl, u, 0.5 * t, step, 0, key));
+    } else if (PROG == P_FLOW2) {
+      // split4 prologue: v = flow(u, t/2) [seq 0], f = flow(u, t/4) [seq 2w]
+      const V<NF> u = load<NF>(a.in, 0, i, s);
+      store<NF>(a.out, 0, i, flow<NF>(a.nl, u, 0.5 * t, step, 0, key));
+      store<NF>(a.out, NF, i, flow<NF>(a.nl, u, 0.25 * t, step, 2 * a.fw, key));
+    } else if (PROG == P_SPLIT4_MID) {
+      const V<NF> v = load<NF>(a.in, 0, i, s), f = load<NF>(a.in, NF, i, s);
+      store<NF>(a.out, 0, i, flow<NF>(a.nl, v, 0.5 * t, step, a.fw, key));
+      store<NF>(a.out, NF, i, flow<NF>(a.nl, f, 0.5 * t, step, 3 * a.fw, key));
+    } else if (PROG == P_SPLIT4_END) {
+      const V<NF> f = load<NF>(a.in, 0, i, s), c = load<NF>(a.in, NF, i, s);
+      const V<NF> fine = flow<NF>(a.nl, f, 0.25 * t, step, 4 * a.fw, key);
+      V<NF> out;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) out.c[q] = cadd(cscale(4.0 / 3.0, fine.c[q]), cscale(-1.0 / 3.0, c.c[q]));
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      store<NF>(a.out, NF, i, flow<NF>(a.nl, out, 0.5 * t, step + 1, 0, key));
+      store<NF>(a.out, 2 * NF, i, flow<NF>(a.nl, out, 0.25 * t, step + 1, 2 * a.fw, key));
+    } else if (PROG == P_STRANG_END) {
+      const V<NF> w = load<NF>(a.in, 0, i, s);
+      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key);
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      store<NF>(a.out, NF, i, flow<NF>(a.nl, out, 0.5 * t, step + 1, 0, key));
+    } else if (PROG == P_IF2_END) {
+      const V<NF> u2 = load<NF>(a.in, 0, i, s), o = load<NF>(a.in, NF, i, s);
+      const V<NF> out = axpy<NF>(0.5 * t, gfun<NF>(a.nl, u2), o);
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      const V<NF> g1 = gfun<NF>(a.nl, out);
+      store<NF>(a.out, NF, i, axpy<NF>(t, g1, out));
+      store<NF>(a.out, 2 * NF, i, axpy<NF>(0.5 * t, g1, out));
+    }
+  }
+  raise_min(a.flag, key);
+  if (is_end) advance_step(a.flag);
+}
+
+template <int NF>
+static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
+  const int grid = grid_for(a.n, kStageThreads);
+  switch (prog) {
+    case P_IF4_PRE: stage_kernel<NF, P_IF4_PRE><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_IF4_MID: stage_kernel<NF, P_IF4_MID><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_IF4_END: stage_kernel<NF, P_IF4_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FLOW1: stage_kernel<NF, P_FLOW1><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FLOW2: stage_kernel<NF, P_FLOW2><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_SPLIT4_MID: stage_kernel<NF, P_SPLIT4_MID><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_SPLIT4_END: stage_kernel<NF, P_SPLIT4_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_STRANG_END: stage_kernel<NF, P_STRANG_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_IF2_PRE: stage_kernel<NF, P_IF2_PRE><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_IF2_END: stage_kernel<NF, P_IF2_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    default: return set_error(CGL_EINVAL, "stage: unknown program");
+  }
+  return check_launch("stage_kernel");
+}
+
+// inputs/outputs per program, in units of component groups
+static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2};
+static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3};
+
+int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonlinear_t* nl, double tau,
+                 double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
+  if (prog < 0 || prog >= P_NPROG) return set_error(CGL_EINVAL, "stage: unknown program");
+  if (nf != 1 && nf != 2) return set_error(CGL_EINVAL, "stage: 1 or 2 components");
+  if ((nl->kind == 2) != (nf == 2)) return set_error(CGL_EINVAL, "stage: component count does not match kind");
+  if (n <= 0) return 0;
+  StageArgs a{};
+  for (int q = 0; q < kIns[prog] * nf; ++q) a.in[q] = reinterpret_cast<const double2*>(in[q]);
+  for (int q = 0; q < kOuts[prog] * nf; ++q) a.out[q] = reinterpret_cast<double2*>(out[q]);
+  a.n = n;
+  a.tau = tau;
+  a.in_scale = in_scale;
+  a.nl = StageNL{nl->alpha3, nl->beta3, nl->alpha4, nl->beta4, nl->alpha5, nl->kind};
+  a.flag = flag;
+  a.pos = pos;
+  a.fw = nl->kind == 0 ? nf : 1;
+  return nf == 1 ? launch_prog<1>(prog, a, st) : launch_prog<2>(prog, a, st);
+}
+
+}  // namespace cgl

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, M3>;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, NT = Cfg::NT;
 
-  if (flag_skip(args.flag, args.pos)) return;
+  if (flag_skip(args.flag, resolve_pos(args.flag, args.pos))) return;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);

@@ -87,10 +87,10 @@ class _OneShotFlag:
     """Device flag for the standalone API functions (not the step loop)."""
 
     def __init__(self):
-        self.t = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        self.t = _lib.new_flag(0)
 
     def raise_if_set(self):
-        key = int(self.t.item()) & ((1 << 64) - 1)
+        key = int(self.t[0].item()) & ((1 << 64) - 1)
         if key != _lib.NO_DIVERGENCE:
             raise DivergenceError(_lib.REASONS[key & 0xFF])
 

@@ -359,7 +359,11 @@ def integrate(problem, scheme_name, fields, t_final, steps, snapshot_steps=(), o
     step_fn = _STEPPERS[scheme_name]
     wanted = set(int(k) for k in snapshot_steps)
 
-    flag = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    from . import plan as _plan
+    if _plan.supports(problem, scheme_name):
+        return _integrate_fused(problem, scheme_name, [d for d, _ in dev], host, tau, steps, wanted, on_snapshot)
+
+    flag = _lib.new_flag(1)
     state = [[d.clone() for d, _ in dev], [torch.empty_like(d) for d, _ in dev]]
     ctx = _Ctx(flag)
     problem._ctx = ctx
@@ -376,7 +380,7 @@ def integrate(problem, scheme_name, fields, t_final, steps, snapshot_steps=(), o
             _check_finite(problem, state[k % 2], ctx.at(_CHECK_SEQ))
             del new
             if k in wanted or k % poll == 0 or k == steps:
-                key = int(flag.item()) & ((1 << 64) - 1)
+                key = int(flag[0].item()) & ((1 << 64) - 1)
                 if key != _lib.NO_DIVERGENCE:
                     break
                 if k in wanted and on_snapshot is not None:
@@ -394,5 +398,39 @@ def integrate(problem, scheme_name, fields, t_final, steps, snapshot_steps=(), o
     k_div, reason = key >> 24, key & 0xFF
     out = state[k_div % 2] if reason == _lib.NONFINITE_STATE else state[(k_div - 1) % 2]
     return IntegrationResult(tuple(to_host_if(f, host) for f in out), steps, tau, seconds,
+                             diverged=True, diverged_at=int(k_div), reason=_lib.REASONS[reason],
+                             device_seconds=dev_s)
+
+
+def _integrate_fused(problem, scheme_name, u0, host, tau, steps, wanted, on_snapshot):
+    """Fused, graph-captured FD path (plan.py); same results contract."""
+    from . import plan as _plan
+    cache = problem.__dict__.setdefault("_plans", {})
+    key = (scheme_name, tuple(u0[0].shape), len(u0))
+    fp = cache.get(key)
+    if fp is None:
+        cache.clear()  # one live plan per problem bounds the device memory
+        fp = cache[key] = _plan.FusedPlan(problem, scheme_name, u0)
+
+    def stop(k, fields):
+        if on_snapshot is not None:
+            on_snapshot(k, k * tau, tuple(to_host_if(f.clone(), host) for f in fields))
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start = time.perf_counter()
+    ev0.record()
+    fkey = fp.run(u0, steps, tau, stop_at=wanted, on_stop=stop)
+    ev1.record()
+    torch.cuda.synchronize()
+    seconds = time.perf_counter() - start
+    dev_s = ev0.elapsed_time(ev1) / 1e3
+    if fkey == _lib.NO_DIVERGENCE:
+        out = fp.state_after(steps)
+        return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
+                                 device_seconds=dev_s)
+    k_div, reason = fkey >> 24, fkey & 0xFF
+    out = fp.state_after(k_div) if reason == _lib.NONFINITE_STATE else fp.state_after(k_div - 1)
+    return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
                              diverged=True, diverged_at=int(k_div), reason=_lib.REASONS[reason],
                              device_seconds=dev_s)

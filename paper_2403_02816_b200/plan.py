@@ -1,0 +1,192 @@
+"""Fused, graph-captured step plans for the Kronecker (finite-difference) path.
+
+A plan owns persistent device buffers for one (problem, scheme, tau) and
+runs each time step as a handful of launches: batched DMMA Tucker chains
+for every exp(f tau K) the step needs (integrators.py:146-215) and ONE
+fused stage kernel between consecutive Tucker groups (csrc/stages.cu).
+Steps are captured into CUDA graphs in chunks, so the host issues one graph
+launch per chunk; kernel positions for the divergence key come from the
+device step counter in the flag record, which the end-of-step kernel
+advances, so a captured chunk replays unchanged.
+
+Per-step launch structure (d = number of dimensions, one GEMM per mode):
+  if4     d GEMM (4 Tuckers)  + MID + d GEMM (2 Tuckers) + END      = 2d + 2
+  strang  d GEMM (1 Tucker)   + END                                  = d + 1
+  split4  d GEMM (2 Tuckers)  + MID + d GEMM (1 Tucker) + END        = 2d + 2
+  if2     d GEMM (2 Tuckers)  + END                                  = d + 1
+"""
+
+import os
+
+import torch
+
+from . import _lib
+from .operators import KroneckerOperator
+from .tensors import tucker_dev
+
+FUSED_SCHEMES = ("if4", "strang", "split4", "if2")
+
+
+def fused_enabled():
+    return os.environ.get("CGL_FUSED", "1") != "0"
+
+
+def supports(problem, scheme_name):
+    return (fused_enabled() and not problem.fourier and scheme_name in FUSED_SCHEMES
+            and all(isinstance(b, KroneckerOperator) for b in problem._blocks))
+
+
+class FusedPlan:
+    CHUNK = 16
+
+    def __init__(self, problem, scheme_name, like):
+        from fractions import Fraction
+        self.p = problem
+        self.scheme = scheme_name
+        self.nf = len(like)
+        self.n = like[0].numel()
+        self.nl = problem._nl
+        self.blocks = problem._blocks
+        self.half, self.one = Fraction(1, 2), Fraction(1)
+        mk = lambda: [torch.empty_like(like[0]) for _ in range(self.nf)]  # noqa: E731
+        nstate = 2 if scheme_name in ("strang", "split4") else 1
+        self.U = [mk() for _ in range(nstate)]
+        nbuf = {"if4": 6, "strang": 2, "split4": 4, "if2": 4}[scheme_name]
+        self.B = [mk() for _ in range(nbuf)]
+        nwork = {"if4": 4, "strang": 1, "split4": 2, "if2": 2}[scheme_name]
+        self.W = [t for _ in range(nwork) for t in mk()] if like[0].ndim > 1 else []
+        self.graphs = {}
+        self.flag = _lib.new_flag(1)   # baked into the captured graphs; reset per run
+        self._flag0 = self.flag.clone()
+
+    # -- launch helpers --------------------------------------------------------
+    def _tucker(self, jobs, flag):
+        """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode."""
+        ins, outs, mats, mts = [], [], [], []
+        for f, fin, fout in jobs:
+            for c in range(self.nf):
+                m, mt = self.blocks[c].exp_factors(f)
+                ins.append(fin[c])
+                outs.append(fout[c])
+                mats.append(m)
+                mts.append(mt)
+        work = self.W[:len(ins)] if self.W else None
+        tucker_dev(ins, mats, mts, outs=outs, flag=flag, pos=_lib.POS_DEVICE, work=work)
+
+    def _stage(self, name, ins, outs, flag, tau):
+        lib = _lib.load()
+        fin = [t for fs in ins for t in fs]
+        fout = [t for fs in outs for t in fs]
+        _lib.check(lib.cgl_stage(_lib.stream(), _lib.STAGE[name], self.nf, self.n, _lib.ctypes.byref(self.nl),
+                                 tau, 1.0, _lib.ptr_array(fin), _lib.ptr_array(fout), _lib.flag_ptr(flag),
+                                 _lib.POS_DEVICE), "cgl_stage")
+
+    # -- scheme bodies -----------------------------------------------------------
+    def state_after(self, k):
+        return self.U[k % len(self.U)]
+
+    def prologue(self, flag, tau):
+        u, B = self.U[0], self.B
+        if self.scheme == "if4":
+            self._stage("if4_pre", [u], [B[0], B[1]], flag, tau)          # X1, X5
+        elif self.scheme == "if2":
+            self._stage("if2_pre", [u], [B[0], B[1]], flag, tau)          # X, Y
+        elif self.scheme == "strang":
+            self._stage("flow1", [u], [B[0]], flag, tau)                  # v
+        elif self.scheme == "split4":
+            self._stage("flow2", [u], [B[0], B[1]], flag, tau)            # v, f
+
+    def step(self, k, flag, tau):
+        """One time step k (1-based); input state_after(k-1), output state_after(k)."""
+        B, H, O = self.B, self.half, self.one
+        if self.scheme == "if4":
+            u = self.U[0]
+            x1, x5, u2, a, b, c = B
+            self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag)
+            self._stage("if4_mid", [u2, a], [u2, a], flag, tau)          # g3 -> u2, s -> a
+            self._tucker([(H, u2, x1), (H, a, x5)], flag)                 # d -> x1, e -> x5
+            self._stage("if4_end", [b, c, x1, x5], [u, x1, x5], flag, tau)
+        elif self.scheme == "if2":
+            u = self.U[0]
+            x, y, u2, o = B
+            self._tucker([(O, x, u2), (O, y, o)], flag)
+            self._stage("if2_end", [u2, o], [u, x, y], flag, tau)
+        elif self.scheme == "strang":
+            v, w = B
+            self._tucker([(O, v, w)], flag)
+            self._stage("strang_end", [w], [self.state_after(k), v], flag, tau)
+        elif self.scheme == "split4":
+            v, f, v2, f2 = B
+            self._tucker([(O, v, v2), (H, f, f2)], flag)
+            self._stage("split4_mid", [v2, f2], [v2, f2], flag, tau)      # coarse c -> v2, f -> f2
+            self._tucker([(H, f2, v)], flag)                              # f3 -> v
+            self._stage("split4_end", [v, v2], [self.state_after(k), v, f], flag, tau)
+
+    # -- driver ------------------------------------------------------------------
+    def _graph(self, k0, count, flag, tau):
+        key = (k0 % len(self.U), count)
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    for j in range(count):
+                        self.step(k0 + j, flag, tau)
+            torch.cuda.current_stream().wait_stream(s)
+            self.graphs[key] = g
+        return g
+
+    def run(self, u0, steps, tau, stop_at=(), on_stop=None, poll_chunks=1):
+        """Advance `steps` steps from u0; returns the flag key (int)."""
+        flag = self.flag
+        flag.copy_(self._flag0)
+        for c in range(self.nf):
+            self.U[0][c].copy_(u0[c])
+        self.prologue(flag, tau)
+        stops = sorted(set(int(s) for s in stop_at if 1 <= int(s) <= steps))
+        k = 1
+        pins = [torch.empty(1, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        pending = None  # (event, pinned) of the last asynchronous flag read
+        eager_first = True
+        nchunk = 0
+
+        def diverged(v):
+            key = int(v) & ((1 << 64) - 1)
+            return key if key != _lib.NO_DIVERGENCE and (key >> 24) <= steps else None
+
+        while k <= steps:
+            nxt = next((s for s in stops if s >= k), steps)
+            count = min(self.CHUNK, nxt - k + 1)
+            if eager_first or count != self.CHUNK:
+                for j in range(count):
+                    self.step(k + j, flag, tau)
+                eager_first = False
+            else:
+                self._graph(k, count, flag, tau).replay()
+            k += count
+            nchunk += 1
+            if (k - 1) in stops or k > steps:
+                torch.cuda.current_stream().synchronize()
+                key = diverged(flag[0].item())
+                if key is not None:
+                    return key
+                if (k - 1) in stops and on_stop is not None:
+                    on_stop(k - 1, self.state_after(k - 1))
+                pending = None
+                continue
+            # non-blocking divergence poll: read the previous chunk's copy if it landed
+            if pending is not None and pending[0].query():
+                key = diverged(pending[1].item())
+                pending = None
+                if key is not None:
+                    torch.cuda.current_stream().synchronize()
+                    return diverged(flag[0].item())
+            if pending is None and nchunk % max(1, poll_chunks) == 0:
+                pin = pins[nchunk % 2]
+                pin.copy_(flag[:1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                pending = (ev, pin)
+        return _lib.NO_DIVERGENCE

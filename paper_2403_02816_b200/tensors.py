@@ -59,15 +59,17 @@ def mode_product_dev(u, m, mt, axis, out=None, alpha=1.0, y=None, beta=0.0, flag
     return out
 
 
-def tucker_dev(fields, mats, mats_t, outs=None, flag=None, pos=0):
+def tucker_dev(fields, mats, mats_t, outs=None, flag=None, pos=0, work=None):
     """Device-level batched Tucker: fields[f] x_1 mats[f][0] ... x_d mats[f][d-1],
-    one GEMM launch per mode for all fields (cgl_tucker)."""
+    one GEMM launch per mode for all fields (cgl_tucker).  `work`: one scratch
+    field per input (allocated when None)."""
     nf = len(fields)
     shape = tuple(fields[0].shape)
     nd = len(shape)
     if outs is None:
         outs = [torch.empty_like(f) for f in fields]
-    work = [torch.empty_like(f) for f in fields] if nd > 1 else []
+    if work is None:
+        work = [torch.empty_like(f) for f in fields] if nd > 1 else []
     lib = _lib.load()
     flat = [m for ms in mats for m in ms]
     flat_t = [m for ms in mats_t for m in ms]
