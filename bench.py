@@ -269,6 +269,7 @@ def gpu_arm(args, w, scheme):
     if world > 1:
         torch.distributed.barrier()
     n_launch0 = lib.cgl_launch_count()
+    replay0 = sum(fp.replayed_launches for fp in getattr(prob, "_plans", {}).values())
     dev_total = 0.0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -276,7 +277,8 @@ def gpu_arm(args, w, scheme):
             torch.cuda.synchronize()
             r = P.integrate(prob, scheme, (x0,), w.t_final, w.steps)
             dev_total += r.device_seconds
-    launches = lib.cgl_launch_count() - n_launch0
+    launches = lib.cgl_launch_count() - n_launch0 + sum(
+        fp.replayed_launches for fp in getattr(prob, "_plans", {}).values()) - replay0
     torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([dev_total], dtype=torch.float64, device="cuda")

@@ -58,6 +58,8 @@ class FusedPlan:
         self.graphs = {}
         self.flag = _lib.new_flag(1)   # baked into the captured graphs; reset per run
         self._flag0 = self.flag.clone()
+        self.graph_launches = {}       # cgl kernels inside each captured graph
+        self.replayed_launches = 0     # cgl kernels launched by graph replays (not seen by the C counter)
 
     # -- launch helpers --------------------------------------------------------
     def _tucker(self, jobs, flag):
@@ -130,12 +132,16 @@ class FusedPlan:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
+            lib = _lib.load()
+            n0 = lib.cgl_launch_count()
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
                     for j in range(count):
                         self.step(k0 + j, flag, tau)
             torch.cuda.current_stream().wait_stream(s)
+            self.graph_launches[key] = lib.cgl_launch_count() - n0
             self.graphs[key] = g
+        self.replayed_launches += self.graph_launches[key]
         return g
 
     def run(self, u0, steps, tau, stop_at=(), on_stop=None, poll_chunks=1):
