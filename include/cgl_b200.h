@@ -168,7 +168,13 @@ enum cgl_stage_program {
   CGL_STAGE_SPLIT4_END = 6, /* in f, c         -> out u', v', f'       */
   CGL_STAGE_STRANG_END = 7, /* in w            -> out u', v'           */
   CGL_STAGE_IF2_PRE = 8,    /* in u            -> out X, Y             */
-  CGL_STAGE_IF2_END = 9     /* in u2, o        -> out u', X', Y'       */
+  CGL_STAGE_IF2_END = 9,    /* in u2, o        -> out u', X', Y'       */
+  /* Fourier if4 (spectral space, integrators.py:205-215 with E = exp(f tau symbol)) */
+  CGL_STAGE_FIF4_S1 = 10,   /* in u, g1        -> out E1/2 (u + t/2 g1)            */
+  CGL_STAGE_FIF4_S2 = 11,   /* in u, g2        -> out E1/2 u + t/2 g2              */
+  CGL_STAGE_FIF4_S3 = 12,   /* in u, g3        -> out t E1/2 g3 + E1 u             */
+  CGL_STAGE_FIF4_S4 = 13,   /* in u,g1,g2,g3,g4 -> out u' (+ check, step++)        */
+  CGL_STAGE_FLOW_END = 14   /* in w (physical) -> out flow(w, t/2) (+ check, step++) */
 };
 /* One fused pass of a step body (integrators.py:146-215): see the program
  * table in csrc/stages.cu.  in/out: (#operands x nfields) pointers, operand
@@ -180,6 +186,15 @@ int cgl_stage(void* stream, int program, int nfields, int64_t n,
               const cgl_nonlinear_t* nl, double tau, double in_scale,
               const double* const* in, double* const* out,
               cgl_flag_t* flag, uint64_t pos);
+
+/* Fourier stage programs (CGL_STAGE_FIF4_*): the separable multipliers are
+ * evaluated in-kernel from per-axis tables, tables[(fr*nfields + c)*ndim + d]
+ * for fraction slot fr (0: 1/2, 1: 1), component c, axis d. */
+int cgl_stage_fourier(void* stream, int program, int nfields, int ndim,
+                      const int64_t* shape, const cgl_nonlinear_t* nl, double tau,
+                      double in_scale, const double* const* tables,
+                      const double* const* in, double* const* out,
+                      cgl_flag_t* flag, uint64_t pos);
 
 /* Hadamard product out = factor .* in (spectral.py:123-129). */
 int cgl_pointwise_mul(void* stream, int64_t n, const double* factor,

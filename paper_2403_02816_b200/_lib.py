@@ -37,7 +37,8 @@ NO_DIVERGENCE = (1 << 64) - 1
 POS_DEVICE = 1 << 63
 
 STAGE = {"if4_pre": 0, "if4_mid": 1, "if4_end": 2, "flow1": 3, "flow2": 4, "split4_mid": 5,
-         "split4_end": 6, "strang_end": 7, "if2_pre": 8, "if2_end": 9}
+         "split4_end": 6, "strang_end": 7, "if2_pre": 8, "if2_end": 9, "fif4_s1": 10, "fif4_s2": 11,
+         "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14}
 
 
 def new_flag(first_step=1):
@@ -77,6 +78,8 @@ _SIGS = {
     "cgl_check_finite": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr, c_u64]),
     "cgl_flag_reset": (c_int, [c_ptr, c_ptr]),
     "cgl_stage": (c_int, [c_ptr, c_int, c_int, c_i64, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),
+    "cgl_stage_fourier": (c_int, [c_ptr, c_int, c_int, c_int, c_ptr, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr,
+                                  c_ptr, c_u64]),
     "cgl_pointwise_mul": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_symbol_exp": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr]),
     "cgl_separable_mul": (c_int, [c_ptr, c_int, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),

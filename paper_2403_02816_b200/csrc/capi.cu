@@ -27,7 +27,7 @@ int fft_plan(int, const int64_t*, void**);
 int fft_exec(void*, cudaStream_t, const double*, double*, int);
 int fft_destroy(void*);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
-                 double* const*, cgl_flag_t*, uint64_t);
+                 double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
 
 static thread_local std::string g_err;
 static unsigned long long g_launches = 0;
@@ -251,7 +251,17 @@ int cgl_separable_mul(void* stream, int ndim, const int64_t* shape, const double
 
 int cgl_stage(void* stream, int program, int nfields, int64_t n, const cgl_nonlinear_t* nl, double tau,
               double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
-  return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos);
+  return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos, 0, nullptr,
+                      nullptr);
+}
+
+int cgl_stage_fourier(void* stream, int program, int nfields, int ndim, const int64_t* shape,
+                      const cgl_nonlinear_t* nl, double tau, double in_scale, const double* const* tables,
+                      const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
+  int64_t n = 1;
+  for (int d = 0; d < ndim; ++d) n *= shape[d];
+  return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos, ndim, shape,
+                      tables);
 }
 
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }

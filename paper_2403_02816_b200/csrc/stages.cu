@@ -148,7 +148,31 @@ struct StageArgs {
   cgl_flag_t* flag;
   uint64_t pos;  // CGL_POS_DEVICE form allowed; low bits ignored (each program knows its seqs)
   int fw;        // flow width: calls per flow() = NF for the exact cubic flow, 1 for RK4
+  // Fourier programs: separable exp(f tau symbol) tables, [fraction 1/2, 1][component][axis]
+  const double2* tab[2][2][4];
+  int64_t ext[4];
+  int nd;
 };
+
+// exp(f tau symbol) at flat index i (C order) for fraction slot fr, component c
+__device__ __forceinline__ double2 sep_factor(const StageArgs& a, int fr, int c, int64_t i) {
+  double2 e = make_double2(1.0, 0.0);
+  int64_t r = i;
+  for (int d = a.nd - 1; d >= 0; --d) {
+    const int64_t j = r % a.ext[d];
+    r /= a.ext[d];
+    e = cmul(e, ld2(a.tab[fr][c][d] + j));
+  }
+  return e;
+}
+
+template <int NF>
+__device__ __forceinline__ V<NF> emul(const StageArgs& a, int fr, int64_t i, const V<NF>& x) {
+  V<NF> r;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) r.c[c] = cmul(sep_factor(a, fr, c, i), x.c[c]);
+  return r;
+}
 
 __device__ __forceinline__ void raise_min(cgl_flag_t* f, uint64_t key) {
   // warp-min then one atomic per warp
@@ -165,7 +189,9 @@ __device__ __forceinline__ void raise_min(cgl_flag_t* f, uint64_t key) {
 
 enum Prog {
   P_IF4_PRE = 0, P_IF4_MID, P_IF4_END, P_FLOW1, P_FLOW2, P_SPLIT4_MID, P_SPLIT4_END, P_STRANG_END,
-  P_IF2_PRE, P_IF2_END, P_NPROG
+  P_IF2_PRE, P_IF2_END,
+  // Fourier (spectral-space) programs; g / flows run in physical space between cuFFT calls
+  P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END, P_NPROG
 };
 
 template <int NF, int PROG>
@@ -176,8 +202,9 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
   int first = 0;
   if (PROG == P_SPLIT4_MID) first = a.fw;           // seq w (coarse second flow)
   if (PROG == P_SPLIT4_END) first = 4 * a.fw;       // seq 4w
-  if (PROG == P_STRANG_END) first = a.fw;           // seq w
-  const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END);
+  if (PROG == P_STRANG_END || PROG == P_FLOW_END) first = a.fw;  // seq w
+  const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END ||
+                       PROG == P_FIF4_S4 || PROG == P_FLOW_END);
   if (flag_skip(cf, (step << 24) | ((uint64_t)first << 8))) return;  // all CTAs agree (key only grows later)
 
   uint64_t key = ~0ull;
@@ -234,6 +261,34 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
       store<NF>(a.out, 0, i, out);
       store<NF>(a.out, NF, i, flow<NF>(a.nl, out, 0.5 * t, step + 1, 0, key));
+    } else if (PROG == P_FIF4_S1) {
+      // u2 = E1/2 (u + t/2 g1)
+      const V<NF> u = load<NF>(a.in, 0, i, s), g1 = load<NF>(a.in, NF, i, s);
+      store<NF>(a.out, 0, i, emul<NF>(a, 0, i, axpy<NF>(0.5 * t, g1, u)));
+    } else if (PROG == P_FIF4_S2) {
+      // u3 = E1/2 u + t/2 g2
+      const V<NF> u = load<NF>(a.in, 0, i, s), g2 = load<NF>(a.in, NF, i, s);
+      store<NF>(a.out, 0, i, axpy<NF>(0.5 * t, g2, emul<NF>(a, 0, i, u)));
+    } else if (PROG == P_FIF4_S3) {
+      // u4 = t E1/2 g3 + E1 u
+      const V<NF> u = load<NF>(a.in, 0, i, s), g3 = load<NF>(a.in, NF, i, s);
+      store<NF>(a.out, 0, i, axpy<NF>(t, emul<NF>(a, 0, i, g3), emul<NF>(a, 1, i, u)));
+    } else if (PROG == P_FIF4_S4) {
+      // out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4
+      const V<NF> u = load<NF>(a.in, 0, i, s), g1 = load<NF>(a.in, NF, i, s);
+      const V<NF> g2 = load<NF>(a.in, 2 * NF, i, s), g3 = load<NF>(a.in, 3 * NF, i, s);
+      const V<NF> g4 = load<NF>(a.in, 4 * NF, i, s);
+      const V<NF> out = axpy<NF>(t / 6.0, g4, axpy<NF>(t / 3.0, emul<NF>(a, 0, i, axpy<NF>(1.0, g2, g3)),
+                                                       emul<NF>(a, 1, i, axpy<NF>(t / 6.0, g1, u))));
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+    } else if (PROG == P_FLOW_END) {
+      // out = flow(w, t/2) at seq w; finiteness of the physical result stands in for the
+      // spectral state's (an FFT of finite values is finite barring overflow)
+      const V<NF> w = load<NF>(a.in, 0, i, s);
+      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key);
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
     } else if (PROG == P_IF2_END) {
       const V<NF> u2 = load<NF>(a.in, 0, i, s), o = load<NF>(a.in, NF, i, s);
       const V<NF> out = axpy<NF>(0.5 * t, gfun<NF>(a.nl, u2), o);
@@ -262,17 +317,23 @@ static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
     case P_STRANG_END: stage_kernel<NF, P_STRANG_END><<<grid, kStageThreads, 0, st>>>(a); break;
     case P_IF2_PRE: stage_kernel<NF, P_IF2_PRE><<<grid, kStageThreads, 0, st>>>(a); break;
     case P_IF2_END: stage_kernel<NF, P_IF2_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FIF4_S1: stage_kernel<NF, P_FIF4_S1><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FIF4_S2: stage_kernel<NF, P_FIF4_S2><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FIF4_S3: stage_kernel<NF, P_FIF4_S3><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FIF4_S4: stage_kernel<NF, P_FIF4_S4><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_FLOW_END: stage_kernel<NF, P_FLOW_END><<<grid, kStageThreads, 0, st>>>(a); break;
     default: return set_error(CGL_EINVAL, "stage: unknown program");
   }
   return check_launch("stage_kernel");
 }
 
 // inputs/outputs per program, in units of component groups
-static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2};
-static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3};
+static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2, 2, 2, 2, 5, 1};
+static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1};
 
 int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonlinear_t* nl, double tau,
-                 double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
+                 double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,
+                 int ndim, const int64_t* shape, const double* const* tables) {
   if (prog < 0 || prog >= P_NPROG) return set_error(CGL_EINVAL, "stage: unknown program");
   if (nf != 1 && nf != 2) return set_error(CGL_EINVAL, "stage: 1 or 2 components");
   if ((nl->kind == 2) != (nf == 2)) return set_error(CGL_EINVAL, "stage: component count does not match kind");
@@ -287,6 +348,18 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
   a.flag = flag;
   a.pos = pos;
   a.fw = nl->kind == 0 ? nf : 1;
+  if (prog >= P_FIF4_S1 && prog <= P_FIF4_S4) {
+    if (ndim < 1 || ndim > 4 || !shape || !tables) return set_error(CGL_EINVAL, "stage: Fourier programs need tables");
+    a.nd = ndim;
+    int64_t tot = 1;
+    for (int d = 0; d < ndim; ++d) { a.ext[d] = shape[d]; tot *= shape[d]; }
+    if (tot != n) return set_error(CGL_ESHAPE, "stage: shape does not match n");
+    // tables: [fraction(2)][component(nf)][axis(ndim)]
+    for (int fr = 0; fr < 2; ++fr)
+      for (int c = 0; c < nf; ++c)
+        for (int d = 0; d < ndim; ++d)
+          a.tab[fr][c][d] = reinterpret_cast<const double2*>(tables[(fr * nf + c) * ndim + d]);
+  }
   return nf == 1 ? launch_prog<1>(prog, a, st) : launch_prog<2>(prog, a, st);
 }
 

@@ -410,7 +410,7 @@ def _integrate_fused(problem, scheme_name, u0, host, tau, steps, wanted, on_snap
     fp = cache.get(key)
     if fp is None:
         cache.clear()  # one live plan per problem bounds the device memory
-        fp = cache[key] = _plan.FusedPlan(problem, scheme_name, u0)
+        fp = cache[key] = _plan.make_plan(problem, scheme_name, u0)
 
     def stop(k, fields):
         if on_snapshot is not None:
@@ -426,11 +426,11 @@ def _integrate_fused(problem, scheme_name, u0, host, tau, steps, wanted, on_snap
     seconds = time.perf_counter() - start
     dev_s = ev0.elapsed_time(ev1) / 1e3
     if fkey == _lib.NO_DIVERGENCE:
-        out = fp.state_after(steps)
+        out = fp.result(steps)
         return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
                                  device_seconds=dev_s)
     k_div, reason = fkey >> 24, fkey & 0xFF
-    out = fp.state_after(k_div) if reason == _lib.NONFINITE_STATE else fp.state_after(k_div - 1)
+    out = fp.result(k_div) if reason == _lib.NONFINITE_STATE else fp.result(k_div - 1)
     return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
                              diverged=True, diverged_at=int(k_div), reason=_lib.REASONS[reason],
                              device_seconds=dev_s)

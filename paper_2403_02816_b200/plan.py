@@ -31,9 +31,21 @@ def fused_enabled():
     return os.environ.get("CGL_FUSED", "1") != "0"
 
 
+FOURIER_SCHEMES = ("if4", "strang")
+
+
 def supports(problem, scheme_name):
-    return (fused_enabled() and not problem.fourier and scheme_name in FUSED_SCHEMES
-            and all(isinstance(b, KroneckerOperator) for b in problem._blocks))
+    if not fused_enabled():
+        return False
+    if problem.fourier:
+        from .operators import FourierOperator
+        return (scheme_name in FOURIER_SCHEMES and len(problem._blocks[0].shape) <= 3
+                and all(isinstance(b, FourierOperator) and b._sep is not None for b in problem._blocks))
+    return scheme_name in FUSED_SCHEMES and all(isinstance(b, KroneckerOperator) for b in problem._blocks)
+
+
+def make_plan(problem, scheme_name, like):
+    return (FourierPlan if problem.fourier else FusedPlan)(problem, scheme_name, like)
 
 
 class FusedPlan:
@@ -86,6 +98,14 @@ class FusedPlan:
     # -- scheme bodies -----------------------------------------------------------
     def state_after(self, k):
         return self.U[k % len(self.U)]
+
+    def result(self, k):
+        """Fields in the operator's representation after step k."""
+        return self.state_after(k)
+
+    def load_state(self, u0, tau):
+        for c in range(self.nf):
+            self.U[0][c].copy_(u0[c])
 
     def prologue(self, flag, tau):
         u, B = self.U[0], self.B
@@ -148,8 +168,7 @@ class FusedPlan:
         """Advance `steps` steps from u0; returns the flag key (int)."""
         flag = self.flag
         flag.copy_(self._flag0)
-        for c in range(self.nf):
-            self.U[0][c].copy_(u0[c])
+        self.load_state(u0, tau)
         self.prologue(flag, tau)
         stops = sorted(set(int(s) for s in stop_at if 1 <= int(s) <= steps))
         k = 1
@@ -179,7 +198,7 @@ class FusedPlan:
                 if key is not None:
                     return key
                 if (k - 1) in stops and on_stop is not None:
-                    on_stop(k - 1, self.state_after(k - 1))
+                    on_stop(k - 1, self.result(k - 1))
                 pending = None
                 continue
             # non-blocking divergence poll: read the previous chunk's copy if it landed
@@ -196,3 +215,138 @@ class FusedPlan:
                 ev.record()
                 pending = (ev, pin)
         return _lib.NO_DIVERGENCE
+
+
+class FourierPlan(FusedPlan):
+    """Fused periodic (pseudospectral) plans: cuFFT Z2Z + spectral stage
+    kernels with the separable exp(f tau symbol) evaluated in-kernel.
+
+    if4: state kept in coefficient space; per step 8 FFTs (4 g evaluations
+    as F g F^-1, integrators.py:99-101) + 4 g kernels (1/N folded) + 4
+    spectral stage kernels (FIF4_S1..S4).
+    strang: the state is kept in PHYSICAL space between steps: the
+    reference's F^-1(F(.)) pair at each step boundary is elided (identical
+    math, rounding-level difference), leaving per step one fused pointwise
+    kernel (flow t/2 of step k, finiteness check, flow t/2 of step k+1),
+    one FFT, the separable E1 multiply and one inverse FFT.  Coefficients are
+    formed once at the end (and at snapshot steps).  cuFFT never writes a
+    state buffer, so divergence semantics are preserved.
+    """
+
+    def __init__(self, problem, scheme_name, like):
+        from fractions import Fraction
+        self.p = problem
+        self.scheme = scheme_name
+        self.nf = len(like)
+        self.shape = tuple(like[0].shape)
+        self.n = like[0].numel()
+        self.nl = problem._nl
+        self.blocks = problem._blocks
+        self.half, self.one = Fraction(1, 2), Fraction(1)
+        mk = lambda: [torch.empty_like(like[0]) for _ in range(self.nf)]  # noqa: E731
+        if scheme_name == "if4":
+            self.U = [mk()]
+            self.B = [mk() for _ in range(5)]      # Q, G1, G2, G3, G4
+        else:
+            self.U = [mk(), mk()]                  # physical state ping-pong
+            self.B = [mk()]                        # Q (v / spectral scratch)
+        self.graphs = {}
+        self.flag = _lib.new_flag(1)
+        self._flag0 = self.flag.clone()
+        self.graph_launches = {}
+        self.replayed_launches = 0
+        self.W = []
+
+    def _tables(self):
+        # [fraction slot (1/2, 1)][component][axis]
+        tabs = []
+        for f in (self.half, self.one):
+            for b in self.blocks:
+                kind, data = b.exp_entry(f) if f in b._cache else ("sep", None)
+                if data is None:
+                    data = b.exp_entry(self.one)[1]  # strang prepares only f = 1; slot unused
+                tabs.extend(data)
+        return tabs
+
+    def _fft(self, fields_in, fields_out, inverse):
+        from .spectral import fft_dev
+        for a, b in zip(fields_in, fields_out):
+            fft_dev(a, inverse=inverse, out=b)
+
+    def _g(self, fields, scale):
+        from .flows import eval_g_dev
+        eval_g_dev(self.nl, fields, scale=scale, outs=fields, flag=self.flag, pos=_lib.POS_DEVICE)
+
+    def _fstage(self, name, ins, outs, tau, scale=1.0):
+        lib = _lib.load()
+        fin = [t for fs in ins for t in fs]
+        fout = [t for fs in outs for t in fs]
+        tabs = self._tab_ptrs
+        _lib.check(lib.cgl_stage_fourier(_lib.stream(), _lib.STAGE[name], self.nf, len(self.shape),
+                                         _lib.i64_array(self.shape), _lib.ctypes.byref(self.nl), tau, scale,
+                                         tabs, _lib.ptr_array(fin), _lib.ptr_array(fout),
+                                         _lib.flag_ptr(self.flag), _lib.POS_DEVICE), "cgl_stage_fourier")
+
+    def _pstage(self, name, ins, outs, tau, scale):
+        lib = _lib.load()
+        fin = [t for fs in ins for t in fs]
+        fout = [t for fs in outs for t in fs]
+        _lib.check(lib.cgl_stage(_lib.stream(), _lib.STAGE[name], self.nf, self.n, _lib.ctypes.byref(self.nl),
+                                 tau, scale, _lib.ptr_array(fin), _lib.ptr_array(fout), _lib.flag_ptr(self.flag),
+                                 _lib.POS_DEVICE), "cgl_stage")
+
+    def _mul_e1(self, fields):
+        lib = _lib.load()
+        for b, x in zip(self.blocks, fields):
+            _, tabs = b.exp_entry(self.one)
+            _lib.check(lib.cgl_separable_mul(_lib.stream(), x.ndim, _lib.i64_array(x.shape), _lib.ptr_array(tabs),
+                                             1.0, _lib.ptr(x), _lib.ptr(x), _lib.flag_ptr(self.flag),
+                                             _lib.POS_DEVICE), "cgl_separable_mul")
+
+    def load_state(self, u0, tau):
+        self._tab_list = self._tables()
+        self._tab_ptrs = _lib.ptr_array(self._tab_list)
+        if self.scheme == "if4":
+            for c in range(self.nf):
+                self.U[0][c].copy_(u0[c])
+        else:
+            # physical state p0 = F^-1 u0 = ifftn(u0) (spectral.py:84-86)
+            from .spectral import scale_dev
+            self._fft(u0, self.U[0], inverse=True)
+            for x in self.U[0]:
+                scale_dev(x, 1.0 / self.n, out=x)
+        self._scale0 = 1.0
+
+    def prologue(self, flag, tau):
+        if self.scheme == "strang":
+            # v = flow(p0 / N, t/2) at seq 0 of step 1
+            self._pstage("flow1", [self.U[0]], [self.B[0]], tau, self._scale0)
+
+    def step(self, k, flag, tau):
+        inv_n = 1.0 / self.n
+        if self.scheme == "if4":
+            u = self.U[0]
+            q, g1, g2, g3, g4 = self.B
+            self._fft(u, q, inverse=True)
+            self._g(q, inv_n)
+            self._fft(q, g1, inverse=False)
+            for name, gin, gout in (("fif4_s1", g1, g2), ("fif4_s2", g2, g3), ("fif4_s3", g3, g4)):
+                self._fstage(name, [u, gin], [q], tau)
+                self._fft(q, q, inverse=True)
+                self._g(q, inv_n)
+                self._fft(q, gout, inverse=False)
+            self._fstage("fif4_s4", [u, g1, g2, g3, g4], [u], tau)
+        else:
+            v = self.B[0]
+            self._fft(v, v, inverse=False)
+            self._mul_e1(v)
+            self._fft(v, v, inverse=True)
+            # out_k = flow(w / N, t/2) [seq w], check, v' = flow(out_k, t/2) [step k+1, seq 0]
+            self._pstage("strang_end", [v], [self.state_after(k), v], tau, inv_n)
+
+    def result(self, k):
+        if self.scheme == "if4":
+            return self.U[0]
+        out = [torch.empty_like(x) for x in self.U[0]]
+        self._fft(self.state_after(k), out, inverse=False)
+        return out
