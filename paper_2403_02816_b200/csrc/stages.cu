@@ -139,7 +139,7 @@ __device__ __forceinline__ bool finite_all(const V<NF>& v) {
 }
 
 struct StageArgs {
-  const double2* in[8];
+  const double2* in[12];  // up to 5 operands x 2 components (FIF4_S4, coupled)
   double2* out[8];
   int64_t n;
   double tau;
@@ -336,6 +336,7 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
                  int ndim, const int64_t* shape, const double* const* tables) {
   if (prog < 0 || prog >= P_NPROG) return set_error(CGL_EINVAL, "stage: unknown program");
   if (nf != 1 && nf != 2) return set_error(CGL_EINVAL, "stage: 1 or 2 components");
+  static_assert(sizeof(((StageArgs*)0)->in) / sizeof(void*) >= 10, "in[] holds 5 operands x 2 components");
   if ((nl->kind == 2) != (nf == 2)) return set_error(CGL_EINVAL, "stage: component count does not match kind");
   if (n <= 0) return 0;
   StageArgs a{};
