@@ -62,10 +62,17 @@ class FusedPlan:
         self.half, self.one = Fraction(1, 2), Fraction(1)
         mk = lambda: [torch.empty_like(like[0]) for _ in range(self.nf)]  # noqa: E731
         nstate = 2 if scheme_name in ("strang", "split4") else 1
-        self.U = [mk() for _ in range(nstate)]
         nbuf = {"if4": 6, "strang": 2, "split4": 4, "if2": 4}[scheme_name]
-        self.B = [mk() for _ in range(nbuf)]
         nwork = {"if4": 4, "strang": 1, "split4": 2, "if2": 2}[scheme_name]
+        # Lean mode for fields that do not fit batched: Tucker jobs run one at a
+        # time through a single scratch field (if4 on 1024^3: 8 x 17.2 GB).
+        field_bytes = 16 * self.n * self.nf
+        free, _ = torch.cuda.mem_get_info()
+        self.lean = (nstate + nbuf + nwork) * field_bytes > 0.85 * free
+        if self.lean:
+            nwork = 1
+        self.U = [mk() for _ in range(nstate)]
+        self.B = [mk() for _ in range(nbuf)]
         self.W = [t for _ in range(nwork) for t in mk()] if like[0].ndim > 1 else []
         self.graphs = {}
         self.flag = _lib.new_flag(1)   # baked into the captured graphs; reset per run
@@ -75,7 +82,12 @@ class FusedPlan:
 
     # -- launch helpers --------------------------------------------------------
     def _tucker(self, jobs, flag):
-        """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode."""
+        """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode
+        (lean mode: one job at a time through the single scratch field)."""
+        if self.lean and len(jobs) > 1:
+            for j in jobs:
+                self._tucker([j], flag)
+            return
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
             for c in range(self.nf):
