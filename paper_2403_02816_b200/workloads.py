@@ -124,6 +124,32 @@ def initial_state(w, seed=SEED):
     raise ValueError(w.ic)
 
 
+def initial_state_device(w, seed=SEED):
+    """Device-built u0 (CUDA complex128) for large grids.  gaussians8 is
+    separable per Gaussian, so it is assembled from 1D factors on the GPU with
+    the same parameters as initial_state (no 17 GB host array); the noise
+    recipes fall back to the host generator (bit-compatible stream)."""
+    import torch
+    if w.ic != "gaussians8":
+        return torch.from_numpy(initial_state(w, seed)).cuda()
+    a, b = w.interval
+    L = b - a
+    u = uniforms(seed, 48).reshape(8, 6)
+    ax = [torch.from_numpy(x).cuda() for x in axes(w)]
+    d = len(ax)
+    out = torch.zeros(w.extents, dtype=torch.complex128, device="cuda")
+    for cx, cy, cz, wd, ph, am in u:
+        centre = [a + L * (0.25 + 0.5 * c) for c in (cx, cy, cz)][:d]
+        width = 1.0 + 3.0 * wd
+        coef = (0.5 + am) * np.exp(2j * np.pi * ph)
+        f = [torch.exp(-((x - c) ** 2) / (2.0 * width ** 2)) for x, c in zip(ax, centre)]
+        term = f[0].to(torch.complex128) * coef
+        for i in range(1, d):
+            term = term.unsqueeze(-1) * f[i].reshape([1] * i + [-1])
+        out += term
+    return out
+
+
 def fd_matrices(w):
     """Per-direction A_mu = (a1 + i b1) D2 + (a2/d) I (host numpy)."""
     from .operators import fd2_second_derivative_dirichlet, fd2_second_derivative_neumann

@@ -17,8 +17,7 @@ steps = int(sys.argv[3]) if len(sys.argv) > 3 else w.steps
 if len(sys.argv) > 4:
     w = w.scaled(int(sys.argv[4]), steps)
 t0 = time.perf_counter()
-u0 = W.initial_state(w)
-x0 = torch.from_numpy(u0).cuda()
+x0 = W.initial_state_device(w)
 prob = W.build_problem(w)
 if w.boundary == "periodic":
     from paper_2403_02816_b200.spectral import fft_dev
