@@ -1,0 +1,191 @@
+"""Axis-0 slab sharding of the finite-difference path across ranks.
+
+One process per GPU (torch.distributed; NCCL on B200s, gloo for the CPU
+tests).  A 3D field of global shape (n0, n1, n2), C order, is split into
+contiguous slabs of n0/P planes along axis 0 (the slowest axis).  Every
+pointwise stage and the mu-mode products along axes 1..d-1 are local; the
+axis-0 product needs whole axis-0 fibres and is done by one all-to-all
+transpose each way:
+
+  to_columns:   (p0, n1*n2) slab  --pack-->  [P][p0][m]  --all_to_all-->  (n0, m)
+                (rank r receives every rank's planes of its column block r,
+                 stacked in source order = the global axis-0 order)
+  local GEMM:   Out (n0, m) = E0 (n0 x n0) * Cols (n0, m)       (DMMA, left form)
+  from_columns: rows of slab s are contiguous in Out -> all_to_all -> unpack
+                into (p0, P, m) = (p0, n1*n2)
+
+The per-rank send volume per transpose is 16 N (P-1)/P^2 bytes (an
+all-gather / reduce-scatter formulation would move P/2 times more).
+
+Divergence: each rank keeps its own sticky key; before every end-of-step
+kernel the keys are min-reduced across ranks (sign-flipped so the signed
+NCCL/gloo MIN orders them as unsigned), so every rank skips exactly the
+kernels the reference's single process would not have run, and all ranks
+return the same (diverged_at, reason).
+"""
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .plan import FusedPlan
+from .tensors import mode_product_dev
+
+_SIGN = -(1 << 63)
+
+
+class SlabLayout:
+    """Slab partition of a global shape along axis 0 over `world` ranks."""
+
+    def __init__(self, shape, world):
+        self.shape = tuple(int(n) for n in shape)
+        self.world = int(world)
+        n0 = self.shape[0]
+        rest = int(math.prod(self.shape[1:])) if len(self.shape) > 1 else 1
+        if n0 % self.world or rest % self.world:
+            raise ValueError(f"axis-0 slab sharding needs n0={n0} and prod(n1..)={rest} divisible by {self.world}")
+        self.n0, self.rest = n0, rest
+        self.p0 = n0 // self.world          # planes per rank
+        self.m = rest // self.world         # columns per rank after the transpose
+
+    def local_shape(self):
+        return (self.p0,) + self.shape[1:]
+
+    def bounds(self, rank):
+        return rank * self.p0, (rank + 1) * self.p0
+
+
+class Transposer:
+    """Owns the send/receive buffers of the axis-0 transposes."""
+
+    def __init__(self, layout, group=None, device=None, dtype=torch.complex128):
+        self.L = layout
+        self.group = group
+        P, p0, m = layout.world, layout.p0, layout.m
+        self.send = torch.empty((P, p0, m), dtype=dtype, device=device)
+        self.recv = torch.empty((P, p0, m), dtype=dtype, device=device)
+        self.cols_out = torch.empty((layout.n0, m), dtype=dtype, device=device)
+
+    def _a2a(self, out, inp):
+        if self.L.world == 1:
+            out.copy_(inp)
+        else:
+            dist.all_to_all_single(out.view(-1), inp.reshape(-1), group=self.group)
+
+    def to_columns(self, local):
+        """(p0, ...) slab -> (n0, m) column block of this rank."""
+        P, p0, m = self.L.world, self.L.p0, self.L.m
+        self.send.copy_(local.reshape(p0, P, m).transpose(0, 1))
+        self._a2a(self.recv, self.send)
+        return self.recv.view(self.L.n0, m)
+
+    def from_columns(self, cols, local_out):
+        """(n0, m) column block -> (p0, ...) slab (written into local_out)."""
+        P, p0, m = self.L.world, self.L.p0, self.L.m
+        self._a2a(self.recv, cols)
+        local_out.reshape(p0, P, m).copy_(self.recv.transpose(0, 1))
+        return local_out
+
+
+def mode0_sharded(local_in, mat, mat_t, local_out, tr, gemm=None, flag=None, pos=0):
+    """Axis-0 mu-mode product of a slab-sharded field."""
+    cols = tr.to_columns(local_in)
+    if gemm is None:
+        mode_product_dev(cols, mat, mat_t, 0, out=tr.cols_out, flag=flag, pos=pos)
+    else:
+        tr.cols_out.copy_(gemm(mat, cols))
+    return tr.from_columns(tr.cols_out, local_out)
+
+
+def tucker_sharded(local_in, mats, mats_t, out, work, tr, gemm=None, flag=None, pos=0):
+    """in x_0 M_0 x_1 M_1 ... on a slab: axis 0 through the transposes, the
+    rest local (same mode order as tensors.py:62-69)."""
+    d = local_in.ndim
+    cur = local_in
+    for axis in range(d):
+        dst = out if (d - axis) % 2 == 1 else work
+        if axis == 0:
+            mode0_sharded(cur, mats[0], mats_t[0], dst, tr, gemm=gemm, flag=flag, pos=pos)
+        else:
+            mode_product_dev(cur, mats[axis], mats_t[axis], axis, out=dst, flag=flag, pos=pos)
+        cur = dst
+    return out
+
+
+def global_min_key(flag, group=None):
+    """Min-reduce the sticky divergence key over ranks (unsigned order)."""
+    k = flag[0:1]
+    t = torch.bitwise_xor(k, _SIGN)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    k.copy_(torch.bitwise_xor(t, _SIGN))
+
+
+class ShardedPlan(FusedPlan):
+    """FusedPlan on the local slab: Tuckers through the axis-0 transposes, a
+    cross-rank key reduction before every end-of-step kernel, eager launches
+    (NCCL collectives are not captured)."""
+
+    CHUNK = 1 << 30  # never graph-capture
+
+    def __init__(self, problem, scheme_name, like, layout, group=None):
+        super().__init__(problem, scheme_name, like)
+        self.layout = layout
+        self.group = group
+        self.tr = Transposer(layout, group, device=like[0].device)
+        if not self.W:
+            self.W = [torch.empty_like(like[0]) for _ in range(self.nf)]
+
+    def _tucker(self, jobs, flag):
+        for f, fin, fout in jobs:
+            for c in range(self.nf):
+                m, mt = self.blocks[c].exp_factors(f)
+                tucker_sharded(fin[c], m, mt, fout[c], self.W[c], self.tr, flag=flag, pos=_lib.POS_DEVICE)
+
+    def _before_end(self, flag):
+        global_min_key(flag, self.group)
+
+    def _graph(self, k0, count, flag, tau):
+        raise RuntimeError("sharded plans run eagerly")
+
+    def run(self, u0, steps, tau, stop_at=(), on_stop=None, poll_chunks=1):
+        flag = self.flag
+        flag.copy_(self._flag0)
+        self.load_state(u0, tau)
+        self.prologue(flag, tau)
+        for k in range(1, steps + 1):
+            self.step(k, flag, tau)
+            if k in stop_at or k == steps or k % 16 == 0:
+                global_min_key(flag, self.group)
+                key = int(flag[0].item()) & ((1 << 64) - 1)
+                if key != _lib.NO_DIVERGENCE and (key >> 24) <= steps:
+                    return key
+                if k in stop_at and on_stop is not None:
+                    on_stop(k, self.result(k))
+        return _lib.NO_DIVERGENCE
+
+
+def integrate_sharded(problem, scheme_name, local_fields, t_final, steps, layout, group=None):
+    """Slab-sharded counterpart of integrate() for FD problems built on the
+    LOCAL slab's operator (the axis-0 factor is the global n0 x n0 matrix).
+    Returns (local result fields, diverged_at, reason, device_seconds)."""
+    from .integrators import SCHEMES
+    if scheme_name not in ("if4", "strang", "split4", "if2"):
+        raise ValueError(f"sharded path supports if4/strang/split4/if2, not {scheme_name!r}")
+    tau = t_final / steps
+    problem.prepare(tau, SCHEMES[scheme_name])
+    plan = ShardedPlan(problem, scheme_name, list(local_fields), layout, group)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    key = plan.run(list(local_fields), steps, tau)
+    ev1.record()
+    torch.cuda.synchronize()
+    dev_s = ev0.elapsed_time(ev1) / 1e3
+    if key == _lib.NO_DIVERGENCE:
+        return plan.result(steps), 0, "", dev_s
+    k_div, reason = key >> 24, key & 0xFF
+    out = plan.result(k_div) if reason == _lib.NONFINITE_STATE else plan.result(k_div - 1)
+    return out, int(k_div), _lib.REASONS[reason], dev_s

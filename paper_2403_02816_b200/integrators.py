@@ -427,10 +427,22 @@ def _integrate_fused(problem, scheme_name, u0, host, tau, steps, wanted, on_snap
     dev_s = ev0.elapsed_time(ev1) / 1e3
     if fkey == _lib.NO_DIVERGENCE:
         out = fp.result(steps)
-        return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
-                                 device_seconds=dev_s)
+        return IntegrationResult(_detach(out, host, cache, key), steps, tau, seconds, device_seconds=dev_s)
     k_div, reason = fkey >> 24, fkey & 0xFF
     out = fp.result(k_div) if reason == _lib.NONFINITE_STATE else fp.result(k_div - 1)
-    return IntegrationResult(tuple(to_host_if(f.clone(), host) for f in out), steps, tau, seconds,
+    return IntegrationResult(_detach(out, host, cache, key), steps, tau, seconds,
                              diverged=True, diverged_at=int(k_div), reason=_lib.REASONS[reason],
                              device_seconds=dev_s)
+
+
+def _detach(fields, host, cache, key):
+    """Result fields independent of the cached plan's buffers: host copies,
+    device clones, or -- when a clone does not fit (1024^3 fields) -- the
+    buffers themselves, handed over by dropping the plan from the cache."""
+    if host:
+        return tuple(f.cpu().numpy() for f in fields)
+    try:
+        return tuple(f.clone() for f in fields)
+    except torch.OutOfMemoryError:
+        cache.pop(key, None)
+        return tuple(fields)

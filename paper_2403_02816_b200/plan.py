@@ -107,6 +107,9 @@ class FusedPlan:
                                  tau, 1.0, _lib.ptr_array(fin), _lib.ptr_array(fout), _lib.flag_ptr(flag),
                                  _lib.POS_DEVICE), "cgl_stage")
 
+    def _before_end(self, flag):
+        """Hook before each end-of-step kernel (cross-rank key reduction)."""
+
     # -- scheme bodies -----------------------------------------------------------
     def state_after(self, k):
         return self.U[k % len(self.U)]
@@ -139,21 +142,25 @@ class FusedPlan:
             self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag)
             self._stage("if4_mid", [u2, a], [u2, a], flag, tau)          # g3 -> u2, s -> a
             self._tucker([(H, u2, x1), (H, a, x5)], flag)                 # d -> x1, e -> x5
+            self._before_end(flag)
             self._stage("if4_end", [b, c, x1, x5], [u, x1, x5], flag, tau)
         elif self.scheme == "if2":
             u = self.U[0]
             x, y, u2, o = B
             self._tucker([(O, x, u2), (O, y, o)], flag)
+            self._before_end(flag)
             self._stage("if2_end", [u2, o], [u, x, y], flag, tau)
         elif self.scheme == "strang":
             v, w = B
             self._tucker([(O, v, w)], flag)
+            self._before_end(flag)
             self._stage("strang_end", [w], [self.state_after(k), v], flag, tau)
         elif self.scheme == "split4":
             v, f, v2, f2 = B
             self._tucker([(O, v, v2), (H, f, f2)], flag)
             self._stage("split4_mid", [v2, f2], [v2, f2], flag, tau)      # coarse c -> v2, f -> f2
             self._tucker([(H, f2, v)], flag)                              # f3 -> v
+            self._before_end(flag)
             self._stage("split4_end", [v, v2], [self.state_after(k), v, f], flag, tau)
 
     # -- driver ------------------------------------------------------------------
