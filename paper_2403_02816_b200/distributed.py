@@ -99,15 +99,18 @@ def mode0_sharded(local_in, mat, mat_t, local_out, tr, gemm=None, flag=None, pos
     return tr.from_columns(tr.cols_out, local_out)
 
 
-def tucker_sharded(local_in, mats, mats_t, out, work, tr, gemm=None, flag=None, pos=0):
+def tucker_sharded(local_in, mats, mats_t, out, work, tr, gemm=None, local=None, flag=None, pos=0):
     """in x_0 M_0 x_1 M_1 ... on a slab: axis 0 through the transposes, the
-    rest local (same mode order as tensors.py:62-69)."""
+    rest local (same mode order as tensors.py:62-69).  `gemm`/`local` replace
+    the DMMA kernels (CPU multi-rank tests only)."""
     d = local_in.ndim
     cur = local_in
     for axis in range(d):
         dst = out if (d - axis) % 2 == 1 else work
         if axis == 0:
             mode0_sharded(cur, mats[0], mats_t[0], dst, tr, gemm=gemm, flag=flag, pos=pos)
+        elif local is not None:
+            dst.copy_(local(cur, mats[axis], axis))
         else:
             mode_product_dev(cur, mats[axis], mats_t[axis], axis, out=dst, flag=flag, pos=pos)
         cur = dst

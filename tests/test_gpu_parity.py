@@ -202,3 +202,39 @@ def test_c1_full_size(P, config_golden, scheme):
     assert np.array_equal(np.isfinite(res.fields[0]), fin)
     if fin.any():
         assert rel_l2(res.fields[0][fin], want[fin]) <= 1e-10
+
+
+@pytest.mark.parametrize("tag,scheme", [("C2s24_split4", "split4"), ("C4s24_if4", "if4")])
+def test_sharded_path_single_rank(P, config_golden, tag, scheme):
+    """The slab-sharded FD path (axis-0 transposes + cross-rank key
+    reduction) at world size 1 reproduces the reference's golden output."""
+    from paper_2403_02816_b200 import distributed as D
+    from paper_2403_02816_b200 import workloads as W
+    meta, arrays = config_golden
+    m = meta[tag]
+    w = W.CONFIGS[m["workload"].split("-")[0]].scaled(m["extents"][0], m["steps"])
+    prob = W.build_problem(w)
+    x0 = torch.from_numpy(W.initial_state(w)).cuda()
+    L = D.SlabLayout(w.extents, 1)
+    out, k_div, reason, _ = D.integrate_sharded(prob, scheme, [x0], w.t_final, w.steps, L)
+    assert k_div == m["diverged_at"]
+    assert rel_l2(out[0].cpu().numpy(), arrays[f"{tag}_out"]) <= 1e-10
+
+
+def test_lean_plan_matches_batched(P, config_golden, monkeypatch):
+    """Lean-memory plans (one Tucker job at a time, used for 1024^3 fields)
+    give the batched plan's result."""
+    from paper_2403_02816_b200 import plan as PL
+    from paper_2403_02816_b200 import workloads as W
+    meta, arrays = config_golden
+    m = meta["C4s24_if4"]
+    w = W.CONFIGS["C4"].scaled(24, m["steps"])
+    x0 = torch.from_numpy(W.initial_state(w)).cuda()
+    orig = PL.FusedPlan.__init__
+
+    def lean_init(self, *a, **k):
+        orig(self, *a, **k)
+        self.lean = True
+    monkeypatch.setattr(PL.FusedPlan, "__init__", lean_init)
+    res = P.integrate(W.build_problem(w), "if4", (x0,), w.t_final, w.steps)
+    assert rel_l2(res.fields[0].cpu().numpy(), arrays["C4s24_if4_out"]) <= 1e-10
