@@ -421,9 +421,13 @@ static int launch_big(const GemmArgs& a, int nitems, cudaStream_t s, int cfg) {
     case 3: return launch_cfg<32, 64, 16, 2, 4, 3, M3>(a, nitems, s);   // 16x16 warp tiles, 8 warps
     case 4: return launch_cfg<64, 32, 32, 4, 2, 3, M3>(a, nitems, s);   // BK = 32
     case 0: return launch_cfg<64, 64, 16, 2, 4, 3, M3>(a, nitems, s);   // 32x16 warp tiles, 8 warps
-    // default (measured best on B200, profiles/r01_zgemm_configs.txt): 64x64 CTA
-    // tile, 16 warps of 16x16, BK = 32, double-buffered, 1 CTA/SM (141 KB smem)
-    default: return launch_cfg<64, 64, 32, 4, 4, 2, M3>(a, nitems, s);
+    case 6: return launch_cfg<128, 64, 32, 4, 2, 2, M3>(a, nitems, s);  // 32x32 warp tiles, 8 warps
+    case 7: return launch_cfg<64, 64, 48, 4, 4, 2, M3>(a, nitems, s);   // BK = 48, 16 warps
+    case 5: return launch_cfg<64, 64, 32, 4, 4, 2, M3>(a, nitems, s);   // 16x16 warp tiles, 16 warps
+    case 9: return launch_cfg<32, 64, 32, 2, 4, 3, M3>(a, nitems, s);   // 16x16, 8 warps, 3 stages
+    // default (measured best on B200, profiles/r01_zgemm_configs.txt): 64x128 CTA
+    // tile, 8 warps of 32x32, BK = 32, double-buffered, 1 CTA/SM (207 KB smem)
+    default: return launch_cfg<64, 128, 32, 2, 4, 2, M3>(a, nitems, s);
   }
 }
 
