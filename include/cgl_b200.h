@@ -122,6 +122,30 @@ int cgl_tucker(void* stream, int ndim, const int64_t* shape, int nfields,
                const double* const* in, double* const* out,
                double* const* work, const cgl_flag_t* flag, uint64_t pos);
 
+/* ---- FP64-accurate complex GEMM on the INT8 tensor cores (Ozaki I) ------- */
+/* (csrc/ozgemm.cu) C = A B with complex A (M x K), B (K x N), computed from
+ * S int8 slices per operand on tcgen05 kind::i8 with TMEM accumulators.
+ * Operands are pre-sliced into the UMMA tile layout:
+ *   A side ("a_mode" = 1): slices of the complex M x K matrix A,
+ *   B side ("a_mode" = 0): slices of Z = B^T (N x K), i.e. rows = output columns.
+ * cgl_oz_slice reads complex Z(r, c) = src[r*sr + c*sc] (rows x cols, per
+ * batch + src_batch_stride), writes S slices (cgl_oz_slice_bytes per batch,
+ * zero-initialise once: padding is never written) and one exponent per row. */
+int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode);
+int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
+                 int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride,
+                 int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
+                 int64_t exp_batch_stride);
+/* nitems independent batched products (S = 7 or 8); C[f] + b*sC, element
+ * (i, j) at i*ldc + j (complex elements); strides of A/B slices in bytes,
+ * of exponents in ints. */
+int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems,
+                const int8_t* const* A, const int* const* Aexp,
+                const int8_t* const* B, const int* const* Bexp,
+                double* const* C, int64_t ldc, int64_t batch,
+                int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
+                const cgl_flag_t* flag, uint64_t pos);
+
 /* ---- pointwise kernels (HBM-bound) --------------------------------------- */
 
 /* out = sum_i coef[i] * x[i] (nterms <= 6, real coefficients) —

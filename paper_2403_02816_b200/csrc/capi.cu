@@ -26,6 +26,12 @@ int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double
 int fft_plan(int, const int64_t*, void**);
 int fft_exec(void*, cudaStream_t, const double*, double*, int);
 int fft_destroy(void*);
+int oz_slice(cudaStream_t, int, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int8_t*,
+             int64_t, int*, int64_t);
+int oz_gemm(cudaStream_t, int, int64_t, int64_t, int64_t, int, const int8_t* const*, const int* const*,
+            const int8_t* const*, const int* const*, double* const*, int64_t, int64_t, int64_t, int64_t, int64_t,
+            int64_t, int64_t, const cgl_flag_t*, uint64_t);
+int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
 
@@ -262,6 +268,25 @@ int cgl_stage_fourier(void* stream, int program, int nfields, int ndim, const in
   for (int d = 0; d < ndim; ++d) n *= shape[d];
   return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos, ndim, shape,
                       tables);
+}
+
+int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode) {
+  return oz_slice_bytes(S, rows, cols, a_mode, a_mode ? 128 : 64);
+}
+
+int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
+                 int64_t batch, int64_t src_batch_stride, int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
+                 int64_t exp_batch_stride) {
+  return oz_slice((cudaStream_t)stream, S, src, sr, sc, rows, cols, batch, src_batch_stride, a_mode, a_mode ? 128 : 64,
+                  out, out_batch_stride, exps, exp_batch_stride);
+}
+
+int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+                const int* const* Aexp, const int8_t* const* B, const int* const* Bexp, double* const* C, int64_t ldc,
+                int64_t batch, int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
+                const cgl_flag_t* flag, uint64_t pos) {
+  return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, B, Bexp, C, ldc, batch, sA, sAexp, sB, sBexp, sC,
+                 flag, pos);
 }
 
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }

@@ -1,0 +1,470 @@
+// FP64-accurate complex GEMM emulated on the INT8 tensor cores (tcgen05
+// kind::i8, TMEM accumulators) by exponent-aligned splitting (Ozaki scheme I).
+//
+// Why: B200's FP64 tensor path is warp-level DMMA at 37 TFLOP/s; the INT8
+// tcgen05 path is ~4.5 POPS dense.  A double with 53 mantissa bits is split
+// into S int8 "slices" of 7 bits each relative to a power-of-two scale shared
+// by its row (A operand) or column (B operand); slice products are exact in
+// INT32, and the products of slice pairs whose weights 2^-7(s+t) are below
+// 2^-7(S+1) are dropped.  For S = 8 the dropped/truncated terms are below
+// 2^-56 of (row max x column max) per product term, i.e. FP64-level error for
+// the dense exp(tau A) factors of the mu-mode products.
+//
+// Complex -> real: the complex product C = A B (M x K times K x N) is the
+// real product of
+//   Ahat (2M x 2K): row 2i = [.., Re a_ik, -Im a_ik, ..], row 2i+1 = [.., Im a_ik, Re a_ik, ..]
+//   Bhat (2K x N):  row 2k = Re b_k., row 2k+1 = Im b_k.
+// so Chat row 2i = Re c_i., row 2i+1 = Im c_i.  Bhat is stored transposed
+// (N x 2K, K-major) as UMMA wants both operands K-major.
+//
+// Operand slices are written by the slicing kernels directly in the UMMA
+// canonical no-swizzle K-major layout, tile by tile: a (rows x KC bytes) tile
+// is a grid of 8-row x 16-byte core matrices, [row group][k group][8][16], so
+// every pipeline stage is a handful of contiguous 1D bulk copies
+// (cp.async.bulk + mbarrier complete_tx) -- no tensor maps.
+//
+// GEMM kernel (one 128 x BN output tile of Chat per CTA, 6 warps):
+//   warp 0: producer -- per K chunk, S slices of A and S of B into a stage
+//   warp 1: MMA issuer -- for every slice pair (s, t) with s + t <= S + 1,
+//           tcgen05.mma into the TMEM accumulator of level d = s + t
+//           (S levels x BN int32 columns = 512 columns for S = 8, BN = 64)
+//   warps 2-5: epilogue -- per level, tcgen05.ld the int32 accumulator, add
+//           2^-7d * D_d in FP64, scale by 2^(e_row + e_col), write complex C.
+#include <cstdint>
+#include <cstdio>
+
+#include "cgl_common.cuh"
+#include "cgl_internal.h"
+
+namespace cgl {
+namespace oz {
+
+constexpr int BM = 128;  // UMMA M (rows of Chat per CTA)
+constexpr int KC = 64;   // K bytes per pipeline chunk (2 UMMA k-steps of 32)
+
+// ---- PTX helpers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols));
+}
+
+// no-swizzle K-major smem descriptor: LBO = K-direction core stride, SBO = 8-row group stride
+__device__ __forceinline__ uint64_t make_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  const uint32_t a = smem_u32(smem);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version = 1 (Blackwell)
+  // base_offset = 0, lbo_mode = 0, layout_type (bits 61-63) = 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// instruction descriptor: kind::i8, s8 x s8 -> s32, both K-major, M x N
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (2u << 4)                       // c_format = S32
+         | (1u << 7) | (1u << 10)         // a/b format = signed int8
+         | ((uint32_t)(N >> 3) << 17)     // n_dim
+         | ((uint32_t)(M >> 4) << 24);    // m_dim
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define LD32x32b_X32(r, taddr)                                                                              \
+  asm volatile(                                                                                             \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                       \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),           \
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),         \
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),         \
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                              \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// ---- operand slicing ---------------------------------------------------------
+// Tiled slice layout: [slice][row tile][k chunk][RT rows x KC bytes], each tile
+// as [row/8][kbyte/16][row%8][kbyte%16].  rows padded to RT, K to KC (zeros).
+__host__ __device__ inline int64_t tile_offset(int64_t R, int64_t kb, int RT, int nchunks) {
+  const int64_t rt = R / RT, r = R % RT, ch = kb / KC, kk = kb % KC;
+  return ((rt * nchunks + ch) * (int64_t)(RT * KC)) + (((r >> 3) * (KC / 16) + (kk >> 4)) * 8 + (r & 7)) * 16 +
+         (kk & 15);
+}
+
+struct SliceArgs {
+  const double2* src;   // complex matrix Z, element (r, c) at src[r*sr + c*sc]
+  int64_t sr, sc;
+  int64_t rows, cols;   // complex extents (rows of Z -> operand rows, cols -> K)
+  int a_mode;           // 1: A operand (2 real rows per complex row: [re,-im],[im,re]); 0: B operand ([re, im])
+  int S;
+  int RT;               // row tile (128 for A, BN for B)
+  int nchunks;          // K chunks per row tile (2*cols padded to KC)
+  int64_t rtiles;       // row tiles
+  int8_t* out;          // S * rtiles * nchunks * RT * KC bytes
+  int* exps;            // per complex row: scale exponent e (values scaled by 2^-e)
+};
+
+// one warp per complex row (blockIdx.y = batch): max -> exponent -> all S
+// slices in one pass, 16-byte packed stores into the tiled layout
+template <int S>
+__global__ void slice_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs, int64_t exp_bs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= a.rows) return;
+  const int64_t b = blockIdx.y;
+  const double2* z = a.src + b * src_bs + row * a.sr;
+  int8_t* outb = a.out + b * out_bs;
+  double m = 0.0;
+  for (int64_t c = lane; c < a.cols; c += 32) {
+    const double2 v = z[c * a.sc];
+    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);  // m = f 2^e, f in [0.5, 1): |x| 2^-e < 1
+  if (lane == 0) a.exps[b * exp_bs + row] = e;
+  const int64_t slice_stride = a.rtiles * a.nchunks * (int64_t)a.RT * KC;
+  const int nreal = a.a_mode ? 2 : 1;
+  const int64_t groups = (a.nchunks * (int64_t)KC) / 16;  // 8 complex per 16-byte group
+  for (int64_t gk = lane; gk < groups; gk += 32) {
+    double2 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = gk * 8 + j;
+      v[j] = c < a.cols ? z[c * a.sc] : make_double2(0.0, 0.0);
+    }
+    for (int part = 0; part < nreal; ++part) {
+      const int64_t R = a.a_mode ? 2 * row + part : row;
+      uint32_t w[S][4];
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) w[s][t] = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double x0, x1;
+        if (a.a_mode) {
+          x0 = part ? v[j].y : v[j].x;
+          x1 = part ? v[j].x : -v[j].y;
+        } else {
+          x0 = v[j].x;
+          x1 = v[j].y;
+        }
+        double r0 = ldexp(x0, -e), r1 = ldexp(x1, -e);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double v0 = r0 * 128.0, v1 = r1 * 128.0;
+          const double t0 = trunc(v0), t1 = trunc(v1);
+          r0 = v0 - t0;
+          r1 = v1 - t1;
+          const uint32_t b0 = (uint32_t)(uint8_t)(int8_t)(int)t0, b1 = (uint32_t)(uint8_t)(int8_t)(int)t1;
+          const int byte = 2 * j;  // bytes 2j, 2j+1 of the 16-byte group
+          w[s][byte >> 2] |= b0 << (8 * (byte & 3));
+          w[s][(byte + 1) >> 2] |= b1 << (8 * ((byte + 1) & 3));
+        }
+      }
+      const int64_t off = tile_offset(R, gk * 16, a.RT, a.nchunks);
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint4*>(outb + s * slice_stride + off) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    }
+  }
+}
+
+// ---- the emulated GEMM --------------------------------------------------------
+struct OzItem {
+  const int8_t* A;   // A-mode slices (batch stride sAb)
+  const int* Ae;     // per complex row exponents (batch stride sAeb)
+  const int8_t* B;   // B-mode slices (batch stride sBb)
+  const int* Be;     // per complex column exponents (batch stride sBeb)
+  double2* C;        // output (batch stride sCb), element (i, j) at i*ldc + j
+};
+
+struct OzArgs {
+  int64_t M, N;           // complex output extents
+  int mtiles, ntiles, nchunks;
+  int64_t sliceA, sliceB; // slice strides (bytes)
+  int64_t sAb, sAeb, sBb, sBeb, sCb, ldc;
+  int64_t batch;
+  const cgl_flag_t* flag;
+  uint64_t pos;
+  OzItem items[kMaxItems];
+};
+
+template <int S, int BN, int STAGES>
+struct OzCfg {
+  static constexpr int A_BYTES = BM * KC;                  // one slice tile of A per chunk
+  static constexpr int B_BYTES = BN * KC;
+  static constexpr int STAGE_BYTES = S * (A_BYTES + B_BYTES);
+  static constexpr int STG_BYTES = BM * (BN + 1) * 8;       // epilogue staging (reuses the stages)
+  static constexpr int BODY = STAGES * STAGE_BYTES > STG_BYTES ? STAGES * STAGE_BYTES : STG_BYTES;
+  static constexpr int SMEM = BODY + 256;                    // + barriers / tmem slot
+  static constexpr int LEVELS = S;                         // d = 2 .. S+1
+  static constexpr uint32_t TMEM_COLS = (S * BN <= 256) ? 256 : 512;
+  static_assert(S * BN <= 512, "levels x BN must fit the 512 TMEM columns");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+};
+
+template <int S, int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
+  using Cfg = OzCfg<S, BN, STAGES>;
+  if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BODY);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // decode (item, batch, tm, tn)
+  int64_t bid = blockIdx.x;
+  const int tn = (int)(bid % a.ntiles);
+  bid /= a.ntiles;
+  const int tm = (int)(bid % a.mtiles);
+  bid /= a.mtiles;
+  const int64_t b = bid % a.batch;
+  const int item = (int)(bid / a.batch);
+  const OzItem& it = a.items[item];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nch = a.nchunks;
+  if (warp == 0 && lane == 0) {
+    // ---- producer ----
+    const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * Cfg::A_BYTES;
+    const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * Cfg::B_BYTES;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % STAGES;
+      const uint32_t ph = (c / STAGES) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+      uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+      uint8_t* sb = sa + S * Cfg::A_BYTES;
+      for (int s = 0; s < S; ++s)
+        bulk_g2s(sa + s * Cfg::A_BYTES, A + s * a.sliceA + (int64_t)c * Cfg::A_BYTES, Cfg::A_BYTES, &full[st]);
+      for (int t = 0; t < S; ++t)
+        bulk_g2s(sb + t * Cfg::B_BYTES, B + t * a.sliceB + (int64_t)c * Cfg::B_BYTES, Cfg::B_BYTES, &full[st]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    constexpr uint32_t idesc = make_idesc(BM, BN);
+    constexpr uint32_t LBO = 128, SBO = (KC / 16) * 128;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % STAGES;
+      const uint32_t ph = (c / STAGES) & 1;
+      mbar_wait(&full[st], ph);
+      tc_fence_after();
+      const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+      const uint8_t* sb = sa + S * Cfg::A_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < KC / 32; ++ks) {
+#pragma unroll
+        for (int s = 1; s <= S; ++s) {
+          const uint64_t ad = make_desc(sa + (s - 1) * Cfg::A_BYTES + ks * 256, LBO, SBO);
+#pragma unroll
+          for (int t = 1; t <= S + 1 - s; ++t) {
+            const int level = s + t - 2;
+            const uint64_t bd = make_desc(sb + (t - 1) * Cfg::B_BYTES + ks * 256, LBO, SBO);
+            const uint32_t acc = (c == 0 && ks == 0 && s == 1) ? 0u : 1u;
+            mma_i8(tmem + level * BN, ad, bd, idesc, acc);
+          }
+        }
+      }
+      mma_commit(&empty[st]);  // frees the stage when these MMAs complete
+    }
+    mma_commit(tfull);
+  } else if (warp >= 2) {
+    // ---- epilogue ----
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    double acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.0;
+#pragma unroll 1
+    for (int level = S - 1; level >= 0; --level) {  // smallest weights first
+      const double w = ldexp(1.0, -7 * (level + 2));
+#pragma unroll
+      for (int h = 0; h < BN / 32; ++h) {
+        uint32_t r[32];
+        LD32x32b_X32(r, tmem + ((uint32_t)(q * 32) << 16) + level * BN + h * 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[h * 32 + j] = fma((double)(int)r[j], w, acc[h * 32 + j]);
+      }
+    }
+    // scale by 2^(e_row + e_col) and stage [row][col] in smem (stages are free now)
+    const int64_t R = (int64_t)tm * BM + row;  // real row of Chat
+    const int64_t i = R >> 1;
+    const int ea = (i < a.M) ? it.Ae[b * a.sAeb + i] : 0;
+    double* stg = reinterpret_cast<double*>(stage_base);
+#pragma unroll
+    for (int j = 0; j < BN; ++j) {
+      const int64_t col = (int64_t)tn * BN + j;
+      const int eb = (col < a.N) ? it.Be[b * a.sBeb + col] : 0;
+      stg[row * (BN + 1) + j] = ldexp(acc[j], ea + eb);
+    }
+    asm volatile("bar.sync 1, 128;\n" ::);
+    // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
+    double2* C = it.C + b * a.sCb;
+    const int et = threadIdx.x - 64;
+    for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
+      const int ii = idx / BN, j = idx % BN;
+      const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
+      if (gi < a.M && gj < a.N)
+        C[gi * a.ldc + gj] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  }
+}
+
+}  // namespace oz
+}  // namespace cgl
+
+namespace cgl {
+
+int oz_slice(cudaStream_t st, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
+             int64_t batch, int64_t src_bs, int a_mode, int RT, int8_t* out, int64_t out_bs, int* exps, int64_t exp_bs) {
+  if (S < 1 || S > 8) return set_error(CGL_EINVAL, "oz_slice: S must be 1..8");
+  if (rows <= 0 || cols <= 0 || batch <= 0) return 0;
+  oz::SliceArgs a{};
+  a.src = reinterpret_cast<const double2*>(src);
+  a.sr = sr;
+  a.sc = sc;
+  a.rows = rows;
+  a.cols = cols;
+  a.a_mode = a_mode;
+  a.S = S;
+  a.RT = RT;
+  a.nchunks = (int)((2 * cols + oz::KC - 1) / oz::KC);
+  a.rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
+  a.out = out;
+  a.exps = exps;
+  dim3 grid((unsigned)((rows + 7) / 8), (unsigned)batch);
+  switch (S) {
+    case 6: oz::slice_kernel<6><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 7: oz::slice_kernel<7><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 8: oz::slice_kernel<8><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    default: oz::slice_kernel<1><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+  }
+  return check_launch("oz_slice");
+}
+
+template <int S, int BN, int STAGES>
+static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
+  using Cfg = oz::OzCfg<S, BN, STAGES>;
+  auto kern = oz::ozgemm_kernel<S, BN, STAGES>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(ozgemm)");
+    init = true;
+  }
+  const int64_t blocks = (int64_t)a.mtiles * a.ntiles * a.batch * nitems;
+  if (blocks <= 0) return 0;
+  kern<<<(unsigned)blocks, 192, Cfg::SMEM, st>>>(a);
+  return check_launch("ozgemm_kernel");
+}
+
+int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+            const int* const* Ae, const int8_t* const* B, const int* const* Be, double* const* C, int64_t ldc,
+            int64_t batch, int64_t sAb, int64_t sAeb, int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag,
+            uint64_t pos) {
+  constexpr int BN = 64;
+  if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "oz_gemm: 1..8 items");
+  oz::OzArgs a{};
+  a.M = M;
+  a.N = N;
+  a.mtiles = (int)((2 * M + oz::BM - 1) / oz::BM);
+  a.ntiles = (int)((N + BN - 1) / BN);
+  a.nchunks = (int)((2 * K + oz::KC - 1) / oz::KC);
+  a.sliceA = (int64_t)a.mtiles * a.nchunks * oz::BM * oz::KC;
+  a.sliceB = (int64_t)a.ntiles * a.nchunks * BN * oz::KC;
+  a.sAb = sAb;
+  a.sAeb = sAeb;
+  a.sBb = sBb;
+  a.sBeb = sBeb;
+  a.sCb = sCb;
+  a.ldc = ldc;
+  a.batch = batch;
+  a.flag = flag;
+  a.pos = pos;
+  for (int f = 0; f < nitems; ++f)
+    a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f])};
+  switch (S) {
+    case 7: return oz_launch_cfg<7, BN, 2>(a, nitems, st);
+    case 8: return oz_launch_cfg<8, BN, 2>(a, nitems, st);
+    case 1: return oz_launch_cfg<1, BN, 2>(a, nitems, st);
+    default: return set_error(CGL_EINVAL, "oz_gemm: S must be 1, 7 or 8");
+  }
+}
+
+int64_t oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode, int RT) {
+  const int64_t nchunks = (2 * cols + oz::KC - 1) / oz::KC;
+  const int64_t rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
+  return (int64_t)S * rtiles * nchunks * RT * oz::KC;
+}
+
+}  // namespace cgl
