@@ -136,12 +136,17 @@ int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
                  int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride,
                  int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
                  int64_t exp_batch_stride);
+/* Block sparsity of a sliced CONSTANT operand: zmap[tile][chunk] = first
+ * non-zero slice (S+1: block all zero); rows/cols/a_mode as in cgl_oz_slice. */
+int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols,
+                int a_mode, int8_t* zmap);
 /* nitems independent batched products (S = 7 or 8); C[f] + b*sC, element
  * (i, j) at i*ldc + j (complex elements); strides of A/B slices in bytes,
- * of exponents in ints. */
+ * of exponents in ints.  Azmap/Bzmap (arrays of nitems, or NULL) let the
+ * kernel skip the zero slice blocks of a constant operand exactly. */
 int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems,
-                const int8_t* const* A, const int* const* Aexp,
-                const int8_t* const* B, const int* const* Bexp,
+                const int8_t* const* A, const int* const* Aexp, const int8_t* const* Azmap,
+                const int8_t* const* B, const int* const* Bexp, const int8_t* const* Bzmap,
                 double* const* C, int64_t ldc, int64_t batch,
                 int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
                 const cgl_flag_t* flag, uint64_t pos);

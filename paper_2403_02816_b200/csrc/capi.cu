@@ -29,8 +29,9 @@ int fft_destroy(void*);
 int oz_slice(cudaStream_t, int, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int8_t*,
              int64_t, int*, int64_t);
 int oz_gemm(cudaStream_t, int, int64_t, int64_t, int64_t, int, const int8_t* const*, const int* const*,
-            const int8_t* const*, const int* const*, double* const*, int64_t, int64_t, int64_t, int64_t, int64_t,
-            int64_t, int64_t, const cgl_flag_t*, uint64_t);
+            const int8_t* const*, const int8_t* const*, const int* const*, const int8_t* const*, double* const*,
+            int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const cgl_flag_t*, uint64_t);
+int oz_zmap(cudaStream_t, int, const int8_t*, int64_t, int64_t, int, int, int8_t*);
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
@@ -282,11 +283,15 @@ int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
 }
 
 int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-                const int* const* Aexp, const int8_t* const* B, const int* const* Bexp, double* const* C, int64_t ldc,
-                int64_t batch, int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
-                const cgl_flag_t* flag, uint64_t pos) {
-  return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, B, Bexp, C, ldc, batch, sA, sAexp, sB, sBexp, sC,
-                 flag, pos);
+                const int* const* Aexp, const int8_t* const* Azmap, const int8_t* const* B, const int* const* Bexp,
+                const int8_t* const* Bzmap, double* const* C, int64_t ldc, int64_t batch, int64_t sA, int64_t sAexp,
+                int64_t sB, int64_t sBexp, int64_t sC, const cgl_flag_t* flag, uint64_t pos) {
+  return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, Azmap, B, Bexp, Bzmap, C, ldc, batch, sA, sAexp,
+                 sB, sBexp, sC, flag, pos);
+}
+
+int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int8_t* zmap) {
+  return oz_zmap((cudaStream_t)stream, S, slices, rows, cols, a_mode, a_mode ? 128 : 64, zmap);
 }
 
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }

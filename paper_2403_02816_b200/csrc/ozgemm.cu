@@ -27,7 +27,11 @@
 //   warp 0: producer -- per K chunk, S slices of A and S of B into a stage
 //   warp 1: MMA issuer -- for every slice pair (s, t) with s + t <= S + 1,
 //           tcgen05.mma into the TMEM accumulator of level d = s + t
-//           (S levels x BN int32 columns = 512 columns for S = 8, BN = 64)
+//           (S levels x BN int32 columns = 512 columns for S = 8, BN = 64);
+//           the B slices of one A slice are issued as ONE wide MMA (N up to
+//           256) because their levels are consecutive -- this keeps the SMEM
+//           operand reads under the 128 B/clk port (ncu: the narrow-MMA
+//           version was bound by sm__mem_tensor_cycles at 93 %)
 //   warps 2-5: epilogue -- per level, tcgen05.ld the int32 accumulator, add
 //           2^-7d * D_d in FP64, scale by 2^(e_row + e_col), write complex C.
 #include <cstdint>
@@ -123,6 +127,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                              \
       : "r"(taddr))
 
+#define ST32x32b_X32(taddr, r)                                                                              \
+  asm volatile(                                                                                             \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),                    \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),   \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),       \
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),      \
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---- operand slicing ---------------------------------------------------------
@@ -214,6 +227,35 @@ __global__ void slice_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs, 
   }
 }
 
+// First non-zero slice (1..S, S+1 = all zero) of every (row tile, K chunk)
+// block of a sliced CONSTANT operand.  The exp(f tau A_mu) factors are
+// numerically banded, so far from the diagonal whole blocks are zero in all
+// S slices (entries below 2^-7S of the row max) and near it the leading
+// slices vanish first; the GEMM skips those loads and MMAs exactly.
+__global__ void zmap_kernel(const int8_t* sl, int S, int64_t slice_stride, int nchunks, int RT, int64_t nblocks,
+                            int8_t* z) {
+  const int64_t blk = blockIdx.x;  // = rt * nchunks + chunk
+  if (blk >= nblocks) return;
+  const int bytes = RT * KC;
+  __shared__ int first;
+  if (threadIdx.x == 0) first = S + 1;
+  __syncthreads();
+  for (int s = 0; s < S; ++s) {
+    const uint4* p = reinterpret_cast<const uint4*>(sl + s * slice_stride + blk * (int64_t)bytes);
+    int nz = 0;
+    for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) {
+      const uint4 v = p[i];
+      nz |= (v.x | v.y | v.z | v.w) != 0;
+    }
+    if (__syncthreads_or(nz)) {
+      if (threadIdx.x == 0) first = s + 1;
+      break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) z[blk] = (int8_t)first;
+}
+
 // ---- the emulated GEMM --------------------------------------------------------
 struct OzItem {
   const int8_t* A;   // A-mode slices (batch stride sAb)
@@ -221,6 +263,8 @@ struct OzItem {
   const int8_t* B;   // B-mode slices (batch stride sBb)
   const int* Be;     // per complex column exponents (batch stride sBeb)
   double2* C;        // output (batch stride sCb), element (i, j) at i*ldc + j
+  const int8_t* Az;  // optional [mtiles][nchunks] first non-zero A slice (constant operand), or null
+  const int8_t* Bz;  // optional [ntiles][nchunks] first non-zero B slice, or null
 };
 
 struct OzArgs {
@@ -283,46 +327,74 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp >= 2) {
+    // zero all level accumulators so every MMA accumulates (blocks may be skipped)
+    const uint32_t q = warp & 3;
+    uint32_t zr[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) zr[j] = 0u;
+#pragma unroll 1
+    for (int col = 0; col < S * BN; col += 32) ST32x32b_X32(tmem + (q * 32 << 16) + col, zr);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   const int nch = a.nchunks;
   if (warp == 0 && lane == 0) {
     // ---- producer ----
     const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * Cfg::A_BYTES;
     const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * Cfg::B_BYTES;
+    int it_n = 0;
     for (int c = 0; c < nch; ++c) {
-      const int st = c % STAGES;
-      const uint32_t ph = (c / STAGES) & 1;
+      const int za = it.Az ? it.Az[(int64_t)tm * nch + c] : 1;
+      const int zb = it.Bz ? it.Bz[(int64_t)tn * nch + c] : 1;
+      if (za + zb > S + 1) continue;  // every slice pair of this chunk is zero
+      const int st = it_n % STAGES;
+      const uint32_t ph = (it_n / STAGES) & 1;
+      ++it_n;
       mbar_wait(&empty[st], ph ^ 1);
-      mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+      const int na = S + 2 - zb - za, nb = S + 2 - za - zb;  // A slices za..S+1-zb, B slices zb..S+1-za
+      mbar_expect_tx(&full[st], na * Cfg::A_BYTES + nb * Cfg::B_BYTES);
       uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
       uint8_t* sb = sa + S * Cfg::A_BYTES;
-      for (int s = 0; s < S; ++s)
-        bulk_g2s(sa + s * Cfg::A_BYTES, A + s * a.sliceA + (int64_t)c * Cfg::A_BYTES, Cfg::A_BYTES, &full[st]);
-      for (int t = 0; t < S; ++t)
-        bulk_g2s(sb + t * Cfg::B_BYTES, B + t * a.sliceB + (int64_t)c * Cfg::B_BYTES, Cfg::B_BYTES, &full[st]);
+      for (int s = za; s <= S + 1 - zb; ++s)
+        bulk_g2s(sa + (s - 1) * Cfg::A_BYTES, A + (s - 1) * a.sliceA + (int64_t)c * Cfg::A_BYTES, Cfg::A_BYTES,
+                 &full[st]);
+      for (int t = zb; t <= S + 1 - za; ++t)
+        bulk_g2s(sb + (t - 1) * Cfg::B_BYTES, B + (t - 1) * a.sliceB + (int64_t)c * Cfg::B_BYTES, Cfg::B_BYTES,
+                 &full[st]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
-    constexpr uint32_t idesc = make_idesc(BM, BN);
     constexpr uint32_t LBO = 128, SBO = (KC / 16) * 128;
+    int it_n = 0;
     for (int c = 0; c < nch; ++c) {
-      const int st = c % STAGES;
-      const uint32_t ph = (c / STAGES) & 1;
+      const int za = it.Az ? it.Az[(int64_t)tm * nch + c] : 1;
+      const int zb = it.Bz ? it.Bz[(int64_t)tn * nch + c] : 1;
+      if (za + zb > S + 1) continue;
+      const int st = it_n % STAGES;
+      const uint32_t ph = (it_n / STAGES) & 1;
+      ++it_n;
       mbar_wait(&full[st], ph);
       tc_fence_after();
       const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
       const uint8_t* sb = sa + S * Cfg::A_BYTES;
 #pragma unroll
       for (int ks = 0; ks < KC / 32; ++ks) {
-#pragma unroll
-        for (int s = 1; s <= S; ++s) {
+        // For slice s of A, the B slices t = zb .. S+1-s are consecutive BN-row
+        // blocks of one K-major operand (same SBO), and their products land in
+        // consecutive level accumulators s+t-2: one MMA covers up to 256/BN
+        // slices (N <= 256), cutting the SMEM reads of A by that factor.
+#pragma unroll 1
+        for (int s = za; s <= S + 1 - zb; ++s) {
           const uint64_t ad = make_desc(sa + (s - 1) * Cfg::A_BYTES + ks * 256, LBO, SBO);
-#pragma unroll
-          for (int t = 1; t <= S + 1 - s; ++t) {
-            const int level = s + t - 2;
-            const uint64_t bd = make_desc(sb + (t - 1) * Cfg::B_BYTES + ks * 256, LBO, SBO);
-            const uint32_t acc = (c == 0 && ks == 0 && s == 1) ? 0u : 1u;
-            mma_i8(tmem + level * BN, ad, bd, idesc, acc);
+          constexpr int PER = 256 / BN;
+          for (int t0 = zb; t0 <= S + 1 - s; t0 += PER) {
+            const int cnt = (S + 2 - s - t0) < PER ? (S + 2 - s - t0) : PER;
+            const uint64_t bd = make_desc(sb + (t0 - 1) * Cfg::B_BYTES + ks * 256, LBO, SBO);
+            mma_i8(tmem + (s + t0 - 2) * BN, ad, bd, make_idesc(BM, cnt * BN), 1u);
           }
         }
       }
@@ -429,9 +501,9 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
 }
 
 int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-            const int* const* Ae, const int8_t* const* B, const int* const* Be, double* const* C, int64_t ldc,
-            int64_t batch, int64_t sAb, int64_t sAeb, int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag,
-            uint64_t pos) {
+            const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
+            const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
+            int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos) {
   constexpr int BN = 64;
   if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "oz_gemm: 1..8 items");
   oz::OzArgs a{};
@@ -452,13 +524,23 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   a.flag = flag;
   a.pos = pos;
   for (int f = 0; f < nitems; ++f)
-    a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f])};
+    a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
+                            Bz ? Bz[f] : nullptr};
   switch (S) {
     case 7: return oz_launch_cfg<7, BN, 2>(a, nitems, st);
     case 8: return oz_launch_cfg<8, BN, 2>(a, nitems, st);
     case 1: return oz_launch_cfg<1, BN, 2>(a, nitems, st);
     default: return set_error(CGL_EINVAL, "oz_gemm: S must be 1, 7 or 8");
   }
+}
+
+int oz_zmap(cudaStream_t st, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int RT, int8_t* z) {
+  const int64_t nchunks = (2 * cols + oz::KC - 1) / oz::KC;
+  const int64_t rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
+  const int64_t nblocks = rtiles * nchunks;
+  if (nblocks <= 0) return 0;
+  oz::zmap_kernel<<<(unsigned)nblocks, 256, 0, st>>>(slices, S, nblocks * RT * oz::KC, (int)nchunks, RT, nblocks, z);
+  return check_launch("oz_zmap");
 }
 
 int64_t oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode, int RT) {

@@ -22,17 +22,28 @@ def slices(Z, rows, cols, sr, sc, a_mode, S, batch=1, bs=0):
     return out, ex, nb
 
 
-def run(A, B, S, nitems=1, reps=0):
+def zmap(sl, rows, cols, a_mode, S):
+    rt = ((2 * rows if a_mode else rows) + (128 if a_mode else 64) - 1) // (128 if a_mode else 64)
+    z = torch.zeros(rt * ((2 * cols + 63) // 64), dtype=torch.int8, device="cuda")
+    _lib.check(lib.cgl_oz_zmap(_lib.stream(), S, _lib.ptr(sl), rows, cols, a_mode, _lib.ptr(z)), "zmap")
+    return z
+
+
+def run(A, B, S, nitems=1, reps=0, sparse_a=False, sparse_b=False):
     M, K = A.shape
     N = B.shape[1]
     As, Ae, _ = slices(A, M, K, K, 1, 1, S)
     Bs, Be, _ = slices(B, N, K, 1, N, 0, S)   # Z = B^T: Z(r=j, c=k) = B[k, j] at k*N + j
+    Az = zmap(As, M, K, 1, S) if sparse_a else None
+    Bz = zmap(Bs, N, K, 0, S) if sparse_b else None
     Cs = [torch.empty(M, N, dtype=torch.complex128, device="cuda") for _ in range(nitems)]
 
     def go():
         _lib.check(lib.cgl_oz_gemm(_lib.stream(), S, M, N, K, nitems, _lib.ptr_array([As] * nitems),
-                                   _lib.ptr_array([Ae] * nitems), _lib.ptr_array([Bs] * nitems),
-                                   _lib.ptr_array([Be] * nitems), _lib.ptr_array(Cs), N, 1, 0, 0, 0, 0, 0, None, 0),
+                                   _lib.ptr_array([Ae] * nitems), _lib.ptr_array([Az] * nitems) if Az is not None
+                                   else None, _lib.ptr_array([Bs] * nitems), _lib.ptr_array([Be] * nitems),
+                                   _lib.ptr_array([Bz] * nitems) if Bz is not None else None,
+                                   _lib.ptr_array(Cs), N, 1, 0, 0, 0, 0, 0, None, 0),
                    "oz_gemm")
     go()
     torch.cuda.synchronize()
@@ -70,3 +81,23 @@ for (M, K, N, nf) in [(512, 512, 512, 1), (512, 512, 512, 4), (256, 256, 65536, 
     err = ((C - want).abs().max() / want.abs().max()).item()
     print(json.dumps({"case": f"random S={S}", "shape": [M, K, N], "fields": nf, "rel_max_err": err,
                       "us": dt * 1e6, "equiv_tflops": 8.0 * M * K * N * nf / dt / 1e12}), flush=True)
+
+# 3. the C1 exponential factor (banded in the sliced representation): left and right forms
+from paper_2403_02816_b200 import workloads as W  # noqa: E402
+w = W.CONFIGS["C1"]
+op = W.build_problem(w).operator
+op.prepare(w.tau, (0.5, 1))
+E = op.exp_factors(1)[0][0]
+U = torch.randn(512, 512, dtype=torch.complex128, device="cuda", generator=g)
+for nf in (1, 4):
+    C, dt = run(E, U, S, nitems=nf, reps=10, sparse_a=True)
+    want = E @ U
+    err = ((C - want).abs().max() / want.abs().max()).item()
+    print(json.dumps({"case": f"E-left sparse S={S}", "fields": nf, "rel_max_err": err, "us": dt * 1e6,
+                      "equiv_tflops": 8.0 * 512 ** 3 * nf / dt / 1e12}), flush=True)
+    Et = E.t().contiguous()
+    C, dt = run(U, Et, S, nitems=nf, reps=10, sparse_b=True)
+    want = U @ Et
+    err = ((C - want).abs().max() / want.abs().max()).item()
+    print(json.dumps({"case": f"E-right sparse S={S}", "fields": nf, "rel_max_err": err, "us": dt * 1e6,
+                      "equiv_tflops": 8.0 * 512 ** 3 * nf / dt / 1e12}), flush=True)
