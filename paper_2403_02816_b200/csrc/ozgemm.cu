@@ -381,20 +381,28 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
       tc_fence_after();
       const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
       const uint8_t* sb = sa + S * Cfg::A_BYTES;
+      // descriptors differ only in the start-address field (16-byte units, no
+      // carry below 256 KB): build once per stage, then add byte offsets >> 4
+      const uint64_t ad0 = make_desc(sa, LBO, SBO), bd0 = make_desc(sb, LBO, SBO);
+      constexpr int PER = 256 / BN;
 #pragma unroll
       for (int ks = 0; ks < KC / 32; ++ks) {
         // For slice s of A, the B slices t = zb .. S+1-s are consecutive BN-row
         // blocks of one K-major operand (same SBO), and their products land in
         // consecutive level accumulators s+t-2: one MMA covers up to 256/BN
         // slices (N <= 256), cutting the SMEM reads of A by that factor.
-#pragma unroll 1
-        for (int s = za; s <= S + 1 - zb; ++s) {
-          const uint64_t ad = make_desc(sa + (s - 1) * Cfg::A_BYTES + ks * 256, LBO, SBO);
-          constexpr int PER = 256 / BN;
-          for (int t0 = zb; t0 <= S + 1 - s; t0 += PER) {
+#pragma unroll
+        for (int s = 1; s <= S; ++s) {
+          if (s < za || s > S + 1 - zb) continue;
+          const uint64_t ad = ad0 + (uint64_t)((((s - 1) * Cfg::A_BYTES) + ks * 256) >> 4);
+#pragma unroll
+          for (int blk = 0; blk < (S + PER - 1) / PER; ++blk) {
+            const int t0 = zb + blk * PER;
+            if (t0 > S + 1 - s) continue;
             const int cnt = (S + 2 - s - t0) < PER ? (S + 2 - s - t0) : PER;
-            const uint64_t bd = make_desc(sb + (t0 - 1) * Cfg::B_BYTES + ks * 256, LBO, SBO);
-            mma_i8(tmem + (s + t0 - 2) * BN, ad, bd, make_idesc(BM, cnt * BN), 1u);
+            const uint64_t bd = bd0 + (uint64_t)((((t0 - 1) * Cfg::B_BYTES) + ks * 256) >> 4);
+            const uint32_t idesc = make_idesc(BM, BN) + ((uint32_t)((cnt - 1) * BN) >> 3 << 17);
+            mma_i8(tmem + (s + t0 - 2) * BN, ad, bd, idesc, 1u);
           }
         }
       }

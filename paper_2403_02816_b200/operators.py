@@ -158,6 +158,7 @@ class KroneckerOperator:
             return  # same (tau, fractions): the cached exponentials are exact
         self._tau = tau
         self._cache = {}
+        self.__dict__.pop("_oz", None)
         _lib.require_cuda()
         for f in fr:
             step = float(f) * self._tau
@@ -177,6 +178,22 @@ class KroneckerOperator:
         if f not in self._cache:
             raise RuntimeError(f"exponential for fraction {f} not prepared; call prepare()")
         return self._cache[f]
+
+    def sliced_factors(self, fraction):
+        """INT8-tensor-core operand slices of exp(f tau A_mu) (ozaki.py), built
+        once per prepared fraction and shared between identical factors."""
+        f = Fraction(fraction)
+        mats, _ = self.exp_factors(f)
+        cache = self.__dict__.setdefault("_oz", {})
+        if f not in cache:
+            from .ozaki import SlicedFactor
+            seen, out = {}, []
+            for m in mats:
+                if id(m) not in seen:
+                    seen[id(m)] = SlicedFactor(m)
+                out.append(seen[id(m)])
+            cache[f] = out
+        return cache[f]
 
     # device-level (integrator) entry points
     def apply_dev(self, u, y=None, beta=0.0, flag=None, pos=0):

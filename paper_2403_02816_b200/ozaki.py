@@ -1,0 +1,141 @@
+"""mu-mode products on the INT8 tensor cores (csrc/ozgemm.cu, Ozaki scheme I).
+
+Each constant factor exp(f tau A_mu) is sliced ONCE at prepare time into
+S = 8 int8 slices in both operand roles (A side for the "left" form
+Out_b = E In_b, B side for the "right" form Out = In E^T of the contiguous
+axis), with its block-sparsity map (the factors are numerically banded, so
+whole slice blocks are exactly zero and skipped).  The data operand is
+sliced per product into a reusable workspace.  Accuracy: ~1e-15 relative
+per product (tools/oz_check.py; parity tests at 1e-10 after full runs).
+"""
+
+import math
+import os
+
+import torch
+
+from . import _lib
+
+S = 8
+
+
+def enabled():
+    return os.environ.get("CGL_GEMM", "oz") == "oz"
+
+
+def _nbytes(rows, cols, a_mode):
+    return _lib.load().cgl_oz_slice_bytes(S, rows, cols, a_mode)
+
+
+def _zmap_len(rows, cols, a_mode):
+    rt = 128 if a_mode else 64
+    return ((2 * rows if a_mode else rows) + rt - 1) // rt * ((2 * cols + 63) // 64)
+
+
+class SlicedFactor:
+    """Both operand roles of one square constant factor E (n x n)."""
+
+    def __init__(self, E):
+        lib = _lib.load()
+        n = E.shape[0]
+        self.n = n
+        st = _lib.stream()
+        # A role: slices of E (rows i, K = k)
+        self.A = torch.zeros(_nbytes(n, n, 1), dtype=torch.int8, device=E.device)
+        self.Ae = torch.empty(n, dtype=torch.int32, device=E.device)
+        _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(E), n, 1, n, n, 1, 0, 1, _lib.ptr(self.A), 0,
+                                    _lib.ptr(self.Ae), 0), "oz_slice(E, A)")
+        self.Az = torch.empty(_zmap_len(n, n, 1), dtype=torch.int8, device=E.device)
+        _lib.check(lib.cgl_oz_zmap(st, S, _lib.ptr(self.A), n, n, 1, _lib.ptr(self.Az)), "oz_zmap(A)")
+        # B role for Out = In E^T: Z = (E^T)^T = E, rows = output columns j, K = k
+        self.B = torch.zeros(_nbytes(n, n, 0), dtype=torch.int8, device=E.device)
+        self.Be = torch.empty(n, dtype=torch.int32, device=E.device)
+        _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(E), n, 1, n, n, 1, 0, 0, _lib.ptr(self.B), 0,
+                                    _lib.ptr(self.Be), 0), "oz_slice(E, B)")
+        self.Bz = torch.empty(_zmap_len(n, n, 0), dtype=torch.int8, device=E.device)
+        _lib.check(lib.cgl_oz_zmap(st, S, _lib.ptr(self.B), n, n, 0, _lib.ptr(self.Bz)), "oz_zmap(B)")
+
+
+class Workspace:
+    """Per-field data-slice buffers, grown on demand (zero-initialised once:
+    the padding bytes are never written)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key, nbytes, nexp, device):
+        b = self.bufs.get(key)
+        if b is None or b[0].numel() < nbytes or b[1].numel() < nexp:
+            b = (torch.zeros(nbytes, dtype=torch.int8, device=device),
+                 torch.empty(nexp, dtype=torch.int32, device=device))
+            self.bufs[key] = b
+        return b
+
+
+def fits(shape, nfields):
+    """Data-slice workspace for one mode of `nfields` fields must stay small
+    next to the fields themselves (1024^3 fields keep the DMMA path)."""
+    pts = math.prod(shape)
+    need = nfields * pts * 16 * S // 8 + (1 << 20)
+    free, _ = torch.cuda.mem_get_info()
+    return need < min(8 << 30, free // 4)
+
+
+def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
+    """outs[f] = ins[f] x_axis E_f for square E_f (SlicedFactor), one GEMM launch."""
+    lib = _lib.load()
+    st = _lib.stream()
+    shape = tuple(ins[0].shape)
+    nd = len(shape)
+    n = shape[axis]
+    P = math.prod(shape[:axis])
+    Q = math.prod(shape[axis + 1:])
+    nf = len(ins)
+    dev = ins[0].device
+    if Q > 1:
+        # left form per slab b: Out_b (n x Q) = E (n x n) In_b (n x Q); data on the B side,
+        # Z_b = In_b^T (Q x n): Z(r = q, c = k) = In_b[k, q] -> sr = 1, sc = Q
+        per = _nbytes(Q, n, 0)
+        Bs, Be = [], []
+        for f, x in enumerate(ins):
+            buf, ex = ws.get(("B", f), per * P, Q * P, dev)
+            _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(x), 1, Q, Q, n, P, n * Q, 0, _lib.ptr(buf), per,
+                                        _lib.ptr(ex), Q), "oz_slice(data, B)")
+            Bs.append(buf)
+            Be.append(ex)
+        rc = lib.cgl_oz_gemm(st, S, n, Q, n, nf,
+                             _lib.ptr_array([fc.A for fc in factors]), _lib.ptr_array([fc.Ae for fc in factors]),
+                             _lib.ptr_array([fc.Az for fc in factors]),
+                             _lib.ptr_array(Bs), _lib.ptr_array(Be), None,
+                             _lib.ptr_array(outs), Q, P, 0, 0, per, Q, n * Q, _lib.flag_ptr(flag), pos)
+        _lib.check(rc, "oz_gemm(left)")
+    else:
+        # right form: Out (P x n) = In (P x n) E^T; data on the A side (rows p, K = k)
+        per = _nbytes(P, n, 1)
+        As, Ae = [], []
+        for f, x in enumerate(ins):
+            buf, ex = ws.get(("A", f), per, P, dev)
+            _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(x), n, 1, P, n, 1, 0, 1, _lib.ptr(buf), 0,
+                                        _lib.ptr(ex), 0), "oz_slice(data, A)")
+            As.append(buf)
+            Ae.append(ex)
+        rc = lib.cgl_oz_gemm(st, S, P, n, n, nf, _lib.ptr_array(As), _lib.ptr_array(Ae), None,
+                             _lib.ptr_array([fc.B for fc in factors]), _lib.ptr_array([fc.Be for fc in factors]),
+                             _lib.ptr_array([fc.Bz for fc in factors]),
+                             _lib.ptr_array(outs), n, 1, 0, 0, 0, 0, 0, _lib.flag_ptr(flag), pos)
+        _lib.check(rc, "oz_gemm(right)")
+    return outs
+
+
+def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0):
+    """Tucker chains of up to 8 fields, one emulated GEMM launch per mode
+    (same mode order and ping-pong as cgl_tucker); `ws` is the caller's
+    Workspace (per plan: captured graphs keep its pointers)."""
+    nd = ins[0].ndim
+    src = list(ins)
+    for axis in range(nd):
+        to_out = (nd - axis) % 2 == 1
+        dst = outs if to_out else work
+        mode_product_oz(src, [fs[axis] for fs in factor_sets], dst, axis, ws, flag=flag, pos=pos)
+        src = dst
+    return outs

@@ -75,6 +75,10 @@ class FusedPlan:
         self.B = [mk() for _ in range(nbuf)]
         self.W = [t for _ in range(nwork) for t in mk()] if like[0].ndim > 1 else []
         self.graphs = {}
+        self.shape = tuple(like[0].shape)
+        self.use_oz = None
+        from .ozaki import Workspace
+        self.oz_ws = Workspace()
         self.flag = _lib.new_flag(1)   # baked into the captured graphs; reset per run
         self._flag0 = self.flag.clone()
         self.graph_launches = {}       # cgl kernels inside each captured graph
@@ -83,10 +87,28 @@ class FusedPlan:
     # -- launch helpers --------------------------------------------------------
     def _tucker(self, jobs, flag):
         """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode
-        (lean mode: one job at a time through the single scratch field)."""
+        (lean mode: one job at a time through the single scratch field).
+        Products run on the INT8 tensor cores (ozaki.py) unless CGL_GEMM=dmma
+        or the data-slice workspace would not fit; else on the DMMA kernel."""
         if self.lean and len(jobs) > 1:
             for j in jobs:
                 self._tucker([j], flag)
+            return
+        from . import ozaki
+        if self.use_oz is None:
+            self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
+        if self.use_oz:
+            ins, outs, facs = [], [], []
+            for f, fin, fout in jobs:
+                for c in range(self.nf):
+                    ins.append(fin[c])
+                    outs.append(fout[c])
+                    facs.append(self.blocks[c].sliced_factors(f))
+            work = self.W[:len(ins)] if self.W else None
+            for i in range(0, len(ins), 8):
+                sl = slice(i, i + 8)
+                ozaki.tucker_oz(ins[sl], facs[sl], outs[sl], work[sl] if work else None, self.oz_ws, flag=flag,
+                                pos=_lib.POS_DEVICE)
             return
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
