@@ -130,12 +130,19 @@ int cgl_tucker(void* stream, int ndim, const int64_t* shape, int nfields,
  *   B side ("a_mode" = 0): slices of Z = B^T (N x K), i.e. rows = output columns.
  * cgl_oz_slice reads complex Z(r, c) = src[r*sr + c*sc] (rows x cols, per
  * batch + src_batch_stride), writes S slices (cgl_oz_slice_bytes per batch,
- * zero-initialise once: padding is never written) and one exponent per row. */
+ * zero-initialise once: padding is never written) and one exponent per row.
+ * A row holding NaN/Inf gets the exponent 0x7fffffff and the GEMM returns
+ * NaN for its outputs (non-finite states propagate as in an FP64 GEMM). */
 int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode);
 int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
                  int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride,
                  int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
                  int64_t exp_batch_stride);
+/* The same for nitems equally shaped matrices in one launch pair. */
+int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* srcs,
+                       int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
+                       int64_t src_batch_stride, int a_mode, int8_t* const* outs,
+                       int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride);
 /* Block sparsity of a sliced CONSTANT operand: zmap[tile][chunk] = first
  * non-zero slice (S+1: block all zero); rows/cols/a_mode as in cgl_oz_slice. */
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols,

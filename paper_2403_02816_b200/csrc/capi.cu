@@ -32,6 +32,8 @@ int oz_gemm(cudaStream_t, int, int64_t, int64_t, int64_t, int, const int8_t* con
             const int8_t* const*, const int8_t* const*, const int* const*, const int8_t* const*, double* const*,
             int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const cgl_flag_t*, uint64_t);
 int oz_zmap(cudaStream_t, int, const int8_t*, int64_t, int64_t, int, int, int8_t*);
+int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                   int, int8_t* const*, int64_t, int* const*, int64_t);
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
@@ -288,6 +290,13 @@ int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems
                 int64_t sB, int64_t sBexp, int64_t sC, const cgl_flag_t* flag, uint64_t pos) {
   return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, Azmap, B, Bexp, Bzmap, C, ldc, batch, sA, sAexp,
                  sB, sBexp, sC, flag, pos);
+}
+
+int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* srcs, int64_t sr, int64_t sc,
+                       int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride, int a_mode,
+                       int8_t* const* outs, int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride) {
+  return oz_slice_multi((cudaStream_t)stream, S, nitems, srcs, sr, sc, rows, cols, batch, src_batch_stride, a_mode,
+                        outs, out_batch_stride, exps, exp_batch_stride);
 }
 
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int8_t* zmap) {

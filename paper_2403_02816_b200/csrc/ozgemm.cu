@@ -44,6 +44,8 @@ namespace cgl {
 namespace oz {
 
 constexpr int BM = 128;  // UMMA M (rows of Chat per CTA)
+constexpr int NONFINITE = 0x7fffffff;  // exponent marker: the row/column holds NaN/Inf
+                                       // -> its outputs are NaN (as an FP64 GEMM would give)
 constexpr int KC = 64;   // K bytes per pipeline chunk (2 UMMA k-steps of 32)
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -148,6 +150,9 @@ __host__ __device__ inline int64_t tile_offset(int64_t R, int64_t kb, int RT, in
 }
 
 struct SliceArgs {
+  const double2* srcs[8];  // per item (blockIdx.z = item * batch + b)
+  int8_t* outs[8];
+  int* expss[8];
   const double2* src;   // complex matrix Z, element (r, c) at src[r*sr + c*sc]
   int64_t sr, sc;
   int64_t rows, cols;   // complex extents (rows of Z -> operand rows, cols -> K)
@@ -155,75 +160,153 @@ struct SliceArgs {
   int S;
   int RT;               // row tile (128 for A, BN for B)
   int nchunks;          // K chunks per row tile (2*cols padded to KC)
+  int64_t cols_items;   // number of items (grid.z = items * batch)
   int64_t rtiles;       // row tiles
   int8_t* out;          // S * rtiles * nchunks * RT * KC bytes
   int* exps;            // per complex row: scale exponent e (values scaled by 2^-e)
 };
 
-// one warp per complex row (blockIdx.y = batch): max -> exponent -> all S
-// slices in one pass, 16-byte packed stores into the tiled layout
-template <int S>
-__global__ void slice_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs, int64_t exp_bs) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= a.rows) return;
-  const int64_t b = blockIdx.y;
-  const double2* z = a.src + b * src_bs + row * a.sr;
-  int8_t* outb = a.out + b * out_bs;
+// ---- coalesced two-pass slicing (used for the per-product data operand) ------
+// pass 1: per-row exponent e (max over the row's K entries, |x| 2^-e < 1).
+// Rows-contiguous inputs (the transposed data operand of the left form):
+// blocks of 32 rows x 8 column groups, each block covering a column range,
+// combined with an integer atomicMax (the frexp exponent is monotone in the
+// max); exps must be pre-set to a very negative value (0x80 bytes).
+__global__ void rowexp_rows_kernel(const SliceArgs a, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
+                                   int64_t src_bs, int64_t exp_bs, int64_t cspan) {
+  __shared__ double red[8][33];
+  const int64_t b = blockIdx.z % batch;
+  const int item = (int)(blockIdx.z / batch);
+  const double2* z = a.srcs[item] + b * src_bs;
+  int* exps = a.expss[item];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * 32 + tx;
+  const int64_t c0 = (int64_t)blockIdx.y * cspan, c1 = c0 + cspan < cols ? c0 + cspan : cols;
   double m = 0.0;
-  for (int64_t c = lane; c < a.cols; c += 32) {
-    const double2 v = z[c * a.sc];
+  if (r < rows) {
+#pragma unroll 4
+    for (int64_t c = c0 + ty; c < c1; c += 8) {
+      const double2 v = z[r + c * sc];
+      const double av = fmax(fabs(v.x), fabs(v.y));
+      m = (av != av || m != m) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, av);  // NaN sticks
+    }
+  }
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && r < rows) {
+    bool bad = !(m == m) || isinf(m);
+    for (int k = 1; k < 8; ++k) {
+      const double o = red[k][tx];
+      bad |= !(o == o) || isinf(o);
+      m = fmax(m, o);
+    }
+    if (bad) {
+      atomicMax(exps + b * exp_bs + r, NONFINITE);
+    } else if (m > 0.0) {
+      int e;
+      frexp(m, &e);
+      atomicMax(exps + b * exp_bs + r, e);
+    }
+  }
+}
+
+// K-contiguous rows: warp per row
+__global__ void rowexp_kernel(const SliceArgs a, int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
+                              int64_t src_bs, int64_t exp_bs) {
+  const int64_t b = blockIdx.y % batch;
+  const int item = (int)(blockIdx.y / batch);
+  const double2* z = a.srcs[item] + b * src_bs;
+  int* exps = a.expss[item];
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  double m = 0.0;
+  bool bad = false;
+  for (int64_t c = lane; c < cols; c += 32) {
+    const double2 v = z[r * sr + c * sc];
+    bad |= !isfinite(v.x) || !isfinite(v.y);
     m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
   }
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  bad = __any_sync(0xffffffffu, bad);
   int e = 0;
-  if (m > 0.0) frexp(m, &e);  // m = f 2^e, f in [0.5, 1): |x| 2^-e < 1
-  if (lane == 0) a.exps[b * exp_bs + row] = e;
+  if (m > 0.0) frexp(m, &e);
+  if (lane == 0) exps[b * exp_bs + r] = bad ? NONFINITE : e;
+}
+
+// pass 2: one CTA per (row tile, 32-complex K chunk, batch); the Z block is
+// staged through shared memory with loads coalesced along whichever of r / c
+// is contiguous, then each thread emits the S slices of one 16-byte group.
+template <int S>
+__global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
+                                                         int64_t exp_bs) {
+  constexpr int CC = KC / 2;             // complex columns per chunk (32)
+  const int CR = a.a_mode ? a.RT / 2 : a.RT;  // complex rows per tile (64)
+  __shared__ double2 blk[64][CC + 1];
+  const int64_t batch = a.rows ? gridDim.z / a.cols_items : 1;
+  const int64_t b = blockIdx.z % batch;
+  const int item = (int)(blockIdx.z / batch);
+  const int rt = blockIdx.x, ch = blockIdx.y;
+  const int64_t r0 = (int64_t)rt * CR, c0 = (int64_t)ch * CC;
+  const double2* z = a.srcs[item] + b * src_bs;
+  const int tid = threadIdx.x;
+  if (a.sc == 1) {
+    for (int i = tid; i < CR * CC; i += 256) {
+      const int rr = i / CC, cc = i % CC;
+      const int64_t r = r0 + rr, c = c0 + cc;
+      blk[rr][cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c] : make_double2(0.0, 0.0);
+    }
+  } else {
+    for (int i = tid; i < CR * CC; i += 256) {
+      const int rr = i % CR, cc = i / CR;
+      const int64_t r = r0 + rr, c = c0 + cc;
+      blk[rr][cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c * a.sc] : make_double2(0.0, 0.0);
+    }
+  }
+  __syncthreads();
   const int64_t slice_stride = a.rtiles * a.nchunks * (int64_t)a.RT * KC;
+  int8_t* outb = a.outs[item] + b * out_bs;
+  const int* exps = a.expss[item];
   const int nreal = a.a_mode ? 2 : 1;
-  const int64_t groups = (a.nchunks * (int64_t)KC) / 16;  // 8 complex per 16-byte group
-  for (int64_t gk = lane; gk < groups; gk += 32) {
-    double2 v[8];
+  // work item = (real row within tile, 16-byte group g of the 64-byte chunk)
+  for (int w = tid; w < CR * nreal * 4; w += 256) {
+    const int g = w & 3, rr_real = w >> 2;
+    const int rr = a.a_mode ? rr_real >> 1 : rr_real, part = a.a_mode ? rr_real & 1 : 0;
+    const int64_t r = r0 + rr;
+    if (r >= a.rows) continue;  // padding rows stay zero (buffer zeroed once)
+    const int e_raw = exps[b * exp_bs + r];
+    const bool nonfinite = e_raw == NONFINITE;
+    const int e = nonfinite ? 0 : e_raw;
+    uint32_t wv[S][4];
+#pragma unroll
+    for (int q = 0; q < S; ++q) wv[q][0] = wv[q][1] = wv[q][2] = wv[q][3] = 0u;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int64_t c = gk * 8 + j;
-      v[j] = c < a.cols ? z[c * a.sc] : make_double2(0.0, 0.0);
-    }
-    for (int part = 0; part < nreal; ++part) {
-      const int64_t R = a.a_mode ? 2 * row + part : row;
-      uint32_t w[S][4];
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) w[s][t] = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double x0, x1;
-        if (a.a_mode) {
-          x0 = part ? v[j].y : v[j].x;
-          x1 = part ? v[j].x : -v[j].y;
-        } else {
-          x0 = v[j].x;
-          x1 = v[j].y;
-        }
-        double r0 = ldexp(x0, -e), r1 = ldexp(x1, -e);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const double v0 = r0 * 128.0, v1 = r1 * 128.0;
-          const double t0 = trunc(v0), t1 = trunc(v1);
-          r0 = v0 - t0;
-          r1 = v1 - t1;
-          const uint32_t b0 = (uint32_t)(uint8_t)(int8_t)(int)t0, b1 = (uint32_t)(uint8_t)(int8_t)(int)t1;
-          const int byte = 2 * j;  // bytes 2j, 2j+1 of the 16-byte group
-          w[s][byte >> 2] |= b0 << (8 * (byte & 3));
-          w[s][(byte + 1) >> 2] |= b1 << (8 * ((byte + 1) & 3));
-        }
+      const double2 v = blk[rr][g * 8 + j];
+      double x0, x1;
+      if (a.a_mode) {
+        x0 = part ? v.y : v.x;
+        x1 = part ? v.x : -v.y;
+      } else {
+        x0 = v.x;
+        x1 = v.y;
       }
-      const int64_t off = tile_offset(R, gk * 16, a.RT, a.nchunks);
+      double q0 = nonfinite ? 0.0 : ldexp(x0, -e), q1 = nonfinite ? 0.0 : ldexp(x1, -e);
 #pragma unroll
-      for (int s = 0; s < S; ++s)
-        *reinterpret_cast<uint4*>(outb + s * slice_stride + off) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+      for (int q = 0; q < S; ++q) {
+        const double v0 = q0 * 128.0, v1 = q1 * 128.0;
+        const double t0 = trunc(v0), t1 = trunc(v1);
+        q0 = v0 - t0;
+        q1 = v1 - t1;
+        const uint32_t b0 = (uint32_t)(uint8_t)(int8_t)(int)t0, b1 = (uint32_t)(uint8_t)(int8_t)(int)t1;
+        wv[q][j >> 1] |= (b0 << (16 * (j & 1))) | (b1 << (16 * (j & 1) + 8));
+      }
     }
+    const int64_t R = a.a_mode ? 2 * r + part : r;
+    const int64_t off = tile_offset(R, (int64_t)ch * KC + g * 16, a.RT, a.nchunks);
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      *reinterpret_cast<uint4*>(outb + q * slice_stride + off) = make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
   }
 }
 
@@ -439,7 +522,8 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
     for (int j = 0; j < BN; ++j) {
       const int64_t col = (int64_t)tn * BN + j;
       const int eb = (col < a.N) ? it.Be[b * a.sBeb + col] : 0;
-      stg[row * (BN + 1) + j] = ldexp(acc[j], ea + eb);
+      stg[row * (BN + 1) + j] = (ea == NONFINITE || eb == NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                                     : ldexp(acc[j], ea + eb);
     }
     asm volatile("bar.sync 1, 128;\n" ::);
     // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
@@ -465,12 +549,19 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
 
 namespace cgl {
 
-int oz_slice(cudaStream_t st, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
-             int64_t batch, int64_t src_bs, int a_mode, int RT, int8_t* out, int64_t out_bs, int* exps, int64_t exp_bs) {
+int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs, int64_t sr, int64_t sc,
+                   int64_t rows, int64_t cols, int64_t batch, int64_t src_bs, int a_mode, int8_t* const* outs,
+                   int64_t out_bs, int* const* exps, int64_t exp_bs) {
   if (S < 1 || S > 8) return set_error(CGL_EINVAL, "oz_slice: S must be 1..8");
+  if (nitems < 1 || nitems > 8) return set_error(CGL_EINVAL, "oz_slice: 1..8 items");
   if (rows <= 0 || cols <= 0 || batch <= 0) return 0;
+  const int RT = a_mode ? 128 : 64;
   oz::SliceArgs a{};
-  a.src = reinterpret_cast<const double2*>(src);
+  for (int f = 0; f < nitems; ++f) {
+    a.srcs[f] = reinterpret_cast<const double2*>(srcs[f]);
+    a.outs[f] = outs[f];
+    a.expss[f] = exps[f];
+  }
   a.sr = sr;
   a.sc = sc;
   a.rows = rows;
@@ -480,16 +571,47 @@ int oz_slice(cudaStream_t st, int S, const double* src, int64_t sr, int64_t sc, 
   a.RT = RT;
   a.nchunks = (int)((2 * cols + oz::KC - 1) / oz::KC);
   a.rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
-  a.out = out;
-  a.exps = exps;
-  dim3 grid((unsigned)((rows + 7) / 8), (unsigned)batch);
+  a.cols_items = nitems;
+  const int64_t zdim = batch * nitems;
+  if (zdim > 65535) return set_error(CGL_ESHAPE, "oz_slice: batch x items too large");
+  // pass 1: exponents
+  if (sr == 1) {
+    for (int f = 0; f < nitems; ++f) {
+      cudaError_t e = cudaSuccess;
+      if (exp_bs == rows) {
+        e = cudaMemsetAsync(exps[f], 0x80, (size_t)batch * rows * sizeof(int), st);
+      } else {
+        for (int64_t bb = 0; bb < batch && e == cudaSuccess; ++bb)
+          e = cudaMemsetAsync(exps[f] + bb * exp_bs, 0x80, (size_t)rows * sizeof(int), st);
+      }
+      if (e != cudaSuccess) return set_cuda_error(e, "oz_slice memset");
+    }
+    const int64_t rblk = (rows + 31) / 32;
+    int64_t csplit = (4 * 148 + rblk * zdim - 1) / (rblk * zdim);
+    if (csplit < 1) csplit = 1;
+    if (csplit > (cols + 63) / 64) csplit = (cols + 63) / 64;
+    const int64_t cspan = (cols + csplit - 1) / csplit;
+    dim3 g1((unsigned)rblk, (unsigned)csplit, (unsigned)zdim);
+    oz::rowexp_rows_kernel<<<g1, 256, 0, st>>>(a, sc, rows, cols, batch, src_bs, exp_bs, cspan);
+  } else {
+    dim3 g1((unsigned)((rows + 7) / 8), (unsigned)zdim);
+    oz::rowexp_kernel<<<g1, 256, 0, st>>>(a, sr, sc, rows, cols, batch, src_bs, exp_bs);
+  }
+  int r = check_launch("oz_rowexp");
+  if (r) return r;
+  dim3 g2((unsigned)a.rtiles, (unsigned)a.nchunks, (unsigned)zdim);
   switch (S) {
-    case 6: oz::slice_kernel<6><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
-    case 7: oz::slice_kernel<7><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
-    case 8: oz::slice_kernel<8><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
-    default: oz::slice_kernel<1><<<grid, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 7: oz::slice_tile_kernel<7><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 8: oz::slice_tile_kernel<8><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    default: oz::slice_tile_kernel<1><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
   }
   return check_launch("oz_slice");
+}
+
+int oz_slice(cudaStream_t st, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
+             int64_t batch, int64_t src_bs, int a_mode, int RT, int8_t* out, int64_t out_bs, int* exps, int64_t exp_bs) {
+  (void)RT;
+  return oz_slice_multi(st, S, 1, &src, sr, sc, rows, cols, batch, src_bs, a_mode, &out, out_bs, &exps, exp_bs);
 }
 
 template <int S, int BN, int STAGES>

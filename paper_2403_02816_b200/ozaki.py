@@ -76,6 +76,8 @@ def fits(shape, nfields):
     """Data-slice workspace for one mode of `nfields` fields must stay small
     next to the fields themselves (1024^3 fields keep the DMMA path)."""
     pts = math.prod(shape)
+    if pts < (1 << 17):
+        return False  # small grids (C0 128^2) are launch-latency bound: the DMMA path is faster
     need = nfields * pts * 16 * S // 8 + (1 << 20)
     free, _ = torch.cuda.mem_get_info()
     return need < min(8 << 30, free // 4)
@@ -97,12 +99,12 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
         # Z_b = In_b^T (Q x n): Z(r = q, c = k) = In_b[k, q] -> sr = 1, sc = Q
         per = _nbytes(Q, n, 0)
         Bs, Be = [], []
-        for f, x in enumerate(ins):
+        for f in range(nf):
             buf, ex = ws.get(("B", f), per * P, Q * P, dev)
-            _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(x), 1, Q, Q, n, P, n * Q, 0, _lib.ptr(buf), per,
-                                        _lib.ptr(ex), Q), "oz_slice(data, B)")
             Bs.append(buf)
             Be.append(ex)
+        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), 1, Q, Q, n, P, n * Q, 0,
+                                          _lib.ptr_array(Bs), per, _lib.ptr_array(Be), Q), "oz_slice(data, B)")
         rc = lib.cgl_oz_gemm(st, S, n, Q, n, nf,
                              _lib.ptr_array([fc.A for fc in factors]), _lib.ptr_array([fc.Ae for fc in factors]),
                              _lib.ptr_array([fc.Az for fc in factors]),
@@ -113,12 +115,12 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
         # right form: Out (P x n) = In (P x n) E^T; data on the A side (rows p, K = k)
         per = _nbytes(P, n, 1)
         As, Ae = [], []
-        for f, x in enumerate(ins):
+        for f in range(nf):
             buf, ex = ws.get(("A", f), per, P, dev)
-            _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(x), n, 1, P, n, 1, 0, 1, _lib.ptr(buf), 0,
-                                        _lib.ptr(ex), 0), "oz_slice(data, A)")
             As.append(buf)
             Ae.append(ex)
+        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), n, 1, P, n, 1, 0, 1,
+                                          _lib.ptr_array(As), 0, _lib.ptr_array(Ae), 0), "oz_slice(data, A)")
         rc = lib.cgl_oz_gemm(st, S, P, n, n, nf, _lib.ptr_array(As), _lib.ptr_array(Ae), None,
                              _lib.ptr_array([fc.B for fc in factors]), _lib.ptr_array([fc.Be for fc in factors]),
                              _lib.ptr_array([fc.Bz for fc in factors]),

@@ -309,3 +309,30 @@ def test_c2_full_size_one_step_vs_oracle(P):
     mats = [p.diffusion * O.fd2_neumann(n, b - a) + (p.alpha2 / 3) * np.eye(n) for n in w.extents]
     ref = O.integrate(O.Prob([O.KronOp(mats)], w.kind, p), "split4", (u0,), w.tau, 1)
     assert rel_l2(res.fields[0], ref.fields[0]) <= 1e-12
+
+
+@pytest.mark.parametrize("gemm", ["oz", "dmma"])
+def test_nonfinite_input_propagates(P, gemm, monkeypatch):
+    """A NaN in the state must surface as "non-finite state" at step 1 on both
+    GEMM paths (the INT8-emulated GEMM marks non-finite rows and returns NaN
+    for their outputs, like an FP64 GEMM)."""
+    from paper_2403_02816_b200 import workloads as W
+    monkeypatch.setenv("CGL_GEMM", gemm)
+    w = W.CONFIGS["C1"]
+    u0 = W.initial_state(w)
+    u0[100, 200] = np.nan
+    res = P.integrate(W.build_problem(w), "if4", (u0,), w.tau * 4, 4)
+    assert res.diverged and res.diverged_at == 1 and res.reason == "non-finite state"
+
+
+def test_oz_and_dmma_paths_agree(P, monkeypatch):
+    """The INT8-emulated and the DMMA mu-mode products give the same C1 if4
+    trajectory to ~1e-14 (both are ~1e-15 per product)."""
+    from paper_2403_02816_b200 import workloads as W
+    w = W.CONFIGS["C1"]
+    u0 = W.initial_state(w)
+    out = {}
+    for gemm in ("oz", "dmma"):
+        monkeypatch.setenv("CGL_GEMM", gemm)
+        out[gemm] = P.integrate(W.build_problem(w), "if4", (u0,), w.tau * 40, 40).fields[0]
+    assert rel_l2(out["oz"], out["dmma"]) <= 1e-12
