@@ -141,3 +141,16 @@ def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0):
         mode_product_oz(src, [fs[axis] for fs in factor_sets], dst, axis, ws, flag=flag, pos=pos)
         src = dst
     return outs
+
+
+def executed_macs_left(factor, ntiles_n, nfields):
+    """INT8 MACs one left-form launch executes (block-sparse A = factor slices,
+    dense data B): sum over (row tile, chunk) of the surviving slice pairs."""
+    z = factor.Az.cpu().numpy().astype(int)
+    pairs = ((S + 1 - z) * (S + 2 - z) // 2) * (z <= S)
+    return int(pairs.sum()) * 128 * 64 * 64 * ntiles_n * nfields
+
+
+def dense_macs(M, N, K, nfields):
+    """INT8 MACs of the same product without block skipping (S(S+1)/2 pairs)."""
+    return (S * (S + 1) // 2) * (2 * M) * N * (2 * K) * nfields
