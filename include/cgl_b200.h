@@ -143,6 +143,9 @@ int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* src
                        int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
                        int64_t src_batch_stride, int a_mode, int8_t* const* outs,
                        int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride);
+/* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last
+ * cgl_oz_gemm records phase timestamps (ns); copies 64 slots to host64. */
+int cgl_oz_trace(long long* host64);
 /* Block sparsity of a sliced CONSTANT operand: zmap[tile][chunk] = first
  * non-zero slice (S+1: block all zero); rows/cols/a_mode as in cgl_oz_slice. */
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols,

@@ -24,6 +24,7 @@ int pw_symexp(cudaStream_t, int64_t, double, const double*, double*);
 int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double, const double*, double*,
                  const cgl_flag_t*, uint64_t);
 int fft_plan(int, const int64_t*, void**);
+extern long long* g_oz_trace;
 int fft_exec(void*, cudaStream_t, const double*, double*, int);
 int fft_destroy(void*);
 int oz_slice(cudaStream_t, int, const double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int8_t*,
@@ -297,6 +298,12 @@ int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* src
                        int8_t* const* outs, int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride) {
   return oz_slice_multi((cudaStream_t)stream, S, nitems, srcs, sr, sc, rows, cols, batch, src_batch_stride, a_mode,
                         outs, out_batch_stride, exps, exp_batch_stride);
+}
+
+int cgl_oz_trace(long long* host64) {
+  if (!g_oz_trace) return -1;
+  cudaError_t e = cudaMemcpy(host64, g_oz_trace, 64 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int8_t* zmap) {

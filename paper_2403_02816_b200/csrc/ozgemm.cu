@@ -36,6 +36,7 @@
 //           2^-7d * D_d in FP64, scale by 2^(e_row + e_col), write complex C.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
@@ -46,7 +47,7 @@ namespace oz {
 constexpr int BM = 128;  // UMMA M (rows of Chat per CTA)
 constexpr int NONFINITE = 0x7fffffff;  // exponent marker: the row/column holds NaN/Inf
                                        // -> its outputs are NaN (as an FP64 GEMM would give)
-constexpr int KC = 64;   // K bytes per pipeline chunk (2 UMMA k-steps of 32)
+constexpr int KC = 64;   // K bytes per pipeline chunk (2 UMMA k-steps of 32 int8)
 
 // ---- PTX helpers -------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -268,9 +269,10 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item];
   const int nreal = a.a_mode ? 2 : 1;
-  // work item = (real row within tile, 16-byte group g of the 64-byte chunk)
-  for (int w = tid; w < CR * nreal * 4; w += 256) {
-    const int g = w & 3, rr_real = w >> 2;
+  // work item = (real row within tile, 16-byte group g of the KC-byte chunk)
+  constexpr int NG = KC / 16;
+  for (int w = tid; w < CR * nreal * NG; w += 256) {
+    const int g = w % NG, rr_real = w / NG;
     const int rr = a.a_mode ? rr_real >> 1 : rr_real, part = a.a_mode ? rr_real & 1 : 0;
     const int64_t r = r0 + rr;
     if (r >= a.rows) continue;  // padding rows stay zero (buffer zeroed once)
@@ -358,8 +360,17 @@ struct OzArgs {
   int64_t batch;
   const cgl_flag_t* flag;
   uint64_t pos;
+  long long* trace;  // optional: CTA 0 phase timestamps (globaltimer ns), see OZ_TRACE
   OzItem items[kMaxItems];
 };
+
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define OZ_TRACE(slot) \
+  do { if (a.trace && blockIdx.x == 0) a.trace[slot] = gtime(); } while (0)
 
 template <int S, int BN, int STAGES>
 struct OzCfg {
@@ -397,6 +408,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
   const int item = (int)(bid / a.batch);
   const OzItem& it = a.items[item];
 
+  if (threadIdx.x == 0) OZ_TRACE(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -423,6 +435,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) OZ_TRACE(1);
 
   const int nch = a.nchunks;
   if (warp == 0 && lane == 0) {
@@ -438,6 +451,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
       const uint32_t ph = (it_n / STAGES) & 1;
       ++it_n;
       mbar_wait(&empty[st], ph ^ 1);
+      if (it_n <= 16) OZ_TRACE(2 + it_n);  // producer: chunk issue times (slots 3..18)
       const int na = S + 2 - zb - za, nb = S + 2 - za - zb;  // A slices za..S+1-zb, B slices zb..S+1-za
       mbar_expect_tx(&full[st], na * Cfg::A_BYTES + nb * Cfg::B_BYTES);
       uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
@@ -462,6 +476,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
       ++it_n;
       mbar_wait(&full[st], ph);
       tc_fence_after();
+      if (it_n <= 16) OZ_TRACE(18 + it_n);  // MMA: chunk data-ready times (slots 19..34)
       const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
       const uint8_t* sb = sa + S * Cfg::A_BYTES;
       // descriptors differ only in the start-address field (16-byte units, no
@@ -498,6 +513,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
     const int row = q * 32 + lane;
     mbar_wait(tfull, 0);
     tc_fence_after();
+    if (threadIdx.x == 64) OZ_TRACE(40);
     double acc[BN];
 #pragma unroll
     for (int j = 0; j < BN; ++j) acc[j] = 0.0;
@@ -526,6 +542,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
                                                                      : ldexp(acc[j], ea + eb);
     }
     asm volatile("bar.sync 1, 128;\n" ::);
+    if (threadIdx.x == 64) OZ_TRACE(41);
     // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
     double2* C = it.C + b * a.sCb;
     const int et = threadIdx.x - 64;
@@ -538,6 +555,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) OZ_TRACE(42);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, Cfg::TMEM_COLS);
@@ -548,6 +566,8 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
 }  // namespace cgl
 
 namespace cgl {
+
+long long* g_oz_trace = nullptr;
 
 int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs, int64_t sr, int64_t sc,
                    int64_t rows, int64_t cols, int64_t batch, int64_t src_bs, int a_mode, int8_t* const* outs,
@@ -653,6 +673,16 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   a.batch = batch;
   a.flag = flag;
   a.pos = pos;
+  {
+    static long long* trace = nullptr;
+    const char* e = getenv("CGL_OZ_TRACE");
+    if (e && e[0] == '1') {
+      if (!trace) cudaMalloc(&trace, 64 * sizeof(long long));
+      cudaMemsetAsync(trace, 0, 64 * sizeof(long long), st);
+      a.trace = trace;
+      g_oz_trace = trace;
+    }
+  }
   for (int f = 0; f < nitems; ++f)
     a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
                             Bz ? Bz[f] : nullptr};

@@ -17,6 +17,7 @@ import torch
 from . import _lib
 
 S = 8
+KC = 32  # K bytes per chunk (csrc/ozgemm.cu oz::KC)
 
 
 def enabled():
@@ -29,7 +30,7 @@ def _nbytes(rows, cols, a_mode):
 
 def _zmap_len(rows, cols, a_mode):
     rt = 128 if a_mode else 64
-    return ((2 * rows if a_mode else rows) + rt - 1) // rt * ((2 * cols + 63) // 64)
+    return ((2 * rows if a_mode else rows) + rt - 1) // rt * ((2 * cols + KC - 1) // KC)
 
 
 class SlicedFactor:
@@ -148,7 +149,7 @@ def executed_macs_left(factor, ntiles_n, nfields):
     dense data B): sum over (row tile, chunk) of the surviving slice pairs."""
     z = factor.Az.cpu().numpy().astype(int)
     pairs = ((S + 1 - z) * (S + 2 - z) // 2) * (z <= S)
-    return int(pairs.sum()) * 128 * 64 * 64 * ntiles_n * nfields
+    return int(pairs.sum()) * 128 * 64 * KC * ntiles_n * nfields
 
 
 def dense_macs(M, N, K, nfields):
