@@ -231,7 +231,8 @@ def gemm_roofline(torch, w, scheme_fields=4):
                                    None, _lib.ptr_array(outs), Q, 1, 0, 0, per, Q, n * Q, None, 0), "oz_gemm")
     dt = _time(torch, gemm_only)
     dt_with_slicing = _time(torch, lambda: ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws))
-    macs = ozaki.executed_macs_left(fac, (Q + 63) // 64, scheme_fields)
+    bn = ozaki.geometry()[1]
+    macs = ozaki.executed_macs_left(fac, (Q + bn - 1) // bn, scheme_fields)
     dense = ozaki.dense_macs(n, Q, n, scheme_fields)
     # live FP64 DMMA peak
     stream = _lib.stream()

@@ -143,6 +143,8 @@ int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* src
                        int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
                        int64_t src_batch_stride, int a_mode, int8_t* const* outs,
                        int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride);
+/* Tile geometry of the emulated GEMM: A row tile, B row tile, K chunk bytes. */
+int cgl_oz_geometry(int* bm, int* bn, int* kc);
 /* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last
  * cgl_oz_gemm records phase timestamps (ns); copies 64 slots to host64. */
 int cgl_oz_trace(long long* host64);

@@ -275,13 +275,13 @@ int cgl_stage_fourier(void* stream, int program, int nfields, int ndim, const in
 }
 
 int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode) {
-  return oz_slice_bytes(S, rows, cols, a_mode, a_mode ? 128 : 64);
+  return oz_slice_bytes(S, rows, cols, a_mode, a_mode ? kOzBM : kOzBN);
 }
 
 int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
                  int64_t batch, int64_t src_batch_stride, int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
                  int64_t exp_batch_stride) {
-  return oz_slice((cudaStream_t)stream, S, src, sr, sc, rows, cols, batch, src_batch_stride, a_mode, a_mode ? 128 : 64,
+  return oz_slice((cudaStream_t)stream, S, src, sr, sc, rows, cols, batch, src_batch_stride, a_mode, a_mode ? kOzBM : kOzBN,
                   out, out_batch_stride, exps, exp_batch_stride);
 }
 
@@ -300,6 +300,13 @@ int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* src
                         outs, out_batch_stride, exps, exp_batch_stride);
 }
 
+int cgl_oz_geometry(int* bm, int* bn, int* kc) {
+  *bm = kOzBM;
+  *bn = kOzBN;
+  *kc = kOzKC;
+  return 0;
+}
+
 int cgl_oz_trace(long long* host64) {
   if (!g_oz_trace) return -1;
   cudaError_t e = cudaMemcpy(host64, g_oz_trace, 64 * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -307,7 +314,7 @@ int cgl_oz_trace(long long* host64) {
 }
 
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int8_t* zmap) {
-  return oz_zmap((cudaStream_t)stream, S, slices, rows, cols, a_mode, a_mode ? 128 : 64, zmap);
+  return oz_zmap((cudaStream_t)stream, S, slices, rows, cols, a_mode, a_mode ? kOzBM : kOzBN, zmap);
 }
 
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan) { return fft_plan(ndim, shape, plan); }

@@ -10,6 +10,11 @@ namespace cgl {
 
 constexpr int kMaxItems = 8;
 
+// INT8-emulated GEMM (ozgemm.cu) tile geometry, shared by the slicing layout
+constexpr int kOzBM = 128;  // A-operand row tile (UMMA M)
+constexpr int kOzBN = 32;   // B-operand row tile (output columns per CTA)
+constexpr int kOzKC = 32;   // K bytes per pipeline chunk
+
 struct GemmItem {
   const double* A;
   const double* B;

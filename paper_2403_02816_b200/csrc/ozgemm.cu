@@ -44,10 +44,10 @@
 namespace cgl {
 namespace oz {
 
-constexpr int BM = 128;  // UMMA M (rows of Chat per CTA)
+constexpr int BM = kOzBM;  // UMMA M (rows of Chat per CTA)
 constexpr int NONFINITE = 0x7fffffff;  // exponent marker: the row/column holds NaN/Inf
                                        // -> its outputs are NaN (as an FP64 GEMM would give)
-constexpr int KC = 64;   // K bytes per pipeline chunk (2 UMMA k-steps of 32 int8)
+constexpr int KC = kOzKC;  // K bytes per pipeline chunk (UMMA k-steps of 32 int8)
 
 // ---- PTX helpers -------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -139,14 +139,24 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),      \
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
 
+// 2^e as a double for any frexp exponent (normal range by bit construction,
+// subnormal results via one extra exact scaling)
+__device__ __forceinline__ double pow2(int e) {
+  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
+  if (e > 1023) return __longlong_as_double(0x7ff0000000000000ll);
+  return __longlong_as_double((long long)(e + 64 + 1023) << 52) * 5.421010862427522e-20;  // * 2^-64
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---- operand slicing ---------------------------------------------------------
-// Tiled slice layout: [slice][row tile][k chunk][RT rows x KC bytes], each tile
+// Tiled slice layout: [row tile][k chunk][slice][RT rows x KC bytes], each tile
 // as [row/8][kbyte/16][row%8][kbyte%16].  rows padded to RT, K to KC (zeros).
-__host__ __device__ inline int64_t tile_offset(int64_t R, int64_t kb, int RT, int nchunks) {
+// Blocks are slice-major inside: [row tile][k chunk][slice][RT x KC], so the
+// slices a pipeline stage needs are ONE contiguous range (one bulk copy).
+__host__ __device__ inline int64_t tile_offset(int64_t R, int64_t kb, int RT, int nchunks, int S) {
   const int64_t rt = R / RT, r = R % RT, ch = kb / KC, kk = kb % KC;
-  return ((rt * nchunks + ch) * (int64_t)(RT * KC)) + (((r >> 3) * (KC / 16) + (kk >> 4)) * 8 + (r & 7)) * 16 +
+  return ((rt * nchunks + ch) * S * (int64_t)(RT * KC)) + (((r >> 3) * (KC / 16) + (kk >> 4)) * 8 + (r & 7)) * 16 +
          (kk & 15);
 }
 
@@ -242,7 +252,7 @@ template <int S>
 __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
                                                          int64_t exp_bs) {
   constexpr int CC = KC / 2;             // complex columns per chunk (32)
-  const int CR = a.a_mode ? a.RT / 2 : a.RT;  // complex rows per tile (64)
+  const int CR = a.a_mode ? a.RT / 2 : a.RT;  // complex rows per tile (<= 64)
   __shared__ double2 blk[64][CC + 1];
   const int64_t batch = a.rows ? gridDim.z / a.cols_items : 1;
   const int64_t b = blockIdx.z % batch;
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
     }
   }
   __syncthreads();
-  const int64_t slice_stride = a.rtiles * a.nchunks * (int64_t)a.RT * KC;
+  const int64_t slice_stride = (int64_t)a.RT * KC;  // slices are adjacent within a block
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item];
   const int nreal = a.a_mode ? 2 : 1;
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
       }
     }
     const int64_t R = a.a_mode ? 2 * r + part : r;
-    const int64_t off = tile_offset(R, (int64_t)ch * KC + g * 16, a.RT, a.nchunks);
+    const int64_t off = tile_offset(R, (int64_t)ch * KC + g * 16, a.RT, a.nchunks, S);
 #pragma unroll
     for (int q = 0; q < S; ++q)
       *reinterpret_cast<uint4*>(outb + q * slice_stride + off) = make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
@@ -326,7 +336,7 @@ __global__ void zmap_kernel(const int8_t* sl, int S, int64_t slice_stride, int n
   if (threadIdx.x == 0) first = S + 1;
   __syncthreads();
   for (int s = 0; s < S; ++s) {
-    const uint4* p = reinterpret_cast<const uint4*>(sl + s * slice_stride + blk * (int64_t)bytes);
+    const uint4* p = reinterpret_cast<const uint4*>(sl + (blk * S + s) * (int64_t)bytes);
     int nz = 0;
     for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) {
       const uint4 v = p[i];
@@ -355,7 +365,6 @@ struct OzItem {
 struct OzArgs {
   int64_t M, N;           // complex output extents
   int mtiles, ntiles, nchunks;
-  int64_t sliceA, sliceB; // slice strides (bytes)
   int64_t sAb, sAeb, sBb, sBeb, sCb, ldc;
   int64_t batch;
   const cgl_flag_t* flag;
@@ -387,7 +396,7 @@ struct OzCfg {
 };
 
 template <int S, int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
+__global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(const OzArgs a) {
   using Cfg = OzCfg<S, BN, STAGES>;
   if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -440,8 +449,8 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
   const int nch = a.nchunks;
   if (warp == 0 && lane == 0) {
     // ---- producer ----
-    const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * Cfg::A_BYTES;
-    const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * Cfg::B_BYTES;
+    const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * S * Cfg::A_BYTES;
+    const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * S * Cfg::B_BYTES;
     int it_n = 0;
     for (int c = 0; c < nch; ++c) {
       const int za = it.Az ? it.Az[(int64_t)tm * nch + c] : 1;
@@ -456,12 +465,11 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
       mbar_expect_tx(&full[st], na * Cfg::A_BYTES + nb * Cfg::B_BYTES);
       uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
       uint8_t* sb = sa + S * Cfg::A_BYTES;
-      for (int s = za; s <= S + 1 - zb; ++s)
-        bulk_g2s(sa + (s - 1) * Cfg::A_BYTES, A + (s - 1) * a.sliceA + (int64_t)c * Cfg::A_BYTES, Cfg::A_BYTES,
-                 &full[st]);
-      for (int t = zb; t <= S + 1 - za; ++t)
-        bulk_g2s(sb + (t - 1) * Cfg::B_BYTES, B + (t - 1) * a.sliceB + (int64_t)c * Cfg::B_BYTES, Cfg::B_BYTES,
-                 &full[st]);
+      // one bulk copy per operand: slices za .. S+1-zb of A, zb .. S+1-za of B
+      bulk_g2s(sa + (za - 1) * Cfg::A_BYTES, A + ((int64_t)c * S + (za - 1)) * Cfg::A_BYTES, na * Cfg::A_BYTES,
+               &full[st]);
+      bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES, nb * Cfg::B_BYTES,
+               &full[st]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
@@ -513,7 +521,7 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
     const int row = q * 32 + lane;
     mbar_wait(tfull, 0);
     tc_fence_after();
-    if (threadIdx.x == 64) OZ_TRACE(40);
+    if (lane == 0) OZ_TRACE(48 + (warp - 2));  // per epilogue warp: tmem-full seen (slots 48..51)
     double acc[BN];
 #pragma unroll
     for (int j = 0; j < BN; ++j) acc[j] = 0.0;
@@ -529,18 +537,24 @@ __global__ void __launch_bounds__(192, 1) ozgemm_kernel(const OzArgs a) {
         for (int j = 0; j < 32; ++j) acc[h * 32 + j] = fma((double)(int)r[j], w, acc[h * 32 + j]);
       }
     }
-    // scale by 2^(e_row + e_col) and stage [row][col] in smem (stages are free now)
+    if (lane == 0) OZ_TRACE(44 + (warp - 2));  // per epilogue warp: level loop done (slots 44..47)
+    // scale by 2^(e_row + e_col) (exact power-of-two multiplies, column scales
+    // broadcast from smem) and stage [row][col] in smem (stages are free now)
+    __shared__ double colscale[BN];
+    const int ct = threadIdx.x - 64;
+    if (ct < BN) {
+      const int64_t col = (int64_t)tn * BN + ct;
+      const int eb = (col < a.N) ? it.Be[b * a.sBeb + col] : 0;
+      colscale[ct] = eb == NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(eb);
+    }
+    asm volatile("bar.sync 1, 128;\n" ::);
     const int64_t R = (int64_t)tm * BM + row;  // real row of Chat
     const int64_t i = R >> 1;
     const int ea = (i < a.M) ? it.Ae[b * a.sAeb + i] : 0;
+    const double rs = ea == NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ea);
     double* stg = reinterpret_cast<double*>(stage_base);
 #pragma unroll
-    for (int j = 0; j < BN; ++j) {
-      const int64_t col = (int64_t)tn * BN + j;
-      const int eb = (col < a.N) ? it.Be[b * a.sBeb + col] : 0;
-      stg[row * (BN + 1) + j] = (ea == NONFINITE || eb == NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll)
-                                                                     : ldexp(acc[j], ea + eb);
-    }
+    for (int j = 0; j < BN; ++j) stg[row * (BN + 1) + j] = (acc[j] * rs) * colscale[j];
     asm volatile("bar.sync 1, 128;\n" ::);
     if (threadIdx.x == 64) OZ_TRACE(41);
     // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
@@ -575,7 +589,7 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   if (S < 1 || S > 8) return set_error(CGL_EINVAL, "oz_slice: S must be 1..8");
   if (nitems < 1 || nitems > 8) return set_error(CGL_EINVAL, "oz_slice: 1..8 items");
   if (rows <= 0 || cols <= 0 || batch <= 0) return 0;
-  const int RT = a_mode ? 128 : 64;
+  const int RT = a_mode ? kOzBM : kOzBN;
   oz::SliceArgs a{};
   for (int f = 0; f < nitems; ++f) {
     a.srcs[f] = reinterpret_cast<const double2*>(srcs[f]);
@@ -654,7 +668,7 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
             const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
             const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
             int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos) {
-  constexpr int BN = 64;
+  constexpr int BN = kOzBN;
   if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "oz_gemm: 1..8 items");
   oz::OzArgs a{};
   a.M = M;
@@ -662,8 +676,6 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   a.mtiles = (int)((2 * M + oz::BM - 1) / oz::BM);
   a.ntiles = (int)((N + BN - 1) / BN);
   a.nchunks = (int)((2 * K + oz::KC - 1) / oz::KC);
-  a.sliceA = (int64_t)a.mtiles * a.nchunks * oz::BM * oz::KC;
-  a.sliceB = (int64_t)a.ntiles * a.nchunks * BN * oz::KC;
   a.sAb = sAb;
   a.sAeb = sAeb;
   a.sBb = sBb;
@@ -699,7 +711,7 @@ int oz_zmap(cudaStream_t st, int S, const int8_t* slices, int64_t rows, int64_t 
   const int64_t rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
   const int64_t nblocks = rtiles * nchunks;
   if (nblocks <= 0) return 0;
-  oz::zmap_kernel<<<(unsigned)nblocks, 256, 0, st>>>(slices, S, nblocks * RT * oz::KC, (int)nchunks, RT, nblocks, z);
+  oz::zmap_kernel<<<(unsigned)nblocks, 256, 0, st>>>(slices, S, 0, (int)nchunks, RT, nblocks, z);
   return check_launch("oz_zmap");
 }
 

@@ -17,7 +17,13 @@ import torch
 from . import _lib
 
 S = 8
-KC = 32  # K bytes per chunk (csrc/ozgemm.cu oz::KC)
+
+
+def geometry():
+    """(A row tile, B row tile, K chunk bytes) of the compiled kernel."""
+    bm, bn, kc = _lib.c_int(), _lib.c_int(), _lib.c_int()
+    _lib.load().cgl_oz_geometry(_lib.ctypes.byref(bm), _lib.ctypes.byref(bn), _lib.ctypes.byref(kc))
+    return bm.value, bn.value, kc.value
 
 
 def enabled():
@@ -29,8 +35,9 @@ def _nbytes(rows, cols, a_mode):
 
 
 def _zmap_len(rows, cols, a_mode):
-    rt = 128 if a_mode else 64
-    return ((2 * rows if a_mode else rows) + rt - 1) // rt * ((2 * cols + KC - 1) // KC)
+    bm, bn, kc = geometry()
+    rt = bm if a_mode else bn
+    return ((2 * rows if a_mode else rows) + rt - 1) // rt * ((2 * cols + kc - 1) // kc)
 
 
 class SlicedFactor:
@@ -149,7 +156,8 @@ def executed_macs_left(factor, ntiles_n, nfields):
     dense data B): sum over (row tile, chunk) of the surviving slice pairs."""
     z = factor.Az.cpu().numpy().astype(int)
     pairs = ((S + 1 - z) * (S + 2 - z) // 2) * (z <= S)
-    return int(pairs.sum()) * 128 * 64 * KC * ntiles_n * nfields
+    bm, bn, kc = geometry()
+    return int(pairs.sum()) * bm * bn * kc * ntiles_n * nfields
 
 
 def dense_macs(M, N, K, nfields):

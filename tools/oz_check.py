@@ -23,8 +23,8 @@ def slices(Z, rows, cols, sr, sc, a_mode, S, batch=1, bs=0):
 
 
 def zmap(sl, rows, cols, a_mode, S):
-    rt = ((2 * rows if a_mode else rows) + (128 if a_mode else 64) - 1) // (128 if a_mode else 64)
-    z = torch.zeros(rt * ((2 * cols + 31) // 32), dtype=torch.int8, device="cuda")
+    from paper_2403_02816_b200 import ozaki
+    z = torch.zeros(ozaki._zmap_len(rows, cols, a_mode), dtype=torch.int8, device="cuda")
     _lib.check(lib.cgl_oz_zmap(_lib.stream(), S, _lib.ptr(sl), rows, cols, a_mode, _lib.ptr(z)), "zmap")
     return z
 

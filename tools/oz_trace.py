@@ -25,6 +25,8 @@ lib.cgl_oz_trace(buf)
 t0 = buf[0]
 names = {0: "start", 1: "setup done (barriers, TMEM alloc+zero)", 40: "epilogue: tmem full", 41: "epilogue: staged",
          42: "end"}
+names.update({44 + i: f"epilogue warp {i + 2}: levels done" for i in range(4)})
+names.update({48 + i: f"epilogue warp {i + 2}: tmem full seen" for i in range(4)})
 for i in range(64):
     if buf[i]:
         lab = names.get(i, f"producer chunk {i - 2}" if 3 <= i <= 18 else f"mma chunk {i - 18} ready")
