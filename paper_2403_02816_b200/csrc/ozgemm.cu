@@ -245,80 +245,87 @@ __global__ void rowexp_kernel(const SliceArgs a, int64_t sr, int64_t sc, int64_t
   if (lane == 0) exps[b * exp_bs + r] = bad ? NONFINITE : e;
 }
 
-// pass 2: one CTA per (row tile, 32-complex K chunk, batch); the Z block is
-// staged through shared memory with loads coalesced along whichever of r / c
-// is contiguous, then each thread emits the S slices of one 16-byte group.
+// pass 2: one CTA per (row tile, CPB consecutive K chunks, item x batch).
+// The Z block is staged through shared memory with loads coalesced along
+// whichever of r / c is contiguous; each value is scaled ONCE to a 56-bit
+// integer q = trunc(x 2^(56-e)) (exact power-of-two scale, truncation toward
+// zero = the Ozaki digit truncation) and its S base-128 digits are peeled
+// off with integer shifts (sign applied to every digit).
+constexpr int CPB = 4;  // K chunks per CTA
+
+__device__ __forceinline__ void digits8(double x, int e, uint32_t (&w)[8][4], int byte) {
+  const double sc = __longlong_as_double((long long)(56 - e + 1023) << 52);  // 2^(56-e), e in (-966, 1079)
+  long long q = (long long)(x * sc);                                         // |q| < 2^56
+  const bool neg = q < 0;
+  unsigned long long m = neg ? (unsigned long long)(-q) : (unsigned long long)q;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int d = (int)((m >> (7 * (7 - s))) & 127ull);
+    const uint32_t v = (uint32_t)(uint8_t)(int8_t)(neg ? -d : d);
+    w[s][byte >> 2] |= v << (8 * (byte & 3));
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
                                                          int64_t exp_bs) {
-  constexpr int CC = KC / 2;             // complex columns per chunk (32)
-  const int CR = a.a_mode ? a.RT / 2 : a.RT;  // complex rows per tile (<= 64)
-  __shared__ double2 blk[64][CC + 1];
-  const int64_t batch = a.rows ? gridDim.z / a.cols_items : 1;
+  constexpr int CC = KC / 2;              // complex columns per chunk
+  constexpr int W = CC * CPB;             // complex columns per CTA
+  extern __shared__ double2 blk_dyn[];    // [CR][W + 1]
+  const int CR = a.a_mode ? a.RT / 2 : a.RT;
+  const int64_t batch = gridDim.z / a.cols_items;
   const int64_t b = blockIdx.z % batch;
   const int item = (int)(blockIdx.z / batch);
-  const int rt = blockIdx.x, ch = blockIdx.y;
-  const int64_t r0 = (int64_t)rt * CR, c0 = (int64_t)ch * CC;
+  const int rt = blockIdx.x, ch0 = blockIdx.y * CPB;
+  const int64_t r0 = (int64_t)rt * CR, c0 = (int64_t)ch0 * CC;
   const double2* z = a.srcs[item] + b * src_bs;
   const int tid = threadIdx.x;
   if (a.sc == 1) {
-    for (int i = tid; i < CR * CC; i += 256) {
-      const int rr = i / CC, cc = i % CC;
+    for (int i = tid; i < CR * W; i += 256) {
+      const int rr = i / W, cc = i % W;
       const int64_t r = r0 + rr, c = c0 + cc;
-      blk[rr][cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c] : make_double2(0.0, 0.0);
+      blk_dyn[rr * (W + 1) + cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c] : make_double2(0.0, 0.0);
     }
   } else {
-    for (int i = tid; i < CR * CC; i += 256) {
+    for (int i = tid; i < CR * W; i += 256) {
       const int rr = i % CR, cc = i / CR;
       const int64_t r = r0 + rr, c = c0 + cc;
-      blk[rr][cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c * a.sc] : make_double2(0.0, 0.0);
+      blk_dyn[rr * (W + 1) + cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c * a.sc] : make_double2(0.0, 0.0);
     }
   }
   __syncthreads();
-  const int64_t slice_stride = (int64_t)a.RT * KC;  // slices are adjacent within a block
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item];
   const int nreal = a.a_mode ? 2 : 1;
-  // work item = (real row within tile, 16-byte group g of the KC-byte chunk)
-  constexpr int NG = KC / 16;
-  for (int w = tid; w < CR * nreal * NG; w += 256) {
-    const int g = w % NG, rr_real = w / NG;
+  constexpr int NG = KC / 16;               // 16-byte groups per chunk
+  const int groups = CPB * NG;
+  for (int w = tid; w < CR * nreal * groups; w += 256) {
+    const int gg = w % groups, rr_real = w / groups;
     const int rr = a.a_mode ? rr_real >> 1 : rr_real, part = a.a_mode ? rr_real & 1 : 0;
     const int64_t r = r0 + rr;
-    if (r >= a.rows) continue;  // padding rows stay zero (buffer zeroed once)
+    const int ch = ch0 + gg / NG, g = gg % NG;
+    if (r >= a.rows || ch >= a.nchunks) continue;  // padding stays zero (buffer zeroed once)
     const int e_raw = exps[b * exp_bs + r];
     const bool nonfinite = e_raw == NONFINITE;
-    const int e = nonfinite ? 0 : e_raw;
-    uint32_t wv[S][4];
+    uint32_t wv[8][4];
 #pragma unroll
-    for (int q = 0; q < S; ++q) wv[q][0] = wv[q][1] = wv[q][2] = wv[q][3] = 0u;
+    for (int q = 0; q < 8; ++q) wv[q][0] = wv[q][1] = wv[q][2] = wv[q][3] = 0u;
+    if (!nonfinite) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double2 v = blk[rr][g * 8 + j];
-      double x0, x1;
-      if (a.a_mode) {
-        x0 = part ? v.y : v.x;
-        x1 = part ? v.x : -v.y;
-      } else {
-        x0 = v.x;
-        x1 = v.y;
-      }
-      double q0 = nonfinite ? 0.0 : ldexp(x0, -e), q1 = nonfinite ? 0.0 : ldexp(x1, -e);
-#pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const double v0 = q0 * 128.0, v1 = q1 * 128.0;
-        const double t0 = trunc(v0), t1 = trunc(v1);
-        q0 = v0 - t0;
-        q1 = v1 - t1;
-        const uint32_t b0 = (uint32_t)(uint8_t)(int8_t)(int)t0, b1 = (uint32_t)(uint8_t)(int8_t)(int)t1;
-        wv[q][j >> 1] |= (b0 << (16 * (j & 1))) | (b1 << (16 * (j & 1) + 8));
+      for (int j = 0; j < 8; ++j) {
+        const double2 v = blk_dyn[rr * (W + 1) + (gg / NG) * CC + g * 8 + j];
+        const double x0 = a.a_mode ? (part ? v.y : v.x) : v.x;
+        const double x1 = a.a_mode ? (part ? v.x : -v.y) : v.y;
+        digits8(x0, e_raw, wv, 2 * j);
+        digits8(x1, e_raw, wv, 2 * j + 1);
       }
     }
     const int64_t R = a.a_mode ? 2 * r + part : r;
     const int64_t off = tile_offset(R, (int64_t)ch * KC + g * 16, a.RT, a.nchunks, S);
 #pragma unroll
     for (int q = 0; q < S; ++q)
-      *reinterpret_cast<uint4*>(outb + q * slice_stride + off) = make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
+      *reinterpret_cast<uint4*>(outb + off + (int64_t)q * a.RT * KC) =
+          make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
   }
 }
 
@@ -633,11 +640,20 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   }
   int r = check_launch("oz_rowexp");
   if (r) return r;
-  dim3 g2((unsigned)a.rtiles, (unsigned)a.nchunks, (unsigned)zdim);
+  dim3 g2((unsigned)a.rtiles, (unsigned)((a.nchunks + oz::CPB - 1) / oz::CPB), (unsigned)zdim);
+  const int CR = a_mode ? RT / 2 : RT;
+  const size_t smem = (size_t)CR * (oz::CPB * oz::KC / 2 + 1) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(oz::slice_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(oz::slice_tile_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(oz::slice_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
   switch (S) {
-    case 7: oz::slice_tile_kernel<7><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
-    case 8: oz::slice_tile_kernel<8><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
-    default: oz::slice_tile_kernel<1><<<g2, 256, 0, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 7: oz::slice_tile_kernel<7><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 8: oz::slice_tile_kernel<8><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
+    default: oz::slice_tile_kernel<1><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
   }
   return check_launch("oz_slice");
 }
