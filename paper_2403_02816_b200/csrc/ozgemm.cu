@@ -299,8 +299,11 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   const int nreal = a.a_mode ? 2 : 1;
   constexpr int NG = KC / 16;               // 16-byte groups per chunk
   const int groups = CPB * NG;
-  for (int w = tid; w < CR * nreal * groups; w += 256) {
-    const int gg = w % groups, rr_real = w / groups;
+  // consecutive threads take consecutive REAL rows of one 16-byte group, so the
+  // slice stores of a warp fill whole 128-byte lines of the core-matrix layout
+  const int nrr = CR * nreal;
+  for (int w = tid; w < nrr * groups; w += 256) {
+    const int rr_real = w % nrr, gg = w / nrr;
     const int rr = a.a_mode ? rr_real >> 1 : rr_real, part = a.a_mode ? rr_real & 1 : 0;
     const int64_t r = r0 + rr;
     const int ch = ch0 + gg / NG, g = gg % NG;
