@@ -138,11 +138,23 @@ int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
                  int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride,
                  int a_mode, int8_t* out, int64_t out_batch_stride, int* exps,
                  int64_t exp_batch_stride);
-/* The same for nitems equally shaped matrices in one launch pair. */
+/* The same for nitems equally shaped matrices in one launch pair, for the
+ * per-product (dense) data operand: digits in floor form (signed top digit,
+ * others in [0, 127]) -- cgl_oz_slice uses sign-magnitude digits, which keep
+ * the leading slices of small entries zero for cgl_oz_zmap skipping. */
 int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* srcs,
                        int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
                        int64_t src_batch_stride, int a_mode, int8_t* const* outs,
                        int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride);
+/* As cgl_oz_gemm but C stored transposed: element (i, j) at C[j*ldc + i].
+ * The last-axis product Out = In E^T runs as Out^T = E In^T with the
+ * constant E on the (block-skipped) A side and the data on the B side. */
+int cgl_oz_gemm_t(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems,
+                  const int8_t* const* A, const int* const* Aexp, const int8_t* const* Azmap,
+                  const int8_t* const* B, const int* const* Bexp, const int8_t* const* Bzmap,
+                  double* const* C, int64_t ldc, int64_t batch,
+                  int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
+                  const cgl_flag_t* flag, uint64_t pos);
 /* Tile geometry of the emulated GEMM: A row tile, B row tile, K chunk bytes. */
 int cgl_oz_geometry(int* bm, int* bn, int* kc);
 /* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last

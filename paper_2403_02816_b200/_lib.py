@@ -79,6 +79,8 @@ _SIGS = {
                                    c_ptr, c_i64, c_ptr, c_i64]),
     "cgl_oz_trace": (c_int, [c_ptr]),
     "cgl_oz_geometry": (c_int, [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
+    "cgl_oz_gemm_t": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                              c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64]),
     "cgl_oz_zmap": (c_int, [c_ptr, c_int, c_ptr, c_i64, c_i64, c_int, c_ptr]),
     "cgl_lincomb": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_eval_g": (c_int, [c_ptr, c_i64, c_ptr, c_int, c_ptr, c_dbl, c_ptr, c_ptr, c_u64]),

@@ -31,10 +31,10 @@ int oz_slice(cudaStream_t, int, const double*, int64_t, int64_t, int64_t, int64_
              int64_t, int*, int64_t);
 int oz_gemm(cudaStream_t, int, int64_t, int64_t, int64_t, int, const int8_t* const*, const int* const*,
             const int8_t* const*, const int8_t* const*, const int* const*, const int8_t* const*, double* const*,
-            int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const cgl_flag_t*, uint64_t);
+            int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const cgl_flag_t*, uint64_t, int);
 int oz_zmap(cudaStream_t, int, const int8_t*, int64_t, int64_t, int, int, int8_t*);
 int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
-                   int, int8_t* const*, int64_t, int* const*, int64_t);
+                   int, int8_t* const*, int64_t, int* const*, int64_t, int);
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
@@ -290,14 +290,22 @@ int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems
                 const int8_t* const* Bzmap, double* const* C, int64_t ldc, int64_t batch, int64_t sA, int64_t sAexp,
                 int64_t sB, int64_t sBexp, int64_t sC, const cgl_flag_t* flag, uint64_t pos) {
   return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, Azmap, B, Bexp, Bzmap, C, ldc, batch, sA, sAexp,
-                 sB, sBexp, sC, flag, pos);
+                 sB, sBexp, sC, flag, pos, 0);
+}
+
+int cgl_oz_gemm_t(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+                  const int* const* Aexp, const int8_t* const* Azmap, const int8_t* const* B, const int* const* Bexp,
+                  const int8_t* const* Bzmap, double* const* C, int64_t ldc, int64_t batch, int64_t sA, int64_t sAexp,
+                  int64_t sB, int64_t sBexp, int64_t sC, const cgl_flag_t* flag, uint64_t pos) {
+  return oz_gemm((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, Azmap, B, Bexp, Bzmap, C, ldc, batch, sA, sAexp,
+                 sB, sBexp, sC, flag, pos, 1);
 }
 
 int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* srcs, int64_t sr, int64_t sc,
                        int64_t rows, int64_t cols, int64_t batch, int64_t src_batch_stride, int a_mode,
                        int8_t* const* outs, int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride) {
   return oz_slice_multi((cudaStream_t)stream, S, nitems, srcs, sr, sc, rows, cols, batch, src_batch_stride, a_mode,
-                        outs, out_batch_stride, exps, exp_batch_stride);
+                        outs, out_batch_stride, exps, exp_batch_stride, 1);
 }
 
 int cgl_oz_geometry(int* bm, int* bn, int* kc) {

@@ -172,6 +172,7 @@ struct SliceArgs {
   int RT;               // row tile (128 for A, BN for B)
   int nchunks;          // K chunks per row tile (2*cols padded to KC)
   int64_t cols_items;   // number of items (grid.z = items * batch)
+  int floor_digits;     // 1: floor digits (dense data operand), 0: sign-magnitude (constant operand)
   int64_t rtiles;       // row tiles
   int8_t* out;          // S * rtiles * nchunks * RT * KC bytes
   int* exps;            // per complex row: scale exponent e (values scaled by 2^-e)
@@ -266,13 +267,39 @@ __device__ __forceinline__ void digits8(double x, int e, uint32_t (&w)[8][4], in
   }
 }
 
-template <int S>
+// Floor ("two's complement") digits for the per-product data operand: the
+// top digit is signed (q >> 49 in [-128, 127]), the others in [0, 127]; the
+// slices represent the same truncated integer q, with ~half the instructions
+// of the sign-magnitude form and no FP64 conversion (q comes from the IEEE
+// bits).  Constant operands keep sign-magnitude digits so their small
+// entries leave the leading slices exactly zero (block skipping).
+__device__ __forceinline__ void digits8_floor(double x, int e, uint32_t (&w)[8][4], int byte) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int E = (int)((bits >> 52) & 0x7FF);
+  long long q = 0;
+  if (E != 0) {
+    const unsigned long long M = (bits & 0xFFFFFFFFFFFFFull) | 0x10000000000000ull;
+    const int k = E - 1019 - e;  // q = M 2^k, |q| < 2^56
+    const unsigned long long mag = k >= 0 ? (M << k) : (k > -64 ? (M >> (-k)) : 0ull);
+    q = (bits >> 63) ? -(long long)mag : (long long)mag;
+  }
+  const int hi = (int)(q >> 28);                 // signed, 28 bits of magnitude
+  const unsigned lo = (unsigned)q & 0x0FFFFFFFu;  // 28 bits
+  const unsigned d[8] = {(unsigned)(hi >> 21), ((unsigned)hi >> 14) & 127u, ((unsigned)hi >> 7) & 127u,
+                         (unsigned)hi & 127u, (lo >> 21) & 127u, (lo >> 14) & 127u, (lo >> 7) & 127u, lo & 127u};
+  const int word = byte >> 2, sh = 8 * (byte & 3);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) w[s][word] |= (d[s] & 0xFFu) << sh;
+}
+
+template <int S, int AMODE>
 __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
                                                          int64_t exp_bs) {
   constexpr int CC = KC / 2;              // complex columns per chunk
   constexpr int W = CC * CPB;             // complex columns per CTA
+  constexpr int RT = AMODE ? BM : kOzBN;  // real rows per tile
+  constexpr int CR = AMODE ? RT / 2 : RT; // complex rows per tile
   extern __shared__ double2 blk_dyn[];    // [CR][W + 1]
-  const int CR = a.a_mode ? a.RT / 2 : a.RT;
   const int64_t batch = gridDim.z / a.cols_items;
   const int64_t b = blockIdx.z % batch;
   const int item = (int)(blockIdx.z / batch);
@@ -280,35 +307,41 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   const int64_t r0 = (int64_t)rt * CR, c0 = (int64_t)ch0 * CC;
   const double2* z = a.srcs[item] + b * src_bs;
   const int tid = threadIdx.x;
+  const int rows_here = (int)min((int64_t)CR, a.rows - r0), cols_here = (int)min((int64_t)W, a.cols - c0);
   if (a.sc == 1) {
+    const double2* zb = z + r0 * a.sr + c0;
+#pragma unroll 4
     for (int i = tid; i < CR * W; i += 256) {
-      const int rr = i / W, cc = i % W;
-      const int64_t r = r0 + rr, c = c0 + cc;
-      blk_dyn[rr * (W + 1) + cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c] : make_double2(0.0, 0.0);
+      const int rr = i / W, cc = i % W;  // W, CR are powers of two: shifts
+      blk_dyn[rr * (W + 1) + cc] = (rr < rows_here && cc < cols_here) ? zb[rr * a.sr + cc] : make_double2(0.0, 0.0);
     }
   } else {
+    const double2* zb = z + r0 + c0 * a.sc;  // sr == 1
+#pragma unroll 4
     for (int i = tid; i < CR * W; i += 256) {
       const int rr = i % CR, cc = i / CR;
-      const int64_t r = r0 + rr, c = c0 + cc;
-      blk_dyn[rr * (W + 1) + cc] = (r < a.rows && c < a.cols) ? z[r * a.sr + c * a.sc] : make_double2(0.0, 0.0);
+      blk_dyn[rr * (W + 1) + cc] = (rr < rows_here && cc < cols_here) ? zb[rr + (int64_t)cc * a.sc]
+                                                                      : make_double2(0.0, 0.0);
     }
   }
   __syncthreads();
   int8_t* outb = a.outs[item] + b * out_bs;
-  const int* exps = a.expss[item];
-  const int nreal = a.a_mode ? 2 : 1;
+  const int* exps = a.expss[item] + b * exp_bs + r0;
+  constexpr int nreal = AMODE ? 2 : 1;
   constexpr int NG = KC / 16;               // 16-byte groups per chunk
-  const int groups = CPB * NG;
+  constexpr int groups = CPB * NG;
   // consecutive threads take consecutive REAL rows of one 16-byte group, so the
   // slice stores of a warp fill whole 128-byte lines of the core-matrix layout
-  const int nrr = CR * nreal;
+  constexpr int nrr = CR * nreal;
+  // block base of row tile rt, chunk ch: ((rt * nchunks + ch) * S) * RT * KC
+  int8_t* tile_base = outb + (int64_t)rt * a.nchunks * S * (RT * KC);
+#pragma unroll 2
   for (int w = tid; w < nrr * groups; w += 256) {
     const int rr_real = w % nrr, gg = w / nrr;
-    const int rr = a.a_mode ? rr_real >> 1 : rr_real, part = a.a_mode ? rr_real & 1 : 0;
-    const int64_t r = r0 + rr;
+    const int rr = AMODE ? rr_real >> 1 : rr_real, part = AMODE ? rr_real & 1 : 0;
     const int ch = ch0 + gg / NG, g = gg % NG;
-    if (r >= a.rows || ch >= a.nchunks) continue;  // padding stays zero (buffer zeroed once)
-    const int e_raw = exps[b * exp_bs + r];
+    if (rr >= rows_here || ch >= a.nchunks) continue;  // padding stays zero (buffer zeroed once)
+    const int e_raw = exps[rr];
     const bool nonfinite = e_raw == NONFINITE;
     uint32_t wv[8][4];
 #pragma unroll
@@ -317,18 +350,22 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const double2 v = blk_dyn[rr * (W + 1) + (gg / NG) * CC + g * 8 + j];
-        const double x0 = a.a_mode ? (part ? v.y : v.x) : v.x;
-        const double x1 = a.a_mode ? (part ? v.x : -v.y) : v.y;
-        digits8(x0, e_raw, wv, 2 * j);
-        digits8(x1, e_raw, wv, 2 * j + 1);
+        const double x0 = AMODE ? (part ? v.y : v.x) : v.x;
+        const double x1 = AMODE ? (part ? v.x : -v.y) : v.y;
+        if (a.floor_digits) {
+          digits8_floor(x0, e_raw, wv, 2 * j);
+          digits8_floor(x1, e_raw, wv, 2 * j + 1);
+        } else {
+          digits8(x0, e_raw, wv, 2 * j);
+          digits8(x1, e_raw, wv, 2 * j + 1);
+        }
       }
     }
-    const int64_t R = a.a_mode ? 2 * r + part : r;
-    const int64_t off = tile_offset(R, (int64_t)ch * KC + g * 16, a.RT, a.nchunks, S);
+    const int R = AMODE ? 2 * rr + part : rr;  // real row within the tile
+    int8_t* dst = tile_base + (int64_t)ch * S * (RT * KC) + (((R >> 3) * (KC / 16) + g) * 8 + (R & 7)) * 16;
 #pragma unroll
     for (int q = 0; q < S; ++q)
-      *reinterpret_cast<uint4*>(outb + off + (int64_t)q * a.RT * KC) =
-          make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
+      *reinterpret_cast<uint4*>(dst + q * (RT * KC)) = make_uint4(wv[q][0], wv[q][1], wv[q][2], wv[q][3]);
   }
 }
 
@@ -377,6 +414,7 @@ struct OzArgs {
   int mtiles, ntiles, nchunks;
   int64_t sAb, sAeb, sBb, sBeb, sCb, ldc;
   int64_t batch;
+  int trans_c;            // 1: element (i, j) stored at C[j*ldc + i] (Out = In E^T computed as E In^T)
   const cgl_flag_t* flag;
   uint64_t pos;
   long long* trace;  // optional: CTA 0 phase timestamps (globaltimer ns), see OZ_TRACE
@@ -570,11 +608,21 @@ __global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(co
     // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
     double2* C = it.C + b * a.sCb;
     const int et = threadIdx.x - 64;
-    for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
-      const int ii = idx / BN, j = idx % BN;
-      const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
-      if (gi < a.M && gj < a.N)
-        C[gi * a.ldc + gj] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
+    if (!a.trans_c) {
+      for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
+        const int ii = idx / BN, j = idx % BN;
+        const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
+        if (gi < a.M && gj < a.N)
+          C[gi * a.ldc + gj] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
+      }
+    } else {
+      // transposed store: consecutive threads walk i, contiguous in C
+      for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
+        const int ii = idx % (BM / 2), j = idx / (BM / 2);
+        const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
+        if (gi < a.M && gj < a.N)
+          C[gj * a.ldc + gi] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
+      }
     }
   }
   tc_fence_before();
@@ -595,7 +643,7 @@ long long* g_oz_trace = nullptr;
 
 int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs, int64_t sr, int64_t sc,
                    int64_t rows, int64_t cols, int64_t batch, int64_t src_bs, int a_mode, int8_t* const* outs,
-                   int64_t out_bs, int* const* exps, int64_t exp_bs) {
+                   int64_t out_bs, int* const* exps, int64_t exp_bs, int floor_digits) {
   if (S < 1 || S > 8) return set_error(CGL_EINVAL, "oz_slice: S must be 1..8");
   if (nitems < 1 || nitems > 8) return set_error(CGL_EINVAL, "oz_slice: 1..8 items");
   if (rows <= 0 || cols <= 0 || batch <= 0) return 0;
@@ -616,6 +664,7 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   a.nchunks = (int)((2 * cols + oz::KC - 1) / oz::KC);
   a.rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
   a.cols_items = nitems;
+  a.floor_digits = floor_digits;
   const int64_t zdim = batch * nitems;
   if (zdim > 65535) return set_error(CGL_ESHAPE, "oz_slice: batch x items too large");
   // pass 1: exponents
@@ -648,23 +697,26 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   const size_t smem = (size_t)CR * (oz::CPB * oz::KC / 2 + 1) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(oz::slice_tile_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(oz::slice_tile_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    cudaFuncSetAttribute(oz::slice_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+#define OZ_ATTR(S_, A_) cudaFuncSetAttribute(oz::slice_tile_kernel<S_, A_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)
+    OZ_ATTR(8, 0); OZ_ATTR(8, 1); OZ_ATTR(7, 0); OZ_ATTR(7, 1); OZ_ATTR(1, 0); OZ_ATTR(1, 1);
+#undef OZ_ATTR
     attr = true;
   }
+#define OZ_SLICE(S_) (a_mode ? (oz::slice_tile_kernel<S_, 1><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs)) \
+                             : (oz::slice_tile_kernel<S_, 0><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs)))
   switch (S) {
-    case 7: oz::slice_tile_kernel<7><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
-    case 8: oz::slice_tile_kernel<8><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
-    default: oz::slice_tile_kernel<1><<<g2, 256, smem, st>>>(a, src_bs, out_bs, exp_bs); break;
+    case 7: OZ_SLICE(7); break;
+    case 8: OZ_SLICE(8); break;
+    default: OZ_SLICE(1); break;
   }
+#undef OZ_SLICE
   return check_launch("oz_slice");
 }
 
 int oz_slice(cudaStream_t st, int S, const double* src, int64_t sr, int64_t sc, int64_t rows, int64_t cols,
              int64_t batch, int64_t src_bs, int a_mode, int RT, int8_t* out, int64_t out_bs, int* exps, int64_t exp_bs) {
   (void)RT;
-  return oz_slice_multi(st, S, 1, &src, sr, sc, rows, cols, batch, src_bs, a_mode, &out, out_bs, &exps, exp_bs);
+  return oz_slice_multi(st, S, 1, &src, sr, sc, rows, cols, batch, src_bs, a_mode, &out, out_bs, &exps, exp_bs, 0);
 }
 
 template <int S, int BN, int STAGES>
@@ -686,7 +738,7 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
 int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
             const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
             const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
-            int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos) {
+            int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos, int trans_c) {
   constexpr int BN = kOzBN;
   if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "oz_gemm: 1..8 items");
   oz::OzArgs a{};
@@ -702,6 +754,7 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   a.sCb = sCb;
   a.ldc = ldc;
   a.batch = batch;
+  a.trans_c = trans_c;
   a.flag = flag;
   a.pos = pos;
   {

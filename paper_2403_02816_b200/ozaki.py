@@ -41,7 +41,8 @@ def _zmap_len(rows, cols, a_mode):
 
 
 class SlicedFactor:
-    """Both operand roles of one square constant factor E (n x n)."""
+    """A-operand slices (+ zero map) of one square constant factor E (n x n):
+    every mode product keeps E on the A side (the last axis via Out^T = E In^T)."""
 
     def __init__(self, E):
         lib = _lib.load()
@@ -55,13 +56,6 @@ class SlicedFactor:
                                     _lib.ptr(self.Ae), 0), "oz_slice(E, A)")
         self.Az = torch.empty(_zmap_len(n, n, 1), dtype=torch.int8, device=E.device)
         _lib.check(lib.cgl_oz_zmap(st, S, _lib.ptr(self.A), n, n, 1, _lib.ptr(self.Az)), "oz_zmap(A)")
-        # B role for Out = In E^T: Z = (E^T)^T = E, rows = output columns j, K = k
-        self.B = torch.zeros(_nbytes(n, n, 0), dtype=torch.int8, device=E.device)
-        self.Be = torch.empty(n, dtype=torch.int32, device=E.device)
-        _lib.check(lib.cgl_oz_slice(st, S, _lib.ptr(E), n, 1, n, n, 1, 0, 0, _lib.ptr(self.B), 0,
-                                    _lib.ptr(self.Be), 0), "oz_slice(E, B)")
-        self.Bz = torch.empty(_zmap_len(n, n, 0), dtype=torch.int8, device=E.device)
-        _lib.check(lib.cgl_oz_zmap(st, S, _lib.ptr(self.B), n, n, 0, _lib.ptr(self.Bz)), "oz_zmap(B)")
 
 
 class Workspace:
@@ -120,20 +114,23 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
                              _lib.ptr_array(outs), Q, P, 0, 0, per, Q, n * Q, _lib.flag_ptr(flag), pos)
         _lib.check(rc, "oz_gemm(left)")
     else:
-        # right form: Out (P x n) = In (P x n) E^T; data on the A side (rows p, K = k)
-        per = _nbytes(P, n, 1)
-        As, Ae = [], []
+        # last axis: Out (P x n) = In (P x n) E^T computed as Out^T = E In^T, so the
+        # constant E stays on the block-skipped A side; data on the B side with
+        # Z = In (rows p, K = k contiguous); C stored transposed (ldc = n)
+        per = _nbytes(P, n, 0)
+        Bs, Be = [], []
         for f in range(nf):
-            buf, ex = ws.get(("A", f), per, P, dev)
-            As.append(buf)
-            Ae.append(ex)
-        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), n, 1, P, n, 1, 0, 1,
-                                          _lib.ptr_array(As), 0, _lib.ptr_array(Ae), 0), "oz_slice(data, A)")
-        rc = lib.cgl_oz_gemm(st, S, P, n, n, nf, _lib.ptr_array(As), _lib.ptr_array(Ae), None,
-                             _lib.ptr_array([fc.B for fc in factors]), _lib.ptr_array([fc.Be for fc in factors]),
-                             _lib.ptr_array([fc.Bz for fc in factors]),
-                             _lib.ptr_array(outs), n, 1, 0, 0, 0, 0, 0, _lib.flag_ptr(flag), pos)
-        _lib.check(rc, "oz_gemm(right)")
+            buf, ex = ws.get(("Bt", f), per, P, dev)
+            Bs.append(buf)
+            Be.append(ex)
+        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), n, 1, P, n, 1, 0, 0,
+                                          _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, Bt)")
+        rc = lib.cgl_oz_gemm_t(st, S, n, P, n, nf,
+                               _lib.ptr_array([fc.A for fc in factors]), _lib.ptr_array([fc.Ae for fc in factors]),
+                               _lib.ptr_array([fc.Az for fc in factors]),
+                               _lib.ptr_array(Bs), _lib.ptr_array(Be), None,
+                               _lib.ptr_array(outs), n, 1, 0, 0, 0, 0, 0, _lib.flag_ptr(flag), pos)
+        _lib.check(rc, "oz_gemm(last axis)")
     return outs
 
 
