@@ -33,14 +33,15 @@ extern "C" {
 #define CGL_ESHAPE (-2)
 #define CGL_ECUFFT (-3)
 
-/* Sticky divergence record + device step counter (24 bytes, device memory).
+/* Sticky divergence record + device step base (24 bytes, device memory).
  * key = (step << 24) | (seq << 8) | reason, atomically min-reduced, so it
  * holds the first (step, call) that failed; mirrors DivergenceError(reason)
  * + diverged_at of integrators.py:264-278 and flows.py:32-39,95-132.
- * Init: key = all ones, step = first step number, done = 0.
- * A `pos` argument with CGL_POS_DEVICE set takes its step from `step`
- * (low 24 bits = seq << 8), so a captured CUDA graph of a step can replay;
- * "end-of-step" stage kernels advance `step` once all their CTAs are done. */
+ * Init: key = all ones, step = 0 (base), done = 0 (reserved).
+ * A `pos` with CGL_POS_DEVICE set is relative: step = flag->step + the local
+ * step index in pos bits 24..62 (seq << 8 in the low bits), so a captured
+ * CUDA graph of a chunk of steps replays unchanged; cgl_flag_advance moves
+ * the base at the end of each chunk. */
 typedef struct cgl_flag_t {
   unsigned long long key;
   unsigned long long step;
@@ -209,6 +210,7 @@ int cgl_check_finite(void* stream, int64_t n, int nfields,
                      const double* const* x, cgl_flag_t* flag, uint64_t pos);
 
 int cgl_flag_reset(void* stream, cgl_flag_t* flag);
+int cgl_flag_advance(void* stream, cgl_flag_t* flag, unsigned long long nsteps);
 
 /* ---- fused per-scheme stage kernels (csrc/stages.cu) -------------------- */
 enum cgl_stage_program {
@@ -231,10 +233,9 @@ enum cgl_stage_program {
 };
 /* One fused pass of a step body (integrators.py:146-215): see the program
  * table in csrc/stages.cu.  in/out: (#operands x nfields) pointers, operand
- * major.  *_END programs check finiteness, run the next step's prologue and
- * advance flag->step; positions come from flag->step when pos has
- * CGL_POS_DEVICE set (CUDA-graph replay), else from pos >> 24.  in/out may
- * alias elementwise (each point is read before it is written). */
+ * major.  *_END programs check finiteness and run the next step's prologue;
+ * the step comes from pos (relative to flag->step when CGL_POS_DEVICE is
+ * set).  in/out may alias elementwise (each point is read before written). */
 int cgl_stage(void* stream, int program, int nfields, int64_t n,
               const cgl_nonlinear_t* nl, double tau, double in_scale,
               const double* const* in, double* const* out,

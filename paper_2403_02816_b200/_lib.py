@@ -41,12 +41,21 @@ STAGE = {"if4_pre": 0, "if4_mid": 1, "if4_end": 2, "flow1": 3, "flow2": 4, "spli
          "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14}
 
 
-def new_flag(first_step=1):
-    """Device flag record (cgl_flag_t): key = all ones, step, done = 0."""
+def new_flag(base=0):
+    """Device flag record (cgl_flag_t): key = all ones, step base, done = 0."""
     f = torch.zeros(3, dtype=torch.int64, device="cuda")
     f[0] = -1
-    f[1] = first_step
+    f[1] = base
     return f
+
+
+def rel_pos(local_step):
+    """Device-relative position of local step `local_step` (>= 1) of a chunk."""
+    return POS_DEVICE | (int(local_step) << 24)
+
+
+def flag_advance(flag, n):
+    check(load().cgl_flag_advance(stream(), flag_ptr(flag), int(n)), "cgl_flag_advance")
 
 KIND_CODES = {"cubic": 0, "cubic_quintic": 1, "coupled_cubic_quintic": 2}
 
@@ -89,6 +98,7 @@ _SIGS = {
     "cgl_rk4_flow": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_int, c_ptr, c_dbl, c_ptr, c_ptr, c_u64]),
     "cgl_check_finite": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr, c_u64]),
     "cgl_flag_reset": (c_int, [c_ptr, c_ptr]),
+    "cgl_flag_advance": (c_int, [c_ptr, c_ptr, ctypes.c_ulonglong]),
     "cgl_stage": (c_int, [c_ptr, c_int, c_int, c_i64, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_stage_fourier": (c_int, [c_ptr, c_int, c_int, c_int, c_ptr, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr,
                                   c_ptr, c_u64]),

@@ -19,6 +19,7 @@ int pw_rk4_flow(cudaStream_t, int64_t, double, const cgl_nonlinear_t*, int, cons
                 double* const*, cgl_flag_t*, uint64_t);
 int pw_check_finite(cudaStream_t, int64_t, int, const double* const*, cgl_flag_t*, uint64_t);
 int pw_flag_reset(cudaStream_t, cgl_flag_t*);
+int pw_flag_advance(cudaStream_t, cgl_flag_t*, unsigned long long);
 int pw_mul(cudaStream_t, int64_t, const double*, const double*, double*, const cgl_flag_t*, uint64_t);
 int pw_symexp(cudaStream_t, int64_t, double, const double*, double*);
 int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double, const double*, double*,
@@ -244,6 +245,9 @@ int cgl_check_finite(void* stream, int64_t n, int nfields, const double* const* 
 }
 
 int cgl_flag_reset(void* stream, cgl_flag_t* flag) { return pw_flag_reset((cudaStream_t)stream, flag); }
+int cgl_flag_advance(void* stream, cgl_flag_t* flag, unsigned long long nsteps) {
+  return pw_flag_advance((cudaStream_t)stream, flag, nsteps);
+}
 
 int cgl_pointwise_mul(void* stream, int64_t n, const double* factor, const double* in, double* out,
                       const cgl_flag_t* flag, uint64_t pos) {

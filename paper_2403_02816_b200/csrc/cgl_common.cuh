@@ -42,10 +42,13 @@ __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 // recorded by the kernel's own blocks never make it skip, so every kernel
 // either runs completely or not at all.
 // ---------------------------------------------------------------------------
+// Device-relative positions: step = flag->step (a base advanced once per
+// captured chunk of steps) + the local step index baked into pos bits 24..62.
 __device__ __forceinline__ uint64_t resolve_pos(const cgl_flag_t* f, uint64_t pos) {
   if (f != nullptr && (pos & CGL_POS_DEVICE)) {
-    const uint64_t step = *reinterpret_cast<const volatile unsigned long long*>(&f->step);
-    return (step << 24) | (pos & 0xFFFFFFull);
+    const uint64_t base = *reinterpret_cast<const volatile unsigned long long*>(&f->step);
+    const uint64_t local = (pos & ~CGL_POS_DEVICE) >> 24;
+    return ((base + local) << 24) | (pos & 0xFFFFFFull);
   }
   return pos & ~CGL_POS_DEVICE;
 }
@@ -55,21 +58,6 @@ __device__ __forceinline__ bool flag_skip(const cgl_flag_t* f, uint64_t pos) {
   if (f == nullptr) return false;
   uint64_t k = *reinterpret_cast<const volatile unsigned long long*>(&f->key);
   return k < pos;
-}
-
-// End-of-step kernels: the last CTA to finish advances the device step.
-__device__ __forceinline__ void advance_step(cgl_flag_t* f) {
-  if (f == nullptr) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned t = atomicAdd(&f->done, 1u);
-    if (t == gridDim.x - 1) {
-      f->step += 1;
-      f->done = 0;
-      __threadfence();
-    }
-  }
 }
 
 __device__ __forceinline__ void flag_raise(cgl_flag_t* f, uint64_t pos, unsigned reason) {

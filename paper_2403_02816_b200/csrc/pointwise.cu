@@ -156,6 +156,7 @@ __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint
 }
 
 __global__ void flag_reset_kernel(cgl_flag_t* f) { f->key = ~0ull; }
+__global__ void flag_advance_kernel(cgl_flag_t* f, unsigned long long n) { f->step += n; }
 
 __global__ void mul_kernel(int64_t n, const double2* f, const double2* in, double2* out, const cgl_flag_t* flag, uint64_t pos) {
   pos = resolve_pos(flag, pos);
@@ -267,6 +268,11 @@ int pw_check_finite(cudaStream_t st, int64_t n, int nf, const double* const* x, 
 int pw_flag_reset(cudaStream_t st, cgl_flag_t* f) {
   flag_reset_kernel<<<1, 1, 0, st>>>(f);
   return check_launch("flag_reset");
+}
+
+int pw_flag_advance(cudaStream_t st, cgl_flag_t* f, unsigned long long n) {
+  flag_advance_kernel<<<1, 1, 0, st>>>(f, n);
+  return check_launch("flag_advance");
 }
 
 int pw_mul(cudaStream_t st, int64_t n, const double* f, const double* in, double* out, const cgl_flag_t* flag, uint64_t pos) {

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
     }
   }
   raise_min(a.flag, key);
-  if (is_end) advance_step(a.flag);
+  (void)is_end;
 }
 
 template <int NF>

@@ -145,7 +145,7 @@ class ShardedPlan(FusedPlan):
         for f, fin, fout in jobs:
             for c in range(self.nf):
                 m, mt = self.blocks[c].exp_factors(f)
-                tucker_sharded(fin[c], m, mt, fout[c], self.W[c], self.tr, flag=flag, pos=_lib.POS_DEVICE)
+                tucker_sharded(fin[c], m, mt, fout[c], self.W[c], self.tr, flag=flag, pos=self._pos)
 
     def _before_end(self, flag):
         global_min_key(flag, self.group)
@@ -156,10 +156,14 @@ class ShardedPlan(FusedPlan):
     def run(self, u0, steps, tau, stop_at=(), on_stop=None, poll_chunks=1):
         flag = self.flag
         flag.copy_(self._flag0)
+        self._k_base = 0
+        self._pos = _lib.rel_pos(1)
         self.load_state(u0, tau)
         self.prologue(flag, tau)
         for k in range(1, steps + 1):
             self.step(k, flag, tau)
+            _lib.flag_advance(flag, 1)
+            self._k_base += 1
             if k in stop_at or k == steps or k % 16 == 0:
                 global_min_key(flag, self.group)
                 key = int(flag[0].item()) & ((1 << 64) - 1)

@@ -79,7 +79,9 @@ class FusedPlan:
         self.use_oz = None
         from .ozaki import Workspace
         self.oz_ws = Workspace()
-        self.flag = _lib.new_flag(1)   # baked into the captured graphs; reset per run
+        self.flag = _lib.new_flag(0)   # baked into the captured graphs; reset per run
+        self._pos = _lib.rel_pos(1)
+        self._k_base = 0               # host copy of the flag's step base
         self._flag0 = self.flag.clone()
         self.graph_launches = {}       # cgl kernels inside each captured graph
         self.replayed_launches = 0     # cgl kernels launched by graph replays (not seen by the C counter)
@@ -108,7 +110,7 @@ class FusedPlan:
             for i in range(0, len(ins), 8):
                 sl = slice(i, i + 8)
                 ozaki.tucker_oz(ins[sl], facs[sl], outs[sl], work[sl] if work else None, self.oz_ws, flag=flag,
-                                pos=_lib.POS_DEVICE)
+                                pos=self._pos)
             return
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
@@ -119,7 +121,7 @@ class FusedPlan:
                 mats.append(m)
                 mts.append(mt)
         work = self.W[:len(ins)] if self.W else None
-        tucker_dev(ins, mats, mts, outs=outs, flag=flag, pos=_lib.POS_DEVICE, work=work)
+        tucker_dev(ins, mats, mts, outs=outs, flag=flag, pos=self._pos, work=work)
 
     def _stage(self, name, ins, outs, flag, tau):
         lib = _lib.load()
@@ -127,7 +129,7 @@ class FusedPlan:
         fout = [t for fs in outs for t in fs]
         _lib.check(lib.cgl_stage(_lib.stream(), _lib.STAGE[name], self.nf, self.n, _lib.ctypes.byref(self.nl),
                                  tau, 1.0, _lib.ptr_array(fin), _lib.ptr_array(fout), _lib.flag_ptr(flag),
-                                 _lib.POS_DEVICE), "cgl_stage")
+                                 self._pos), "cgl_stage")
 
     def _before_end(self, flag):
         """Hook before each end-of-step kernel (cross-rank key reduction)."""
@@ -157,6 +159,7 @@ class FusedPlan:
 
     def step(self, k, flag, tau):
         """One time step k (1-based); input state_after(k-1), output state_after(k)."""
+        self._pos = _lib.rel_pos(k - self._k_base)
         B, H, O = self.B, self.half, self.one
         if self.scheme == "if4":
             u = self.U[0]
@@ -199,6 +202,7 @@ class FusedPlan:
                 with torch.cuda.graph(g, stream=s):
                     for j in range(count):
                         self.step(k0 + j, flag, tau)
+                    _lib.flag_advance(flag, count)
             torch.cuda.current_stream().wait_stream(s)
             self.graph_launches[key] = lib.cgl_launch_count() - n0
             self.graphs[key] = g
@@ -209,6 +213,8 @@ class FusedPlan:
         """Advance `steps` steps from u0; returns the flag key (int)."""
         flag = self.flag
         flag.copy_(self._flag0)
+        self._k_base = 0
+        self._pos = _lib.rel_pos(1)
         self.load_state(u0, tau)
         self.prologue(flag, tau)
         stops = sorted(set(int(s) for s in stop_at if 1 <= int(s) <= steps))
@@ -228,9 +234,11 @@ class FusedPlan:
             if eager_first or count != self.CHUNK:
                 for j in range(count):
                     self.step(k + j, flag, tau)
+                _lib.flag_advance(flag, count)
                 eager_first = False
             else:
                 self._graph(k, count, flag, tau).replay()
+            self._k_base += count
             k += count
             nchunk += 1
             if (k - 1) in stops or k > steps:
@@ -292,7 +300,9 @@ class FourierPlan(FusedPlan):
             self.U = [mk(), mk()]                  # physical state ping-pong
             self.B = [mk()]                        # Q (v / spectral scratch)
         self.graphs = {}
-        self.flag = _lib.new_flag(1)
+        self.flag = _lib.new_flag(0)
+        self._pos = _lib.rel_pos(1)
+        self._k_base = 0
         self._flag0 = self.flag.clone()
         self.graph_launches = {}
         self.replayed_launches = 0
@@ -316,7 +326,7 @@ class FourierPlan(FusedPlan):
 
     def _g(self, fields, scale):
         from .flows import eval_g_dev
-        eval_g_dev(self.nl, fields, scale=scale, outs=fields, flag=self.flag, pos=_lib.POS_DEVICE)
+        eval_g_dev(self.nl, fields, scale=scale, outs=fields, flag=self.flag, pos=self._pos)
 
     def _fstage(self, name, ins, outs, tau, scale=1.0):
         lib = _lib.load()
@@ -326,7 +336,7 @@ class FourierPlan(FusedPlan):
         _lib.check(lib.cgl_stage_fourier(_lib.stream(), _lib.STAGE[name], self.nf, len(self.shape),
                                          _lib.i64_array(self.shape), _lib.ctypes.byref(self.nl), tau, scale,
                                          tabs, _lib.ptr_array(fin), _lib.ptr_array(fout),
-                                         _lib.flag_ptr(self.flag), _lib.POS_DEVICE), "cgl_stage_fourier")
+                                         _lib.flag_ptr(self.flag), self._pos), "cgl_stage_fourier")
 
     def _pstage(self, name, ins, outs, tau, scale):
         lib = _lib.load()
@@ -334,7 +344,7 @@ class FourierPlan(FusedPlan):
         fout = [t for fs in outs for t in fs]
         _lib.check(lib.cgl_stage(_lib.stream(), _lib.STAGE[name], self.nf, self.n, _lib.ctypes.byref(self.nl),
                                  tau, scale, _lib.ptr_array(fin), _lib.ptr_array(fout), _lib.flag_ptr(self.flag),
-                                 _lib.POS_DEVICE), "cgl_stage")
+                                 self._pos), "cgl_stage")
 
     def _mul_e1(self, fields):
         lib = _lib.load()
@@ -342,7 +352,7 @@ class FourierPlan(FusedPlan):
             _, tabs = b.exp_entry(self.one)
             _lib.check(lib.cgl_separable_mul(_lib.stream(), x.ndim, _lib.i64_array(x.shape), _lib.ptr_array(tabs),
                                              1.0, _lib.ptr(x), _lib.ptr(x), _lib.flag_ptr(self.flag),
-                                             _lib.POS_DEVICE), "cgl_separable_mul")
+                                             self._pos), "cgl_separable_mul")
 
     def load_state(self, u0, tau):
         self._tab_list = self._tables()
@@ -364,6 +374,7 @@ class FourierPlan(FusedPlan):
             self._pstage("flow1", [self.U[0]], [self.B[0]], tau, self._scale0)
 
     def step(self, k, flag, tau):
+        self._pos = _lib.rel_pos(k - self._k_base)
         inv_n = 1.0 / self.n
         if self.scheme == "if4":
             u = self.U[0]
