@@ -255,7 +255,8 @@ def gemm_roofline(torch, w, scheme_fields=4):
             # dram__bytes_read.sum + dram__bytes_write.sum of this launch, ncu --set full
             # (profiles/r01_ozgemm_ncu_summary.txt; ncu flushes caches, so this is the cold
             # upper bound -- in the step the operands are L2-resident)
-            "traffic": {"bytes": 23.2e6, "source": "profiles/r01_ozgemm_ncu_summary.txt"},
+            "traffic": 23.2e6, "traffic_unit": "bytes per launch",
+            "traffic_source": "profiles/r01_ozgemm_ncu_summary.txt (cold-cache ncu capture)",
             "kernel": "ozgemm_kernel<8,32,2> (tcgen05.mma kind::i8, TMEM accumulators): 4-field mode-1 product of "
                       "the if4 step, M=N=K=512 complex per field, S=8 int8 slices",
             "per_launch_ms": dt * 1e3, "per_launch_ms_incl_data_slicing": dt_with_slicing * 1e3,
