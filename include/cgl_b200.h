@@ -250,6 +250,18 @@ int cgl_stage_fourier(void* stream, int program, int nfields, int ndim,
                       const double* const* in, double* const* out,
                       cgl_flag_t* flag, uint64_t pos);
 
+/* Column-block variants for the slab-sharded spectral layout: the local
+ * field is the (shape[0] x cols) block of columns col_offset .. +cols of the
+ * global (shape[0] x prod(shape[1:])) matrix (after the axis-0 transpose). */
+int cgl_stage_fourier_cols(void* stream, int program, int nfields, int ndim,
+                           const int64_t* shape, int64_t cols, int64_t col_offset,
+                           const cgl_nonlinear_t* nl, double tau, double in_scale,
+                           const double* const* tables, const double* const* in,
+                           double* const* out, cgl_flag_t* flag, uint64_t pos);
+int cgl_separable_mul_cols(void* stream, int ndim, const int64_t* shape, int64_t cols,
+                           int64_t col_offset, const double* const* tables, double in_scale,
+                           const double* in, double* out, const cgl_flag_t* flag, uint64_t pos);
+
 /* Hadamard product out = factor .* in (spectral.py:123-129). */
 int cgl_pointwise_mul(void* stream, int64_t n, const double* factor,
                       const double* in, double* out,
@@ -273,6 +285,11 @@ int cgl_separable_mul(void* stream, int ndim, const int64_t* shape,
  * in_scale. */
 int cgl_fft_plan(int ndim, const int64_t* shape, void** plan);
 int cgl_fft_exec(void* plan, void* stream, const double* in, double* out, int inverse);
+/* Batched plan with advanced layout (cufftPlanMany semantics, embeds = n):
+ * 2D slab transforms and strided 1D transforms along axis 0 of the
+ * transposed column blocks in the slab-sharded 3D FFT. */
+int cgl_fft_plan_many(int rank, const int64_t* n, int64_t batch, int64_t istride,
+                      int64_t idist, int64_t ostride, int64_t odist, void** plan);
 int cgl_fft_destroy(void* plan);
 
 #ifdef __cplusplus

@@ -102,6 +102,10 @@ _SIGS = {
     "cgl_stage": (c_int, [c_ptr, c_int, c_int, c_i64, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_stage_fourier": (c_int, [c_ptr, c_int, c_int, c_int, c_ptr, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr,
                                   c_ptr, c_u64]),
+    "cgl_stage_fourier_cols": (c_int, [c_ptr, c_int, c_int, c_int, c_ptr, c_i64, c_i64, c_ptr, c_dbl, c_dbl, c_ptr,
+                                       c_ptr, c_ptr, c_ptr, c_u64]),
+    "cgl_separable_mul_cols": (c_int, [c_ptr, c_int, c_ptr, c_i64, c_i64, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),
+    "cgl_fft_plan_many": (c_int, [c_int, c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.POINTER(c_ptr)]),
     "cgl_pointwise_mul": (c_int, [c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_u64]),
     "cgl_symbol_exp": (c_int, [c_ptr, c_i64, c_dbl, c_ptr, c_ptr]),
     "cgl_separable_mul": (c_int, [c_ptr, c_int, c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr, c_u64]),

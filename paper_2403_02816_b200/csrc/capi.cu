@@ -23,7 +23,8 @@ int pw_flag_advance(cudaStream_t, cgl_flag_t*, unsigned long long);
 int pw_mul(cudaStream_t, int64_t, const double*, const double*, double*, const cgl_flag_t*, uint64_t);
 int pw_symexp(cudaStream_t, int64_t, double, const double*, double*);
 int pw_separable(cudaStream_t, int, const int64_t*, const double* const*, double, const double*, double*,
-                 const cgl_flag_t*, uint64_t);
+                 const cgl_flag_t*, uint64_t, int64_t, int64_t);
+int fft_plan_many(int, const int64_t*, int64_t, int64_t, int64_t, int64_t, int64_t, void**);
 int fft_plan(int, const int64_t*, void**);
 extern long long* g_oz_trace;
 int fft_exec(void*, cudaStream_t, const double*, double*, int);
@@ -38,7 +39,7 @@ int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_
                    int, int8_t* const*, int64_t, int* const*, int64_t, int);
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
-                 double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*);
+                 double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*, int64_t, int64_t);
 
 static thread_local std::string g_err;
 static unsigned long long g_launches = 0;
@@ -260,13 +261,24 @@ int cgl_symbol_exp(void* stream, int64_t n, double s, const double* symbol, doub
 
 int cgl_separable_mul(void* stream, int ndim, const int64_t* shape, const double* const* tables, double in_scale,
                       const double* in, double* out, const cgl_flag_t* flag, uint64_t pos) {
-  return pw_separable((cudaStream_t)stream, ndim, shape, tables, in_scale, in, out, flag, pos);
+  return pw_separable((cudaStream_t)stream, ndim, shape, tables, in_scale, in, out, flag, pos, 0, 0);
+}
+
+int cgl_separable_mul_cols(void* stream, int ndim, const int64_t* shape, int64_t cols, int64_t col_offset,
+                           const double* const* tables, double in_scale, const double* in, double* out,
+                           const cgl_flag_t* flag, uint64_t pos) {
+  return pw_separable((cudaStream_t)stream, ndim, shape, tables, in_scale, in, out, flag, pos, cols, col_offset);
+}
+
+int cgl_fft_plan_many(int rank, const int64_t* n, int64_t batch, int64_t istride, int64_t idist, int64_t ostride,
+                      int64_t odist, void** plan) {
+  return fft_plan_many(rank, n, batch, istride, idist, ostride, odist, plan);
 }
 
 int cgl_stage(void* stream, int program, int nfields, int64_t n, const cgl_nonlinear_t* nl, double tau,
               double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos) {
   return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos, 0, nullptr,
-                      nullptr);
+                      nullptr, 0, 0);
 }
 
 int cgl_stage_fourier(void* stream, int program, int nfields, int ndim, const int64_t* shape,
@@ -275,7 +287,15 @@ int cgl_stage_fourier(void* stream, int program, int nfields, int ndim, const in
   int64_t n = 1;
   for (int d = 0; d < ndim; ++d) n *= shape[d];
   return stage_launch((cudaStream_t)stream, program, nfields, n, nl, tau, in_scale, in, out, flag, pos, ndim, shape,
-                      tables);
+                      tables, 0, 0);
+}
+
+int cgl_stage_fourier_cols(void* stream, int program, int nfields, int ndim, const int64_t* shape, int64_t cols,
+                           int64_t col_offset, const cgl_nonlinear_t* nl, double tau, double in_scale,
+                           const double* const* tables, const double* const* in, double* const* out, cgl_flag_t* flag,
+                           uint64_t pos) {
+  return stage_launch((cudaStream_t)stream, program, nfields, shape[0] * cols, nl, tau, in_scale, in, out, flag, pos,
+                      ndim, shape, tables, cols, col_offset);
 }
 
 int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode) {

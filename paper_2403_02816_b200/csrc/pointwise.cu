@@ -176,6 +176,7 @@ struct SepArgs {
   const double2* tab[4];
   int64_t ext[4];
   int nd;
+  int64_t tm, toff, t12;  // optional column-block layout (see stages.cu)
 };
 
 // out[j] = s * prod_mu tab_mu[j_mu] * in[j] (C order: last axis fastest)
@@ -184,7 +185,7 @@ __global__ void separable_kernel(int64_t n, SepArgs a, double s, const double2* 
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i;
+    int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
     double2 e = make_double2(s, 0.0);
     for (int d = a.nd - 1; d >= 0; --d) {
       const int64_t j = r % a.ext[d];
@@ -291,12 +292,19 @@ int pw_symexp(cudaStream_t st, int64_t n, double s, const double* sym, double* o
 }
 
 int pw_separable(cudaStream_t st, int nd, const int64_t* shape, const double* const* tabs, double s, const double* in,
-                 double* out, const cgl_flag_t* flag, uint64_t pos) {
+                 double* out, const cgl_flag_t* flag, uint64_t pos, int64_t tm, int64_t toff) {
   if (nd < 1 || nd > 4) return set_error(CGL_EINVAL, "separable_mul: 1..4 dims");
   SepArgs a{};
   a.nd = nd;
   int64_t n = 1;
   for (int d = 0; d < nd; ++d) { a.tab[d] = reinterpret_cast<const double2*>(tabs[d]); a.ext[d] = shape[d]; n *= shape[d]; }
+  if (tm > 0) {
+    a.tm = tm;
+    a.toff = toff;
+    a.t12 = n / shape[0];
+    if (toff + tm > a.t12) return set_error(CGL_ESHAPE, "separable_mul: bad column block");
+    n = shape[0] * tm;
+  }
   if (n <= 0) return 0;
   separable_kernel<<<grid_for(n, kThreads), kThreads, 0, st>>>(n, a, s, reinterpret_cast<const double2*>(in),
                                                                reinterpret_cast<double2*>(out), flag, pos);

@@ -152,12 +152,15 @@ struct StageArgs {
   const double2* tab[2][2][4];
   int64_t ext[4];
   int nd;
+  // column-block (transposed) layout of a slab-sharded spectral field: local
+  // element (k0, c) of an (n0 x tm) block is global flat k0*t12 + toff + c
+  int64_t tm, toff, t12;
 };
 
 // exp(f tau symbol) at flat index i (C order) for fraction slot fr, component c
 __device__ __forceinline__ double2 sep_factor(const StageArgs& a, int fr, int c, int64_t i) {
   double2 e = make_double2(1.0, 0.0);
-  int64_t r = i;
+  int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
   for (int d = a.nd - 1; d >= 0; --d) {
     const int64_t j = r % a.ext[d];
     r /= a.ext[d];
@@ -333,7 +336,7 @@ static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1};
 
 int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonlinear_t* nl, double tau,
                  double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,
-                 int ndim, const int64_t* shape, const double* const* tables) {
+                 int ndim, const int64_t* shape, const double* const* tables, int64_t tm, int64_t toff) {
   if (prog < 0 || prog >= P_NPROG) return set_error(CGL_EINVAL, "stage: unknown program");
   if (nf != 1 && nf != 2) return set_error(CGL_EINVAL, "stage: 1 or 2 components");
   static_assert(sizeof(((StageArgs*)0)->in) / sizeof(void*) >= 10, "in[] holds 5 operands x 2 components");
@@ -354,7 +357,15 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
     a.nd = ndim;
     int64_t tot = 1;
     for (int d = 0; d < ndim; ++d) { a.ext[d] = shape[d]; tot *= shape[d]; }
-    if (tot != n) return set_error(CGL_ESHAPE, "stage: shape does not match n");
+    if (tm > 0) {
+      // local (n0 x tm) column block of a global shape (sharded spectral layout)
+      a.tm = tm;
+      a.toff = toff;
+      a.t12 = tot / shape[0];
+      if (n != shape[0] * tm || toff + tm > a.t12) return set_error(CGL_ESHAPE, "stage: bad column block");
+    } else if (tot != n) {
+      return set_error(CGL_ESHAPE, "stage: shape does not match n");
+    }
     // tables: [fraction(2)][component(nf)][axis(ndim)]
     for (int fr = 0; fr < 2; ++fr)
       for (int c = 0; c < nf; ++c)
