@@ -27,10 +27,6 @@ def P():
     return pkg
 
 
-@pytest.fixture(scope="module")
-def P_pkg(P):
-    return P
-
 
 @pytest.mark.parametrize("i", range(len(SHAPES)))
 def test_mode_product_tucker_kronsum(P, unit_golden, i):
@@ -343,9 +339,9 @@ def test_oz_and_dmma_paths_agree(P, monkeypatch):
     assert rel_l2(out["oz"], out["dmma"]) <= 1e-12
 
 
-@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("nranks", [1, 2, 4])
 @pytest.mark.parametrize("scheme,tag", [("if4", "C3s32_if4"), ("strang", "C3s32_strang")])
-def test_slab_sharded_fourier_virtual_ranks(P_pkg, config_golden, P, scheme, tag):
+def test_slab_sharded_fourier_virtual_ranks(P, config_golden, nranks, scheme, tag):
     """The slab-sharded 3D FFT path (2D FFT + all-to-all + 1D FFT, spectral
     data in transposed column blocks) with P virtual ranks on one GPU
     reproduces the reference (C3 physics on a 32^3 grid)."""
@@ -358,11 +354,11 @@ def test_slab_sharded_fourier_virtual_ranks(P_pkg, config_golden, P, scheme, tag
     prob = W.build_problem(w)
     prob.prepare(w.tau, SCHEMES[scheme])
     uhat = dft_forward(torch.from_numpy(W.initial_state(w)).cuda())
-    plan = SF.ShardedFourierPlan(prob, scheme, w.extents, P, list(range(P)))
+    plan = SF.ShardedFourierPlan(prob, scheme, w.extents, nranks, list(range(nranks)))
     if scheme == "if4":
-        key = plan.run(SF.split_global(uhat, P, "cols"), w.steps, w.tau)
+        key = plan.run(SF.split_global(uhat, nranks, "cols"), w.steps, w.tau)
     else:
-        key = plan.run(SF.split_global(dft_inverse(uhat), P, "slabs"), w.steps, w.tau)
+        key = plan.run(SF.split_global(dft_inverse(uhat), nranks, "slabs"), w.steps, w.tau)
     assert key == (1 << 64) - 1
     got = SF.gather_cols(plan.result_cols(w.steps), w.extents).cpu().numpy()
     assert rel_l2(got, arrays[f"{tag}_out"]) <= 1e-10
