@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--scheme", default=None)
     ap.add_argument("--no-extras", action="store_true", help="skip strang/rk4 side runs and the CPU sample")
     ap.add_argument("--cpu-sample-steps", type=int, default=24)
+    ap.add_argument("--time-steps", type=int, default=0, help="override the workload's step count (3D configs)")
+    ap.add_argument("--sharded", action="store_true", help="use the slab-sharded 3D path even at N = 1")
     return ap.parse_args()
 
 
@@ -96,7 +98,7 @@ def reference_arm(args, w, scheme):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sample = max(1, args.cpu_sample_steps // 3)
+    sample = max(1, int((args.cpu_sample_steps // 3) * (1 << 18) / w.points))
     for _ in range(args.warmup):
         oracle_run(w, scheme, sample)
     tot_s, tot_steps = 0.0, 0
@@ -358,7 +360,8 @@ def gpu_arm(args, w, scheme):
                              "diverged": rr.diverged, "diverged_at": rr.diverged_at, "reason": rr.reason}
             line["per_stepper"] = extras
             if world == 1:
-                sample = args.cpu_sample_steps
+                # bounded CPU sample: ~24 C1-sized time steps worth of work
+                sample = max(1, int(args.cpu_sample_steps * (1 << 18) / w.points))
                 s_cpu, n_cpu = oracle_run(w, scheme, sample)
                 line["cpu_baseline"] = {"value": w.points * n_cpu / s_cpu, "unit": UNIT, "cores": cpu_cores(),
                                         "kind": "port",
@@ -369,13 +372,69 @@ def gpu_arm(args, w, scheme):
         torch.distributed.destroy_process_group()
 
 
+def sharded_arm(args, w, scheme):
+    """3D configs at N > 1: axis-0 slab sharding (FD: NCCL all-to-all inside the
+    axis-0 mode product; Fourier: distributed 3D FFT).  Strong scaling: the
+    global grid is fixed; value = global points x steps / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2403_02816_b200 import SCHEMES, distributed as D, slabfourier as SF, workloads as W
+    from paper_2403_02816_b200.spectral import dft_forward, dft_inverse
+    steps = args.time_steps or w.steps
+    wl = w.scaled(w.extents[0], steps) if steps != w.steps else w
+    prob = W.build_problem(wl)
+    u0 = W.initial_state_device(wl)
+    times = []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        if wl.boundary == "periodic":
+            prob.prepare(wl.tau, SCHEMES[scheme])
+            uhat = dft_forward(u0)
+            plan = SF.ShardedFourierPlan(prob, scheme, wl.extents, world, [rank], dist.group.WORLD)
+            x0 = SF.split_global(uhat if scheme == "if4" else dft_inverse(uhat), world,
+                                 "cols" if scheme == "if4" else "slabs")[rank:rank + 1]
+            del uhat
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            plan.run(x0, steps, wl.tau)
+            e1.record()
+            torch.cuda.synchronize()
+            dt = e0.elapsed_time(e1) / 1e3
+        else:
+            L = D.SlabLayout(wl.extents, world)
+            a, b = L.bounds(rank)
+            x0 = [u0[a:b].contiguous()]
+            _, _, _, dt = D.integrate_sharded(prob, scheme, x0, wl.t_final, steps, L, dist.group.WORLD)
+        if it >= args.warmup:
+            times.append(dt)
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    value = wl.points * steps * args.steps / total
+    if rank == 0:
+        cfg = config_dict(wl, scheme, world)
+        cfg["parallelism"] = f"axis-0 slabs x{world}"
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+                          "config": cfg}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     from paper_2403_02816_b200 import workloads as W
     w = W.CONFIGS[args.workload]
     scheme = args.scheme or w.schemes[0]
+    _, world, _ = dist_env()
     if args.impl == "reference":
         reference_arm(args, w, scheme)
+    elif (world > 1 or args.sharded) and len(w.extents) == 3:
+        sharded_arm(args, w, scheme)
     else:
         gpu_arm(args, w, scheme)
 

@@ -196,3 +196,22 @@ def integrate_sharded(problem, scheme_name, local_fields, t_final, steps, layout
     k_div, reason = key >> 24, key & 0xFF
     out = plan.result(k_div) if reason == _lib.NONFINITE_STATE else plan.result(k_div - 1)
     return out, int(k_div), _lib.REASONS[reason], dev_s
+
+
+def tucker_slabs(slabs, mats, mats_t, ex, flag=None, pos=0):
+    """Tucker chain of an axis-0 slab-sharded 3D field held as a list of the
+    local slabs (one per held rank; all P with virtual ranks), using the
+    slab <-> column-block exchange of slabfourier.SlabExchange: the axis-0
+    product runs on the (n0 x m) column blocks, the others on the slabs."""
+    n0 = ex.shape[0]
+    cols = [torch.empty((n0, ex.m), dtype=torch.complex128, device=s.device) for s in slabs]
+    ex.to_cols(slabs, cols)
+    outc = [mode_product_dev(c, mats[0], mats_t[0], 0, flag=flag, pos=pos) for c in cols]
+    tmp = [torch.empty_like(s) for s in slabs]
+    ex.to_slabs(outc, tmp)
+    out = []
+    for t in tmp:
+        for axis in range(1, t.ndim):
+            t = mode_product_dev(t, mats[axis], mats_t[axis], axis, flag=flag, pos=pos)
+        out.append(t)
+    return out
