@@ -99,6 +99,16 @@ def unit_fixtures():
     out["fft_u"] = u
     out["fft_out"] = rspec.dft_forward(u)
     out["ifft_out"] = rspec.dft_inverse(u)
+    # snapshot bytes (io.py:35-59): reference writer on a small 3D pair
+    import tempfile
+    from cglsolve import io as rio
+    su, sv = rc(rng, (3, 4, 5)), rc(rng, (3, 4, 5))
+    grids = [np.linspace(0.0, 1.0, 3), np.linspace(-1.0, 1.0, 4), np.arange(5.0)]
+    with tempfile.TemporaryDirectory() as td:
+        rio.write_snapshot(td + "/s.cgls", (su, sv), 0.75, grids)
+        out["snap_bytes"] = np.frombuffer(open(td + "/s.cgls", "rb").read(), dtype=np.uint8).copy()
+        out["snap_grid"] = np.frombuffer(open(td + "/s.cgls.grid.txt", "rb").read(), dtype=np.uint8).copy()
+    out["snap_u"], out["snap_v"] = su, sv
     # FD matrices (operators.py:49-85)
     out["fd4_dir_9"] = rops.fd_second_derivative_dirichlet(9, 3.0)
     out["fd4_dn_10"] = rops.fd_second_derivative_dirichlet_neumann(10, 3.0)

@@ -159,3 +159,27 @@ def test_workloads_are_baseline_configs():
     assert x[0] == pytest.approx(-20.0 + 40.0 / 129.0)
     g = workloads.initial_state(C["C4"].scaled(16))
     assert g.shape == (16, 16, 16) and np.all(np.isfinite(g))
+
+
+def test_snapshot_bitwise_vs_reference(unit_golden, tmp_path):
+    """write_snapshot reproduces the reference writer's bytes exactly
+    (io.py:35-59), and read_snapshot round-trips them."""
+    from paper_2403_02816_b200 import io as cio
+    g = unit_golden
+    grids = [np.linspace(0.0, 1.0, 3), np.linspace(-1.0, 1.0, 4), np.arange(5.0)]
+    path = tmp_path / "s.cgls"
+    cio.write_snapshot(path, (g["snap_u"], g["snap_v"]), 0.75, grids)
+    assert path.read_bytes() == g["snap_bytes"].tobytes()
+    assert (tmp_path / "s.cgls.grid.txt").read_bytes() == g["snap_grid"].tobytes()
+    (u, v), t = cio.read_snapshot(path)
+    assert t == 0.75 and u.tobytes() == g["snap_u"].tobytes() and v.tobytes() == g["snap_v"].tobytes()
+
+
+def test_snapshot_errors(tmp_path):
+    from paper_2403_02816_b200 import io as cio
+    p = tmp_path / "bad.cgls"
+    p.write_bytes(b"WAT?" + b"\x00" * 64)
+    with pytest.raises(ValueError, match="magic"):
+        cio.read_snapshot(p)
+    with pytest.raises(ValueError):
+        cio.write_snapshot(tmp_path / "x.cgls", (np.zeros((2, 3)), np.zeros((3, 2))), 0.0, [range(2), range(3)])
