@@ -79,6 +79,15 @@ def _worker(rank, world, port, q):
         flag[0] = ((7 << 24) | 5) if rank == 0 else (0x7F << 56)
         global_min_key(flag)
         res["key2"] = int(flag[0].item())
+        # slab-sharded Fourier exchange (real ranks): slab -> column block -> slab
+        from paper_2403_02816_b200.slabfourier import SlabExchange
+        ex = SlabExchange(SHAPE, world, [rank], group=dist.group.WORLD, device="cpu")
+        cols = [torch.empty((SHAPE[0], ex.m), dtype=torch.complex128)]
+        ex.to_cols([local], cols)
+        res["fcols"] = torch.equal(cols[0], flat[:, rank * ex.m:(rank + 1) * ex.m])
+        back2 = [torch.empty_like(local)]
+        ex.to_slabs(cols, back2)
+        res["froundtrip"] = torch.equal(back2[0], local)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -98,6 +107,7 @@ def test_slab_sharded_path_gloo(world):
         assert p.exitcode == 0
     for rank, res in results.items():
         assert res["cols"] and res["roundtrip"], (rank, res)
+        assert res["fcols"] and res["froundtrip"], (rank, res)
         assert res["mode0"] <= 1e-14 and res["tucker"] <= 1e-14, (rank, res)
         assert res["key"] == (3 << 24) | (1 << 8) | 4
         assert res["key2"] == (7 << 24) | 5
