@@ -147,6 +147,18 @@ __device__ __forceinline__ double pow2(int e) {
   return __longlong_as_double((long long)(e + 64 + 1023) << 52) * 5.421010862427522e-20;  // * 2^-64
 }
 
+#define LD32x32b_X16(r, taddr)                                                                              \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
+                 "=r"(r[15])                                                                                     \
+               : "r"(taddr))
+#define ST32x32b_X16(taddr, r)                                                                              \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" \
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),        \
+               "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
+               "r"(r[15]))
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---- operand slicing ---------------------------------------------------------
@@ -443,8 +455,10 @@ struct OzCfg {
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
 };
 
+constexpr int OZ_THREADS = 320;  // warp 0 producer, warp 1 MMA issuer, warps 2-9 epilogue
+
 template <int S, int BN, int STAGES>
-__global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(const OzArgs a) {
+__global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(const OzArgs a) {
   using Cfg = OzCfg<S, BN, STAGES>;
   if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -480,13 +494,15 @@ __global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp >= 2) {
-    // zero all level accumulators so every MMA accumulates (blocks may be skipped)
-    const uint32_t q = warp & 3;
-    uint32_t zr[32];
+    // zero all level accumulators so every MMA accumulates (blocks may be skipped);
+    // epilogue warp pairs share a TMEM lane quadrant and split the columns
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t zr[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) zr[j] = 0u;
+    for (int j = 0; j < 16; ++j) zr[j] = 0u;
 #pragma unroll 1
-    for (int col = 0; col < S * BN; col += 32) ST32x32b_X32(tmem + (q * 32 << 16) + col, zr);
+    for (int level = 0; level < S; ++level)
+      ST32x32b_X16(tmem + (q * 32 << 16) + level * BN + half * (BN / 2), zr);
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
   tc_fence_before();
@@ -564,30 +580,27 @@ __global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(co
     }
     mma_commit(tfull);
   } else if (warp >= 2) {
-    // ---- epilogue ----
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    const int row = q * 32 + lane;
+    // ---- epilogue: 8 warps, warp pairs share a TMEM lane quadrant (BN/2 columns each) ----
+    constexpr int HC = BN / 2;
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int row = q * 32 + lane;  // real row of the tile (2i + part)
     mbar_wait(tfull, 0);
     tc_fence_after();
-    if (lane == 0) OZ_TRACE(48 + (warp - 2));  // per epilogue warp: tmem-full seen (slots 48..51)
-    double acc[BN];
+    if (lane == 0 && warp < 6) OZ_TRACE(48 + (warp - 2));
+    double acc[HC];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.0;
+    for (int j = 0; j < HC; ++j) acc[j] = 0.0;
 #pragma unroll 1
     for (int level = S - 1; level >= 0; --level) {  // smallest weights first
-      const double w = ldexp(1.0, -7 * (level + 2));
+      const double w = pow2(-7 * (level + 2));
+      uint32_t r[HC];
+      LD32x32b_X16(r, tmem + ((uint32_t)(q * 32) << 16) + level * BN + half * HC);
+      tmem_wait_ld();
 #pragma unroll
-      for (int h = 0; h < BN / 32; ++h) {
-        uint32_t r[32];
-        LD32x32b_X32(r, tmem + ((uint32_t)(q * 32) << 16) + level * BN + h * 32);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[h * 32 + j] = fma((double)(int)r[j], w, acc[h * 32 + j]);
-      }
+      for (int j = 0; j < HC; ++j) acc[j] = fma((double)(int)r[j], w, acc[j]);
     }
-    if (lane == 0) OZ_TRACE(44 + (warp - 2));  // per epilogue warp: level loop done (slots 44..47)
-    // scale by 2^(e_row + e_col) (exact power-of-two multiplies, column scales
-    // broadcast from smem) and stage [row][col] in smem (stages are free now)
+    if (lane == 0 && warp < 6) OZ_TRACE(44 + (warp - 2));
+    // exact power-of-two scales: rows from Ae, columns broadcast from smem
     __shared__ double colscale[BN];
     const int ct = threadIdx.x - 64;
     if (ct < BN) {
@@ -595,35 +608,37 @@ __global__ void __launch_bounds__(192, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(co
       const int eb = (col < a.N) ? it.Be[b * a.sBeb + col] : 0;
       colscale[ct] = eb == NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(eb);
     }
-    asm volatile("bar.sync 1, 128;\n" ::);
-    const int64_t R = (int64_t)tm * BM + row;  // real row of Chat
+    asm volatile("bar.sync 1, 256;\n" ::);
+    const int64_t R = (int64_t)tm * BM + row;
     const int64_t i = R >> 1;
+    const int part = lane & 1;  // 0: Re row, 1: Im row (rows 2i, 2i+1 sit in adjacent lanes)
     const int ea = (i < a.M) ? it.Ae[b * a.sAeb + i] : 0;
     const double rs = ea == NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(ea);
-    double* stg = reinterpret_cast<double*>(stage_base);
+    double v[HC];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) stg[row * (BN + 1) + j] = (acc[j] * rs) * colscale[j];
-    asm volatile("bar.sync 1, 128;\n" ::);
-    if (threadIdx.x == 64) OZ_TRACE(41);
-    // complex rows tm*64 .. +64, cols tn*BN .. +BN: re = row 2i', im = row 2i'+1
+    for (int j = 0; j < HC; ++j) v[j] = (acc[j] * rs) * colscale[half * HC + j];
+    // lane pairs swap halves: the Re lane writes columns 0..HC/2-1, the Im lane HC/2..HC-1
+    double2 out[HC / 2];
+#pragma unroll
+    for (int c = 0; c < HC / 2; ++c) {
+      const double send = part ? v[c] : v[c + HC / 2];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      out[c] = part ? make_double2(recv, v[c + HC / 2]) : make_double2(v[c], recv);
+    }
     double2* C = it.C + b * a.sCb;
-    const int et = threadIdx.x - 64;
-    if (!a.trans_c) {
-      for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
-        const int ii = idx / BN, j = idx % BN;
-        const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
-        if (gi < a.M && gj < a.N)
-          C[gi * a.ldc + gj] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
-      }
-    } else {
-      // transposed store: consecutive threads walk i, contiguous in C
-      for (int idx = et; idx < (BM / 2) * BN; idx += 128) {
-        const int ii = idx % (BM / 2), j = idx / (BM / 2);
-        const int64_t gi = (int64_t)tm * (BM / 2) + ii, gj = (int64_t)tn * BN + j;
-        if (gi < a.M && gj < a.N)
-          C[gj * a.ldc + gi] = make_double2(stg[(2 * ii) * (BN + 1) + j], stg[(2 * ii + 1) * (BN + 1) + j]);
+    const int64_t col0 = (int64_t)tn * BN + half * HC + part * (HC / 2);
+    if (i < a.M) {
+      if (!a.trans_c) {
+#pragma unroll
+        for (int c = 0; c < HC / 2; ++c)
+          if (col0 + c < a.N) C[i * a.ldc + col0 + c] = out[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < HC / 2; ++c)
+          if (col0 + c < a.N) C[(col0 + c) * a.ldc + i] = out[c];
       }
     }
+    if (threadIdx.x == 64) OZ_TRACE(41);
   }
   tc_fence_before();
   __syncthreads();
@@ -731,7 +746,7 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
   }
   const int64_t blocks = (int64_t)a.mtiles * a.ntiles * a.batch * nitems;
   if (blocks <= 0) return 0;
-  kern<<<(unsigned)blocks, 192, Cfg::SMEM, st>>>(a);
+  kern<<<(unsigned)blocks, oz::OZ_THREADS, Cfg::SMEM, st>>>(a);
   return check_launch("ozgemm_kernel");
 }
 

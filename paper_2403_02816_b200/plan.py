@@ -198,11 +198,21 @@ class FusedPlan:
             s.wait_stream(torch.cuda.current_stream())
             lib = _lib.load()
             n0 = lib.cgl_launch_count()
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    for j in range(count):
-                        self.step(k0 + j, flag, tau)
-                    _lib.flag_advance(flag, count)
+            # no garbage collection while capturing: a finaliser that frees device
+            # memory (e.g. a cuFFT plan) would invalidate the capture
+            import gc
+            gc.collect()
+            was = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                        for j in range(count):
+                            self.step(k0 + j, flag, tau)
+                        _lib.flag_advance(flag, count)
+            finally:
+                if was:
+                    gc.enable()
             torch.cuda.current_stream().wait_stream(s)
             self.graph_launches[key] = lib.cgl_launch_count() - n0
             self.graphs[key] = g
