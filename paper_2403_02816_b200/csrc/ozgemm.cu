@@ -576,6 +576,7 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
           }
         }
       }
+      if (it_n <= 8) OZ_TRACE(55 + it_n);   // MMA: chunk issue finished (slots 56..63)
       mma_commit(&empty[st]);  // frees the stage when these MMAs complete
     }
     mma_commit(tfull);
@@ -587,18 +588,35 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
     mbar_wait(tfull, 0);
     tc_fence_after();
     if (lane == 0 && warp < 6) OZ_TRACE(48 + (warp - 2));
-    double acc[HC];
+    // Exact integer recombination of the levels: levels 0..3 (d = 2..5) and
+    // 4..S-1 (d = 6..S+1) are folded base-128 into two int64 sums, each below
+    // 2^53 in magnitude, so the FP64 result is one rounding of
+    // hi 2^-35 + lo 2^-7(S+1) (no per-level int->double conversions).
+    long long hi[HC], lo[HC];
 #pragma unroll
-    for (int j = 0; j < HC; ++j) acc[j] = 0.0;
-#pragma unroll 1
-    for (int level = S - 1; level >= 0; --level) {  // smallest weights first
-      const double w = pow2(-7 * (level + 2));
-      uint32_t r[HC];
-      LD32x32b_X16(r, tmem + ((uint32_t)(q * 32) << 16) + level * BN + half * HC);
+    for (int j = 0; j < HC; ++j) hi[j] = lo[j] = 0;
+#pragma unroll
+    for (int level = 0; level < S; level += 2) {
+      uint32_t r0[HC], r1[HC];
+      LD32x32b_X16(r0, tmem + ((uint32_t)(q * 32) << 16) + level * BN + half * HC);
+      if (level + 1 < S) LD32x32b_X16(r1, tmem + ((uint32_t)(q * 32) << 16) + (level + 1) * BN + half * HC);
       tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < HC; ++j) acc[j] = fma((double)(int)r[j], w, acc[j]);
+      for (int j = 0; j < HC; ++j) {
+        const long long d0 = (long long)(int)r0[j];
+        if (level < 4) hi[j] = hi[j] * 128 + d0; else lo[j] = lo[j] * 128 + d0;
+        if (level + 1 < S) {
+          const long long d1 = (long long)(int)r1[j];
+          if (level + 1 < 4) hi[j] = hi[j] * 128 + d1; else lo[j] = lo[j] * 128 + d1;
+        }
+      }
     }
+    // hi carries 4 levels (or S if S < 4): weight of its last level
+    constexpr int HL = S < 4 ? S : 4;
+    const double whi = pow2(-7 * (HL + 1)), wlo = pow2(-7 * (S + 1));
+    double acc[HC];
+#pragma unroll
+    for (int j = 0; j < HC; ++j) acc[j] = fma((double)hi[j], whi, (double)lo[j] * wlo);
     if (lane == 0 && warp < 6) OZ_TRACE(44 + (warp - 2));
     // exact power-of-two scales: rows from Ae, columns broadcast from smem
     __shared__ double colscale[BN];

@@ -27,7 +27,10 @@ names = {0: "start", 1: "setup done (barriers, TMEM alloc+zero)", 40: "epilogue:
          42: "end"}
 names.update({44 + i: f"epilogue warp {i + 2}: levels done" for i in range(4)})
 names.update({48 + i: f"epilogue warp {i + 2}: tmem full seen" for i in range(4)})
+names.update({55 + i: f"mma chunk {i} issued" for i in range(1, 9)})
 for i in range(64):
     if buf[i]:
         lab = names.get(i, f"producer chunk {i - 2}" if 3 <= i <= 18 else f"mma chunk {i - 18} ready")
+        if 56 <= i <= 63:
+            lab = f"mma chunk {i - 55} issued"
         print(f"{(buf[i] - t0) / 1e3:8.2f} us  {lab}")
