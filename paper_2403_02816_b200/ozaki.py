@@ -75,62 +75,92 @@ class Workspace:
 
 
 def fits(shape, nfields):
-    """Data-slice workspace for one mode of `nfields` fields must stay small
-    next to the fields themselves (1024^3 fields keep the DMMA path)."""
-    pts = math.prod(shape)
-    if pts < (1 << 17):
-        return False  # small grids (C0 128^2) are launch-latency bound: the DMMA path is faster
-    need = nfields * pts * 16 * S // 8 + (1 << 20)
-    free, _ = torch.cuda.mem_get_info()
-    return need < min(8 << 30, free // 4)
+    """Small grids (C0 128^2) are launch-latency bound: the DMMA path is faster."""
+    return math.prod(shape) >= (1 << 17)
+
+
+# data-slice workspace budget per field (bytes); larger products are chunked
+CHUNK_BYTES = int(os.environ.get("CGL_OZ_CHUNK_BYTES", str(2 << 30)))
+
+
+def _chunks(total, per_unit, nf, align=128):
+    """Split `total` units (rows of Z or batches) so one chunk's slices for
+    all nf fields stay under CHUNK_BYTES."""
+    units = max(1, CHUNK_BYTES // max(1, per_unit * nf))
+    if units < total:
+        units = max(align, units // align * align)  # whole row tiles per chunk
+    return [(a, min(total, a + units)) for a in range(0, total, units)]
 
 
 def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
-    """outs[f] = ins[f] x_axis E_f for square E_f (SlicedFactor), one GEMM launch."""
+    """outs[f] = ins[f] x_axis E_f for square E_f (SlicedFactor), one GEMM
+    launch per chunk (one chunk unless the data slices would exceed
+    CHUNK_BYTES, e.g. 1024^3 fields)."""
     lib = _lib.load()
     st = _lib.stream()
     shape = tuple(ins[0].shape)
-    nd = len(shape)
     n = shape[axis]
     P = math.prod(shape[:axis])
     Q = math.prod(shape[axis + 1:])
     nf = len(ins)
     dev = ins[0].device
-    if Q > 1:
-        # left form per slab b: Out_b (n x Q) = E (n x n) In_b (n x Q); data on the B side,
-        # Z_b = In_b^T (Q x n): Z(r = q, c = k) = In_b[k, q] -> sr = 1, sc = Q
+    Aa = _lib.ptr_array([fc.A for fc in factors])
+    Ae = _lib.ptr_array([fc.Ae for fc in factors])
+    Az = _lib.ptr_array([fc.Az for fc in factors])
+    if Q > 1 and P > 1:
+        # middle axis: per slab b, Out_b (n x Q) = E In_b; chunk over slabs
         per = _nbytes(Q, n, 0)
-        Bs, Be = [], []
-        for f in range(nf):
-            buf, ex = ws.get(("B", f), per * P, Q * P, dev)
-            Bs.append(buf)
-            Be.append(ex)
-        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), 1, Q, Q, n, P, n * Q, 0,
-                                          _lib.ptr_array(Bs), per, _lib.ptr_array(Be), Q), "oz_slice(data, B)")
-        rc = lib.cgl_oz_gemm(st, S, n, Q, n, nf,
-                             _lib.ptr_array([fc.A for fc in factors]), _lib.ptr_array([fc.Ae for fc in factors]),
-                             _lib.ptr_array([fc.Az for fc in factors]),
-                             _lib.ptr_array(Bs), _lib.ptr_array(Be), None,
-                             _lib.ptr_array(outs), Q, P, 0, 0, per, Q, n * Q, _lib.flag_ptr(flag), pos)
-        _lib.check(rc, "oz_gemm(left)")
+        for b0, b1 in _chunks(P, per, nf, align=1):
+            nb = b1 - b0
+            Bs, Be = [], []
+            for f in range(nf):
+                buf, ex = ws.get(("D", f, n), per * nb, Q * nb, dev)
+                Bs.append(buf)
+                Be.append(ex)
+            srcs = [x.view(-1)[b0 * n * Q:] for x in ins]
+            dsts = [o.view(-1)[b0 * n * Q:] for o in outs]
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), 1, Q, Q, n, nb, n * Q, 0,
+                                              _lib.ptr_array(Bs), per, _lib.ptr_array(Be), Q), "oz_slice(data, B)")
+            _lib.check(lib.cgl_oz_gemm(st, S, n, Q, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
+                                       None, _lib.ptr_array(dsts), Q, nb, 0, 0, per, Q, n * Q,
+                                       _lib.flag_ptr(flag), pos), "oz_gemm(middle)")
+    elif Q > 1:
+        # first axis (P = 1): Out (n x Q) = E In; data Z = In^T rows q; chunk over q
+        per_row = _nbytes(1 << 10, n, 0) >> 10 if Q >= (1 << 10) else _nbytes(Q, n, 0) // Q
+        for q0, q1 in _chunks(Q, per_row, nf):
+            nq = q1 - q0
+            per = _nbytes(nq, n, 0)
+            Bs, Be = [], []
+            for f in range(nf):
+                buf, ex = ws.get(("D", f, n), per, nq, dev)
+                Bs.append(buf)
+                Be.append(ex)
+            srcs = [x.view(-1)[q0:] for x in ins]
+            dsts = [o.view(-1)[q0:] for o in outs]
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), 1, Q, nq, n, 1, 0, 0,
+                                              _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, B)")
+            _lib.check(lib.cgl_oz_gemm(st, S, n, nq, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
+                                       None, _lib.ptr_array(dsts), Q, 1, 0, 0, 0, 0, 0,
+                                       _lib.flag_ptr(flag), pos), "oz_gemm(first)")
     else:
-        # last axis: Out (P x n) = In (P x n) E^T computed as Out^T = E In^T, so the
-        # constant E stays on the block-skipped A side; data on the B side with
-        # Z = In (rows p, K = k contiguous); C stored transposed (ldc = n)
-        per = _nbytes(P, n, 0)
-        Bs, Be = [], []
-        for f in range(nf):
-            buf, ex = ws.get(("Bt", f), per, P, dev)
-            Bs.append(buf)
-            Be.append(ex)
-        _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(ins), n, 1, P, n, 1, 0, 0,
-                                          _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, Bt)")
-        rc = lib.cgl_oz_gemm_t(st, S, n, P, n, nf,
-                               _lib.ptr_array([fc.A for fc in factors]), _lib.ptr_array([fc.Ae for fc in factors]),
-                               _lib.ptr_array([fc.Az for fc in factors]),
-                               _lib.ptr_array(Bs), _lib.ptr_array(Be), None,
-                               _lib.ptr_array(outs), n, 1, 0, 0, 0, 0, 0, _lib.flag_ptr(flag), pos)
-        _lib.check(rc, "oz_gemm(last axis)")
+        # last axis: Out (P x n) = In E^T computed as Out^T = E In^T (constant E on the
+        # block-skipped A side); data Z = In rows p (K contiguous); chunk over p
+        per_row = max(1, _nbytes(min(P, 1 << 10), n, 0) // min(P, 1 << 10))
+        for p0, p1 in _chunks(P, per_row, nf):
+            np_ = p1 - p0
+            per = _nbytes(np_, n, 0)
+            Bs, Be = [], []
+            for f in range(nf):
+                buf, ex = ws.get(("D", f, n), per, np_, dev)
+                Bs.append(buf)
+                Be.append(ex)
+            srcs = [x.view(-1)[p0 * n:] for x in ins]
+            dsts = [o.view(-1)[p0 * n:] for o in outs]
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), n, 1, np_, n, 1, 0, 0,
+                                              _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, Bt)")
+            _lib.check(lib.cgl_oz_gemm_t(st, S, n, np_, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
+                                         None, _lib.ptr_array(dsts), n, 1, 0, 0, 0, 0, 0,
+                                         _lib.flag_ptr(flag), pos), "oz_gemm(last axis)")
     return outs
 
 

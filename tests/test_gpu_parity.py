@@ -246,10 +246,12 @@ def test_lean_plan_matches_batched(P, config_golden, monkeypatch):
 # cannot run C3/C4 at full size inside a test budget).
 # ---------------------------------------------------------------------------
 
-def test_c4_full_size_tucker_rank1(P):
+@pytest.mark.parametrize("gemm", ["dmma", "oz"])
+def test_c4_full_size_tucker_rank1(P, gemm):
     """C4 grid (1024^3, 2nd-order Dirichlet, tau = 0.005): exp(tau K) of a
     rank-1 (separable) field is the outer product of the three 1D actions
-    E_mu f_mu -- checks the full-size DMMA mode products (17 GB field)."""
+    E_mu f_mu -- checks the full-size DMMA and (chunked) INT8-emulated mode
+    products (17 GB field)."""
     from paper_2403_02816_b200 import workloads as W
     from paper_2403_02816_b200.tensors import tucker_dev
     w = W.CONFIGS["C4"]
@@ -259,7 +261,13 @@ def test_c4_full_size_tucker_rank1(P):
     ax = [torch.from_numpy(x).cuda() for x in W.axes(w)]
     f = [torch.exp(-(x - 0.3 * (i + 1)) ** 2 / 8.0).to(torch.complex128) * (1 + 0.5j * i) for i, x in enumerate(ax)]
     u = f[0][:, None, None] * f[1][None, :, None] * f[2][None, None, :]
-    out = tucker_dev([u], [mats], [mts])[0]
+    if gemm == "dmma":
+        out = tucker_dev([u], [mats], [mts])[0]
+    else:
+        from paper_2403_02816_b200 import ozaki
+        out, work = torch.empty_like(u), torch.empty_like(u)
+        ozaki.tucker_oz([u], [[ozaki.SlicedFactor(m) for m in mats]], [out], [work], ozaki.Workspace())
+        del work
     del u
     g = [m @ v for m, v in zip(mats, f)]
     want_norm2 = float(np.prod([torch.sum(torch.abs(v) ** 2).item() for v in g]))
@@ -337,6 +345,32 @@ def test_oz_and_dmma_paths_agree(P, monkeypatch):
         monkeypatch.setenv("CGL_GEMM", gemm)
         out[gemm] = P.integrate(W.build_problem(w), "if4", (u0,), w.tau * 40, 40).fields[0]
     assert rel_l2(out["oz"], out["dmma"]) <= 1e-12
+
+
+def test_oz_chunked_products_bit_identical(P, monkeypatch):
+    """Chunking the data slices (first axis over columns, middle axis over
+    slabs, last axis over rows; what 1024^3 fields use) changes no bit of the
+    emulated mu-mode products, and each product matches the DMMA one."""
+    from paper_2403_02816_b200 import ozaki, tensors
+    g = torch.Generator().manual_seed(7)
+    shape = (64, 96, 160)
+    x = torch.complex(torch.randn(shape, generator=g, dtype=torch.float64),
+                      torch.randn(shape, generator=g, dtype=torch.float64)).cuda()
+    res = {}
+    for cb in (1 << 40, 200_000):
+        monkeypatch.setattr(ozaki, "CHUNK_BYTES", cb)
+        ws = ozaki.Workspace()
+        for axis, n in enumerate(shape):
+            E = torch.complex(torch.randn(n, n, generator=g.manual_seed(n), dtype=torch.float64),
+                              torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+            out = torch.empty_like(x)
+            ozaki.mode_product_oz([x], [ozaki.SlicedFactor(E)], [out], axis, ws)
+            res[(cb, axis)] = out
+            if cb == 200_000:
+                ref = tensors.mode_product_dev(x, E, E.transpose(0, 1).contiguous(), axis)
+                assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
+    for axis in range(3):
+        assert torch.equal(res[(1 << 40, axis)], res[(200_000, axis)])
 
 
 @pytest.mark.parametrize("nranks", [1, 2, 4])
