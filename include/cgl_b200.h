@@ -160,7 +160,7 @@ int cgl_oz_gemm_t(void* stream, int S, int64_t M, int64_t N, int64_t K, int nite
 int cgl_oz_geometry(int* bm, int* bn, int* kc);
 /* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last
  * cgl_oz_gemm records phase timestamps (ns); copies 64 slots to host64. */
-int cgl_oz_trace(long long* host64);
+int cgl_oz_trace(long long* host128);
 /* Block sparsity of a sliced CONSTANT operand: zmap[tile][chunk] = first
  * non-zero slice (S+1: block all zero); rows/cols/a_mode as in cgl_oz_slice. */
 int cgl_oz_zmap(void* stream, int S, const int8_t* slices, int64_t rows, int64_t cols,

@@ -31,8 +31,8 @@ def nvcc_path():
     return "nvcc"
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+def sources(csrc=CSRC):
+    return sorted(glob.glob(os.path.join(csrc, "*.cu")))
 
 
 def _deps():
@@ -48,15 +48,17 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, csrc=CSRC, out=LIB):
+    """Build `out` from the sources in `csrc` (defaults: the package library;
+    other values only for kernel A/B experiments, see tools/oz_bench.py)."""
+    if out == LIB and not force and not needs_build():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     objs = []
     nvcc = nvcc_path()
-    for src in sources():
+    for src in sources(csrc):
         obj = os.path.join(LIB_DIR, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
                "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
@@ -64,16 +66,16 @@ def build(force=False, verbose=False):
         if r.returncode:
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcufft", "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

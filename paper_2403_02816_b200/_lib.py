@@ -127,7 +127,10 @@ def load():
     if _LIB is not None:
         return _LIB
     path = _build.LIB
-    if not os.path.exists(path) or _build.needs_build():
+    override = os.environ.get("CGL_LIB_OVERRIDE")  # kernel A/B experiments (tools/oz_bench.py)
+    if override:
+        path = override
+    elif not os.path.exists(path) or _build.needs_build():
         try:
             _build.build()
         except (RuntimeError, FileNotFoundError) as e:

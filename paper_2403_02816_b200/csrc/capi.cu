@@ -339,9 +339,9 @@ int cgl_oz_geometry(int* bm, int* bn, int* kc) {
   return 0;
 }
 
-int cgl_oz_trace(long long* host64) {
+int cgl_oz_trace(long long* host128) {
   if (!g_oz_trace) return -1;
-  cudaError_t e = cudaMemcpy(host64, g_oz_trace, 64 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(host128, g_oz_trace, 128 * sizeof(long long), cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? 0 : (int)e;
 }
 

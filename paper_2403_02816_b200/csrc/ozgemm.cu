@@ -68,6 +68,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity));
 }
+// wait with back-off for roles that do not need sub-100 ns wake-up (keeps
+// spinning warps off the shared-memory port the tensor core reads from)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity));
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                    smem_u32(dst)),
@@ -113,6 +131,24 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// warp-uniform issue: every lane executes the call with identical operands and
+// one elected lane issues (keeps descriptors warp-uniform, no per-MMA
+// R2UR/ELECT loop around the instruction)
+__device__ __forceinline__ void mma_i8_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc));
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -430,6 +466,7 @@ struct OzArgs {
   const cgl_flag_t* flag;
   uint64_t pos;
   long long* trace;  // optional: CTA 0 phase timestamps (globaltimer ns), see OZ_TRACE
+  int debug;         // CGL_OZ_DEBUG (timing experiments only; results invalid): 1 skip MMAs, 2 skip copies
   OzItem items[kMaxItems];
 };
 
@@ -667,6 +704,308 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
   }
 }
 
+
+// ---- persistent variant -------------------------------------------------------
+// One CTA per SM walks tiles t = blockIdx.x, +gridDim.x, ...; the S level
+// accumulators are double-buffered in TMEM (2 x S x BN <= 512 columns) so the
+// epilogue of tile j (TMEM -> registers -> HBM) overlaps the MMAs of tile
+// j+1, and the smem ring keeps streaming across tile boundaries.  Same
+// operands, zero maps and arithmetic as ozgemm_kernel (bit-identical).
+// warps 0, 10, 11, 12: producers (producer p owns ring stage p: bulk copies
+// serialise per issuing warp, ~0.4 us each, so one warp per in-flight stage);
+// warp 1: MMA issuer; warps 2-9: epilogue
+constexpr int OZP_PRODUCERS = 4;
+constexpr int OZP_THREADS = 32 * (10 + OZP_PRODUCERS - 1);
+
+template <int S, int BN, int STAGES>
+struct OzPCfg {
+  static constexpr int A_BYTES = BM * KC;
+  static constexpr int B_BYTES = BN * KC;
+  static constexpr int STAGE_BYTES = S * (A_BYTES + B_BYTES);
+  static constexpr int BODY = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BODY + 256;
+  static constexpr uint32_t ACC_COLS = S * BN;
+  static_assert(2 * S * BN <= 512, "two level buffers must fit the 512 TMEM columns");
+};
+
+template <int S, int BN, int STAGES>
+__global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const OzArgs a, int64_t total) {
+  using Cfg = OzPCfg<S, BN, STAGES>;
+  if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stage_base = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BODY);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2] MMAs of the buffer's tile done
+  uint64_t* acc_empty = acc_full + 2;   // [2] epilogue has read (and re-zeroed) the buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) OZ_TRACE(0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp >= 2 && warp < 10) {
+    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t zr[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) zr[j] = 0u;
+#pragma unroll 1
+    for (int level = 0; level < 2 * S; ++level)
+      ST32x32b_X16(tmem + (q * 32 << 16) + level * BN + half * (BN / 2), zr);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) OZ_TRACE(1);
+
+  const int nch = a.nchunks;
+  const int64_t step = gridDim.x;
+  if (warp == 0 || warp >= 10) {
+    // ---- producers: one ring across all tiles of this CTA.  Every producer
+    // warp reads the zero maps 32 chunks at a time (one load latency per 32
+    // chunks, ballot of the live ones); producer p issues the copies of the
+    // live chunks it_n with it_n % STAGES == p (its own stage). ----
+    static_assert(STAGES == OZP_PRODUCERS, "one producer warp per stage");
+    const int pw = warp == 0 ? 0 : warp - 9;
+    int it_n = 0;
+    for (int64_t t = blockIdx.x; t < total; t += step) {
+      int64_t bid = t;
+      const int tn = (int)(bid % a.ntiles);
+      bid /= a.ntiles;
+      const int tm = (int)(bid % a.mtiles);
+      bid /= a.mtiles;
+      const int64_t b = bid % a.batch;
+      const OzItem& it = a.items[(int)(bid / a.batch)];
+      const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * S * Cfg::A_BYTES;
+      const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * S * Cfg::B_BYTES;
+      const int8_t* az = it.Az ? it.Az + (int64_t)tm * nch : nullptr;
+      const int8_t* bz = it.Bz ? it.Bz + (int64_t)tn * nch : nullptr;
+      for (int c0 = 0; c0 < nch; c0 += 32) {
+        int zal = S + 1, zbl = S + 1;
+        if (c0 + lane < nch) {
+          zal = az ? az[c0 + lane] : 1;
+          zbl = bz ? bz[c0 + lane] : 1;
+        }
+        unsigned live = __ballot_sync(0xffffffffu, zal + zbl <= S + 1);
+        while (live) {
+          const int l = __ffs(live) - 1;
+          live &= live - 1;
+          const int za = __shfl_sync(0xffffffffu, zal, l), zb = __shfl_sync(0xffffffffu, zbl, l);
+          if (lane == 0 && it_n % STAGES == pw) {
+            const int c = c0 + l;
+            const int st = it_n % STAGES;
+            const uint32_t ph = (it_n / STAGES) & 1;
+            mbar_wait_sleep(&empty[st], ph ^ 1, 64);
+            if (it_n < 8) OZ_TRACE(44 + it_n);
+            if (it_n >= 8 && it_n < 16) OZ_TRACE(96 + it_n);
+            const int na = S + 2 - zb - za;
+            if (a.debug & 2) {
+              mbar_arrive(&full[st]);
+            } else {
+              mbar_expect_tx(&full[st], na * (Cfg::A_BYTES + Cfg::B_BYTES));
+              uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+              uint8_t* sb = sa + S * Cfg::A_BYTES;
+              bulk_g2s(sa + (za - 1) * Cfg::A_BYTES, A + ((int64_t)c * S + (za - 1)) * Cfg::A_BYTES,
+                       na * Cfg::A_BYTES, &full[st]);
+              bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
+                       na * Cfg::B_BYTES, &full[st]);
+            }
+          }
+          ++it_n;
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: the whole warp runs the (warp-uniform) loop, one
+    // elected lane issues each tcgen05 instruction ----
+    constexpr uint32_t LBO = 128, SBO = (KC / 16) * 128;
+    constexpr int PER = 256 / BN;
+    int it_n = 0, j = 0;
+    for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
+      int64_t bid = t;
+      const int tn = (int)(bid % a.ntiles);
+      bid /= a.ntiles;
+      const int tm = (int)(bid % a.mtiles);
+      bid /= a.mtiles;
+      const OzItem& it = a.items[(int)(bid / a.batch)];
+      const int8_t* az = it.Az ? it.Az + (int64_t)tm * nch : nullptr;
+      const int8_t* bz = it.Bz ? it.Bz + (int64_t)tn * nch : nullptr;
+      const int buf = j & 1;
+      mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0 && j < 8) OZ_TRACE(3 + j);
+      const uint32_t dt = tmem + buf * Cfg::ACC_COLS;
+      for (int c0 = 0; c0 < nch; c0 += 32) {
+        int zal = S + 1, zbl = S + 1;
+        if (c0 + lane < nch) {
+          zal = az ? az[c0 + lane] : 1;
+          zbl = bz ? bz[c0 + lane] : 1;
+        }
+        unsigned live = __ballot_sync(0xffffffffu, zal + zbl <= S + 1);
+        while (live) {
+          const int l = __ffs(live) - 1;
+          live &= live - 1;
+          const int za = __shfl_sync(0xffffffffu, zal, l), zb = __shfl_sync(0xffffffffu, zbl, l);
+          const int st = it_n % STAGES;
+          const uint32_t ph = (it_n / STAGES) & 1;
+          mbar_wait(&full[st], ph);  // TMA writes -> MMA reads: ordered by complete_tx
+          if (lane == 0 && it_n < 8) OZ_TRACE(52 + it_n);
+          if (lane == 0 && it_n >= 8 && it_n < 16) OZ_TRACE(80 + it_n);
+          if (!(a.debug & 1)) {
+            const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+            const uint64_t ad0 = make_desc(sa, LBO, SBO), bd0 = make_desc(sa + S * Cfg::A_BYTES, LBO, SBO);
+#pragma unroll
+            for (int ks = 0; ks < KC / 32; ++ks) {
+#pragma unroll
+              for (int s = 1; s <= S; ++s) {
+                if (s < za || s > S + 1 - zb) continue;
+                const uint64_t ad = ad0 + (uint64_t)((((s - 1) * Cfg::A_BYTES) + ks * 256) >> 4);
+#pragma unroll
+                for (int blk = 0; blk < (S + PER - 1) / PER; ++blk) {
+                  const int t0 = zb + blk * PER;
+                  if (t0 > S + 1 - s) continue;
+                  const int cnt = (S + 2 - s - t0) < PER ? (S + 2 - s - t0) : PER;
+                  const uint64_t bd = bd0 + (uint64_t)((((t0 - 1) * Cfg::B_BYTES) + ks * 256) >> 4);
+                  const uint32_t idesc = make_idesc(BM, BN) + ((uint32_t)((cnt - 1) * BN) >> 3 << 17);
+                  mma_i8_warp(dt + (s + t0 - 2) * BN, ad, bd, idesc);
+                }
+              }
+            }
+          }
+          mma_commit_warp(&empty[st]);
+          if (lane == 0 && it_n < 16) OZ_TRACE(64 + it_n);
+          ++it_n;
+        }
+      }
+      mma_commit_warp(&acc_full[buf]);
+      if (lane == 0 && j < 8) OZ_TRACE(11 + j);
+      if (lane == 0 && j == 0 && a.trace && blockIdx.x == 0) a.trace[63] = it_n;  // chunks of tile 0
+    }
+  } else if (warp >= 2) {
+    // ---- epilogue (8 warps; warp pairs share a TMEM lane quadrant) ----
+    constexpr int HC = BN / 2;
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const int part = lane & 1;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + half * HC;
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
+      int64_t bid = t;
+      const int tn = (int)(bid % a.ntiles);
+      bid /= a.ntiles;
+      const int tm = (int)(bid % a.mtiles);
+      bid /= a.mtiles;
+      const int64_t b = bid % a.batch;
+      const OzItem& it = a.items[(int)(bid / a.batch)];
+      const int buf = j & 1;
+      // exponents do not depend on the MMAs: fetch them before waiting
+      // (one column exponent per lane, shared through shuffles below)
+      const int64_t R = (int64_t)tm * BM + row;
+      const int64_t i = R >> 1;
+      const int ea = (i < a.M) ? __ldg(it.Ae + b * a.sAeb + i) : 0;
+      const int64_t ccol = (int64_t)tn * BN + lane;
+      const int eb_lane = (lane < BN && ccol < a.N) ? __ldg(it.Be + b * a.sBeb + ccol) : 0;
+      mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1, 256);
+      tc_fence_after();
+      if (j < 8 && threadIdx.x == 64) OZ_TRACE(19 + j);
+      const uint32_t base = lane_base + buf * Cfg::ACC_COLS;
+      long long hi[HC], lo[HC];
+#pragma unroll
+      for (int k = 0; k < HC; ++k) hi[k] = lo[k] = 0;
+#pragma unroll
+      for (int level = 0; level < S; level += 2) {
+        uint32_t r0[HC], r1[HC];
+        LD32x32b_X16(r0, base + level * BN);
+        if (level + 1 < S) LD32x32b_X16(r1, base + (level + 1) * BN);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < HC; ++k) {
+          const long long d0 = (long long)(int)r0[k];
+          if (level < 4) hi[k] = hi[k] * 128 + d0; else lo[k] = lo[k] * 128 + d0;
+          if (level + 1 < S) {
+            const long long d1 = (long long)(int)r1[k];
+            if (level + 1 < 4) hi[k] = hi[k] * 128 + d1; else lo[k] = lo[k] * 128 + d1;
+          }
+        }
+      }
+      if (j < 2 && threadIdx.x == 64) OZ_TRACE(36 + 3 * j);
+      {  // re-zero the buffer for the tile after next, then hand it back to the issuer
+        uint32_t zr[HC];
+#pragma unroll
+        for (int k = 0; k < HC; ++k) zr[k] = 0u;
+#pragma unroll
+        for (int level = 0; level < S; ++level) ST32x32b_X16(base + level * BN, zr);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      }
+      if (j < 2 && threadIdx.x == 64) OZ_TRACE(37 + 3 * j);
+      constexpr int HL = S < 4 ? S : 4;
+      const double whi = pow2(-7 * (HL + 1)), wlo = pow2(-7 * (S + 1));
+      // value = ((hi 2^-35 + lo 2^-7(S+1)) 2^ea) 2^eb: one rounding in the fma,
+      // then exact power-of-two scalings (row scale first); NONFINITE
+      // exponents give NaN
+      const int64_t cbase = (int64_t)tn * BN + half * HC;
+      static_assert(BN <= 32, "one column exponent per lane");
+      const double rs = pow2(ea);
+      double v[HC];
+#pragma unroll
+      for (int k = 0; k < HC; ++k) {
+        const int eb = __shfl_sync(0xffffffffu, eb_lane, half * HC + k);
+        const double x = fma((double)hi[k], whi, (double)lo[k] * wlo);
+        const double y = (x * rs) * pow2(eb);
+        v[k] = (ea == NONFINITE || eb == NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll) : y;
+      }
+      if (j < 2 && threadIdx.x == 64) OZ_TRACE(38 + 3 * j);
+      double2 out[HC / 2];
+#pragma unroll
+      for (int c = 0; c < HC / 2; ++c) {
+        const double send = part ? v[c] : v[c + HC / 2];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        out[c] = part ? make_double2(recv, v[c + HC / 2]) : make_double2(v[c], recv);
+      }
+      double2* C = it.C + b * a.sCb;
+      const int64_t col0 = cbase + part * (HC / 2);
+      if (i < a.M) {
+        if (!a.trans_c) {
+#pragma unroll
+          for (int c = 0; c < HC / 2; ++c)
+            if (col0 + c < a.N) C[i * a.ldc + col0 + c] = out[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < HC / 2; ++c)
+            if (col0 + c < a.N) C[(col0 + c) * a.ldc + i] = out[c];
+        }
+      }
+      if (j < 8 && threadIdx.x == 64) OZ_TRACE(27 + j);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) OZ_TRACE(42);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace oz
 }  // namespace cgl
 
@@ -768,6 +1107,26 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
   return check_launch("ozgemm_kernel");
 }
 
+template <int S, int BN, int STAGES>
+static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
+  using Cfg = oz::OzPCfg<S, BN, STAGES>;
+  auto kern = oz::ozgemm_persistent_kernel<S, BN, STAGES>;
+  static int nsm = 0;
+  if (!nsm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(ozgemm_persistent)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int64_t tiles = (int64_t)a.mtiles * a.ntiles * a.batch * nitems;
+  if (tiles <= 0) return 0;
+  const int64_t grid = tiles < nsm ? tiles : nsm;
+  kern<<<(unsigned)grid, oz::OZP_THREADS, Cfg::SMEM, st>>>(a, tiles);
+  return check_launch("ozgemm_persistent_kernel");
+}
+
 int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
             const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
             const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
@@ -791,11 +1150,15 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   a.flag = flag;
   a.pos = pos;
   {
+    const char* dbg = getenv("CGL_OZ_DEBUG");
+    a.debug = dbg ? atoi(dbg) : 0;
+  }
+  {
     static long long* trace = nullptr;
     const char* e = getenv("CGL_OZ_TRACE");
     if (e && e[0] == '1') {
-      if (!trace) cudaMalloc(&trace, 64 * sizeof(long long));
-      cudaMemsetAsync(trace, 0, 64 * sizeof(long long), st);
+      if (!trace) cudaMalloc(&trace, 128 * sizeof(long long));
+      cudaMemsetAsync(trace, 0, 128 * sizeof(long long), st);
       a.trace = trace;
       g_oz_trace = trace;
     }
@@ -803,6 +1166,11 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   for (int f = 0; f < nitems; ++f)
     a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
                             Bz ? Bz[f] : nullptr};
+  static const int persistent = [] {
+    const char* e = getenv("CGL_OZ_PERSISTENT");
+    return e ? atoi(e) : 1;
+  }();
+  if (persistent && S == 8) return oz_launch_persistent<8, BN, 4>(a, nitems, st);
   switch (S) {
     case 7: return oz_launch_cfg<7, BN, 2>(a, nitems, st);
     case 8: return oz_launch_cfg<8, BN, 2>(a, nitems, st);

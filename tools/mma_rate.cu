@@ -1,0 +1,162 @@
+// tcgen05.mma kind::i8 issue/execute rate from one thread per CTA (1 CTA/SM):
+// per "chunk" the GEMM's MMA pattern (8 MMAs, N = 256, 224, ..., 32, K = 32 B)
+// or a dense pattern (N = 256 only), operands resident in smem.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t make_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  const uint32_t a = smem_u32(smem);
+  uint64_t d = 0;
+  d |= (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+               "l"(adesc), "l"(bdesc), "r"(idesc));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+               "@P1 bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}\n" ::"r"(smem_u32(bar)), "r"(parity));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int MODE, int TMA = 0, int RND = 0>  // RND: random operand bytes; TMA: concurrent 40 KB/chunk bulk copies from 4 warps; 0: GEMM pattern (8 MMAs N=256..32); 1: 4.5 x N=256; 2: 36 x N=32; 3: pattern, A_BYTES slice stride 0
+__global__ void kern(int chunks, long long* out, const uint8_t* src) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536 + 4 * 40960);
+  uint64_t* tbar = bar + 8;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&tbar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    reinterpret_cast<uint32_t*>(smem)[i] = RND == 0 ? 0x01010101u : RND == 1 ? h : (h & 0x3f3f3f3fu);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *slot;
+  long long t0 = clock64();
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (TMA && warp >= 1 && warp <= 4 && (threadIdx.x & 31) == 0) {
+    // keep streaming 40 KB per stage until the MMA thread is done
+    const int w = warp - 1;
+    uint8_t* dst = smem + 65536 + w * 40960;
+    for (int i = 0; !stop; ++i) {
+      if (i) mbar_wait(&tbar[w], (i - 1) & 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&tbar[w])), "r"(40960));
+      const uint8_t* g = src + (((size_t)(blockIdx.x * 4 + w) * 131 + i * 7) % 512) * 40960;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       smem_u32(dst)), "l"(g), "r"(32768), "r"(smem_u32(&tbar[w])) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       smem_u32(dst + 32768)), "l"(g + 32768), "r"(8192), "r"(smem_u32(&tbar[w])) : "memory");
+    }
+    mbar_wait(&tbar[w], 0);  // drain is approximate; parity not tracked after stop
+  }
+  if (threadIdx.x == 0) {
+    constexpr uint32_t LBO = 128, SBO = 256;
+    const uint8_t* sa = smem;
+    const uint8_t* sb = smem + 32768;
+    const uint64_t ad0 = make_desc(sa, LBO, SBO), bd0 = make_desc(sb, LBO, SBO);
+    for (int c = 0; c < chunks; ++c) {
+      if (MODE == 0 || MODE == 3) {
+#pragma unroll
+        for (int s = 1; s <= 8; ++s) {
+          const uint64_t ad = ad0 + (MODE == 3 ? 0 : (uint64_t)(((s - 1) * 4096) >> 4));
+          const int cnt = 9 - s;
+          const uint32_t idesc = make_idesc(128, 32) + ((uint32_t)((cnt - 1) * 32) >> 3 << 17);
+          mma_i8(tmem + (s - 1) * 32, ad, bd0, idesc);
+        }
+      } else if (MODE == 1) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) mma_i8(tmem + (s & 1) * 256, ad0 + (s * 4096 >> 4), bd0, make_idesc(128, 256));
+        if (c & 1) mma_i8(tmem, ad0, bd0, make_idesc(128, 256));
+      } else {
+#pragma unroll
+        for (int s = 0; s < 36; ++s) mma_i8(tmem + (s % 8) * 32, ad0 + ((s % 8) * 4096 >> 4), bd0, make_idesc(128, 32));
+      }
+      mma_commit(&bar[c & 3]);
+      if (c >= 3) mbar_wait(&bar[(c - 3) & 3], ((c - 3) >> 2) & 1);
+    }
+    for (int c = chunks; c < chunks + 3; ++c) mbar_wait(&bar[(c - 3) & 3], ((c - 3) >> 2) & 1);
+    stop = 1;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = t1 - t0;
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+template <int MODE, int TMA = 0, int RND = 0>
+void run(const char* name, int nsm, long long* d_out, const uint8_t* src) {
+  const int smem = 65536 + 4 * 40960 + 256;
+  cudaFuncSetAttribute(kern<MODE, TMA, RND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int chunks = 4000;
+  kern<MODE, TMA, RND><<<nsm, 160, smem>>>(100, d_out, src);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kern<MODE, TMA, RND><<<nsm, 160, smem>>>(chunks, d_out, src);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long cyc;
+  cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
+  const double macs = 4718592.0 * chunks * nsm;  // 36 x (128 x 32 x 32) per chunk
+  printf("%-40s %.3f us/chunk  %.0f clk/chunk  %.1f%% of 8192 MAC/clk  (%s)\n", name, ms * 1e3 / chunks,
+         (double)cyc / chunks, 100.0 * 4718592.0 / 8192.0 / ((double)cyc / chunks),
+         cudaGetErrorString(cudaGetLastError()));
+  (void)macs;
+}
+
+int main() {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  long long* d_out;
+  cudaMalloc(&d_out, 64);
+  uint8_t* src;
+  cudaMalloc(&src, 512 * 40960 + 65536);
+  cudaMemset(src, 1, 512 * 40960 + 65536);
+  run<0>("pattern 8 MMAs N=256..32", nsm, d_out, src);
+  run<1>("4.5 x N=256 (same MACs)", nsm, d_out, src);
+  run<0, 1>("pattern + concurrent TMA 4x40KB ring", nsm, d_out, src);
+  run<1, 1>("4.5 x N=256 + concurrent TMA", nsm, d_out, src);
+  run<0, 0, 1>("pattern, random bytes", nsm, d_out, src);
+  run<1, 0, 1>("4.5 x N=256, random bytes", nsm, d_out, src);
+  run<0, 0, 2>("pattern, random 6-bit magnitudes", nsm, d_out, src);
+  return 0;
+}
