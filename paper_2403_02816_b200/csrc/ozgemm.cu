@@ -38,6 +38,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <climits>
+#include <cooperative_groups.h>
+
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
 
@@ -340,18 +343,23 @@ __device__ __forceinline__ void digits8_floor(double x, int e, uint32_t (&w)[8][
   for (int s = 0; s < 8; ++s) w[s][word] |= (d[s] & 0xFFu) << sh;
 }
 
-template <int S, int AMODE>
+// FUSED (data operand, B mode): the CTAs of one row tile form a thread-block
+// cluster spanning the whole K range; each reduces its staged block to
+// partial row exponents, the cluster combines them through distributed
+// shared memory, and every CTA slices its block with the row exponents --
+// one launch, the data read from HBM once (replaces rowexp_* + this kernel).
+template <int S, int AMODE, int CPBT = CPB, bool FUSED = false>
 __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
                                                          int64_t exp_bs) {
   constexpr int CC = KC / 2;              // complex columns per chunk
-  constexpr int W = CC * CPB;             // complex columns per CTA
+  constexpr int W = CC * CPBT;            // complex columns per CTA
   constexpr int RT = AMODE ? BM : kOzBN;  // real rows per tile
   constexpr int CR = AMODE ? RT / 2 : RT; // complex rows per tile
   extern __shared__ double2 blk_dyn[];    // [CR][W + 1]
   const int64_t batch = gridDim.z / a.cols_items;
   const int64_t b = blockIdx.z % batch;
   const int item = (int)(blockIdx.z / batch);
-  const int rt = blockIdx.x, ch0 = blockIdx.y * CPB;
+  const int rt = blockIdx.x, ch0 = blockIdx.y * CPBT;
   const int64_t r0 = (int64_t)rt * CR, c0 = (int64_t)ch0 * CC;
   const double2* z = a.srcs[item] + b * src_bs;
   const int tid = threadIdx.x;
@@ -375,9 +383,52 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   __syncthreads();
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item] + b * exp_bs + r0;
+  __shared__ int erow[FUSED ? CR : 1];
+  if constexpr (FUSED) {
+    static_assert(!AMODE && CR == 32, "fused exponents: data operand, 32-row tiles");
+    __shared__ double red[8][33];
+    __shared__ int redbad[8][32];
+    __shared__ int epart[32];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    {
+      const int rr = tid & 31, part = tid >> 5;
+      double m = 0.0;
+      bool bad = false;
+      for (int cc = part; cc < cols_here; cc += 8) {
+        const double2 v = blk_dyn[rr * (W + 1) + cc];
+        bad |= !isfinite(v.x) || !isfinite(v.y);
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+      }
+      red[part][rr] = m;
+      redbad[part][rr] = bad;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      double m = red[0][tid];
+      int bad = redbad[0][tid];
+      for (int k = 1; k < 8; ++k) {
+        m = fmax(m, red[k][tid]);
+        bad |= redbad[k][tid];
+      }
+      int e = INT_MIN;
+      if (bad) e = NONFINITE;
+      else if (m > 0.0) frexp(m, &e);
+      epart[tid] = e;
+    }
+    cluster.sync();
+    if (tid < 32) {
+      int e = INT_MIN;
+      for (unsigned rk = 0; rk < cluster.num_blocks(); ++rk) e = max(e, cluster.map_shared_rank(epart, rk)[tid]);
+      if (e == INT_MIN) e = 0;  // all-zero row (same convention as rowexp_kernel)
+      erow[tid] = e;
+      if (blockIdx.y == 0 && tid < rows_here) a.expss[item][b * exp_bs + r0 + tid] = e;
+    }
+    cluster.sync();  // partials read before any CTA of the cluster moves on; erow visible
+  }
   constexpr int nreal = AMODE ? 2 : 1;
   constexpr int NG = KC / 16;               // 16-byte groups per chunk
-  constexpr int groups = CPB * NG;
+  constexpr int groups = CPBT * NG;
   // consecutive threads take consecutive REAL rows of one 16-byte group, so the
   // slice stores of a warp fill whole 128-byte lines of the core-matrix layout
   constexpr int nrr = CR * nreal;
@@ -389,7 +440,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
     const int rr = AMODE ? rr_real >> 1 : rr_real, part = AMODE ? rr_real & 1 : 0;
     const int ch = ch0 + gg / NG, g = gg % NG;
     if (rr >= rows_here || ch >= a.nchunks) continue;  // padding stays zero (buffer zeroed once)
-    const int e_raw = exps[rr];
+    const int e_raw = FUSED ? erow[rr] : exps[rr];
     const bool nonfinite = e_raw == NONFINITE;
     uint32_t wv[8][4];
 #pragma unroll
@@ -1039,6 +1090,38 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   a.floor_digits = floor_digits;
   const int64_t zdim = batch * nitems;
   if (zdim > 65535) return set_error(CGL_ESHAPE, "oz_slice: batch x items too large");
+  static const bool fuse_ok = [] {
+    const char* e = getenv("CGL_OZ_FUSED_SLICE");
+    return !(e && e[0] == '0');
+  }();
+  if (fuse_ok && !a_mode && floor_digits && S == 8 && a.nchunks <= 64) {
+    // one cluster of <= 8 CTAs per row tile covers all K chunks
+    const int cpb = a.nchunks <= 32 ? 4 : 8;
+    const int cy = (a.nchunks + cpb - 1) / cpb;
+    const size_t smem = (size_t)kOzBN * (cpb * oz::KC / 2 + 1) * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(oz::slice_tile_kernel<8, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(oz::slice_tile_kernel<8, 0, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)a.rtiles, (unsigned)cy, (unsigned)zdim);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = (unsigned)cy;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cpb == 4 ? cudaLaunchKernelEx(&cfg, oz::slice_tile_kernel<8, 0, 4, true>, a, src_bs, out_bs, exp_bs)
+                             : cudaLaunchKernelEx(&cfg, oz::slice_tile_kernel<8, 0, 8, true>, a, src_bs, out_bs, exp_bs);
+    if (e != cudaSuccess) return set_cuda_error(e, "oz_slice (fused cluster launch)");
+    return check_launch("oz_slice_fused");
+  }
   // pass 1: exponents
   if (sr == 1) {
     for (int f = 0; f < nitems; ++f) {
