@@ -204,8 +204,8 @@ def _time(torch, fn, reps=20):
 
 
 def gemm_roofline(torch, w, scheme_fields=4):
-    """Dominant kernel of the if4 step: the 4-field mode-1 (left-form) product
-    on the INT8 tensor cores (ozgemm_kernel), timed per launch with CUDA
+    """Dominant kernel of the if4 step: the 4-field axis-0 (left-form) product
+    on the INT8 tensor cores (ozgemm_persistent_kernel), timed per launch with CUDA
     events on the workload shapes, data pre-sliced as in the step.  Reported
     against the INT8 dense tensor peak on EXECUTED int8 MACs (block skipping
     counted out), plus the FP64-equivalent view against the measured DMMA
@@ -223,8 +223,8 @@ def gemm_roofline(torch, w, scheme_fields=4):
     ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws)  # slices the data into ws
     Q = w.points // n
     per = lib.cgl_oz_slice_bytes(ozaki.S, Q, n, 0)
-    Bs = [ws.bufs[("B", f)][0] for f in range(scheme_fields)]
-    Be = [ws.bufs[("B", f)][1] for f in range(scheme_fields)]
+    Bs = [ws.bufs[("D", f, n)][0] for f in range(scheme_fields)]
+    Be = [ws.bufs[("D", f, n)][1] for f in range(scheme_fields)]
 
     def gemm_only():
         _lib.check(lib.cgl_oz_gemm(_lib.stream(), ozaki.S, n, Q, n, scheme_fields,
@@ -259,8 +259,9 @@ def gemm_roofline(torch, w, scheme_fields=4):
             # upper bound -- in the step the operands are L2-resident)
             "traffic": 23.2e6, "traffic_unit": "bytes per launch",
             "traffic_source": "profiles/r01_ozgemm_ncu_summary.txt (cold-cache ncu capture)",
-            "kernel": "ozgemm_kernel<8,32,2> (tcgen05.mma kind::i8, TMEM accumulators): 4-field mode-1 product of "
-                      "the if4 step, M=N=K=512 complex per field, S=8 int8 slices",
+            "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
+                      "accumulators): 4-field axis-0 product of the if4 step, M=N=K=512 complex per field, "
+                      "S=8 int8 slices",
             "per_launch_ms": dt * 1e3, "per_launch_ms_incl_data_slicing": dt_with_slicing * 1e3,
             "executed_int8_macs_per_launch": macs, "dense_int8_macs_per_launch": dense,
             "block_skip_fraction": 1.0 - macs / dense,

@@ -135,6 +135,33 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// lane predicate of one elected lane (all lanes call; compute once per loop)
+__device__ __forceinline__ uint32_t elect_lane() {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}\n"
+      : "=r"(r));
+  return r;
+}
+// all lanes execute with identical operands; the lane with leader != 0 issues
+__device__ __forceinline__ void mma_i8_lead(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(leader));
+}
+__device__ __forceinline__ void mma_commit_lead(uint64_t* bar, uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %1, 0;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(bar)), "r"(leader)
+      : "memory");
+}
 // warp-uniform issue: every lane executes the call with identical operands and
 // one elected lane issues (keeps descriptors warp-uniform, no per-MMA
 // R2UR/ELECT loop around the instruction)
@@ -774,10 +801,30 @@ struct OzPCfg {
   static constexpr int B_BYTES = BN * KC;
   static constexpr int STAGE_BYTES = S * (A_BYTES + B_BYTES);
   static constexpr int BODY = STAGES * STAGE_BYTES;
-  static constexpr int SMEM = BODY + 256;
+  static constexpr int NTI = 4;          // tile-info ring slots
+  static constexpr int KMAXCH = 256;     // max K chunks per tile (K <= 8192 bytes)
+  static constexpr int TINFO = BODY + 256;
+  static constexpr int SMEM = TINFO + NTI * (KMAXCH + 1) * 4;
   static constexpr uint32_t ACC_COLS = S * BN;
   static_assert(2 * S * BN <= 512, "two level buffers must fit the 512 TMEM columns");
 };
+
+// tile t -> (tn fastest, tm, batch b, item); 32-bit (host checks total < 2^31)
+struct TileId {
+  int tn, tm, b, item;
+};
+__device__ __forceinline__ TileId decode_tile(const OzArgs& a, uint32_t t) {
+  TileId d;
+  const uint32_t nt = (uint32_t)a.ntiles, mt = (uint32_t)a.mtiles, nb = (uint32_t)a.batch;
+  uint32_t q = t / nt;
+  d.tn = (int)(t - q * nt);
+  const uint32_t q2 = q / mt;
+  d.tm = (int)(q - q2 * mt);
+  const uint32_t q3 = q2 / nb;
+  d.b = (int)(q2 - q3 * nb);
+  d.item = (int)q3;
+  return d;
+}
 
 template <int S, int BN, int STAGES>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const OzArgs a, int64_t total) {
@@ -789,10 +836,18 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2] MMAs of the buffer's tile done
   uint64_t* acc_empty = acc_full + 2;   // [2] epilogue has read (and re-zeroed) the buffer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* ti_full = acc_empty + 2;    // [NTI] live-chunk list of a tile written (producer warp 0)
+  uint64_t* ti_empty = ti_full + Cfg::NTI;  // [NTI] list consumed (issuer + producer warps 10-12)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ti_empty + Cfg::NTI);
+  // tile-info ring: [slot][0] = live chunk count, [slot][1 + e] = c | za << 16 | zb << 24
+  uint32_t* tinfo = reinterpret_cast<uint32_t*>(smem + Cfg::TINFO);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) OZ_TRACE(0);
+  // item table in shared memory: a dynamically indexed kernel-parameter load
+  // misses the constant cache, and the dependent global loads would stall on it
+  __shared__ OzItem sitems[kMaxItems];
+  if (threadIdx.x < kMaxItems) sitems[threadIdx.x] = a.items[threadIdx.x];
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -801,6 +856,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 8);
+    }
+    for (int s = 0; s < Cfg::NTI; ++s) {
+      mbar_init(&ti_full[s], 1);
+      mbar_init(&ti_empty[s], OZP_PRODUCERS);  // issuer + the 3 other producer warps
     }
     fence_barrier_init();
   }
@@ -827,100 +886,118 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   const int nch = a.nchunks;
   const int64_t step = gridDim.x;
   if (warp == 0 || warp >= 10) {
-    // ---- producers: one ring across all tiles of this CTA.  Every producer
-    // warp reads the zero maps 32 chunks at a time (one load latency per 32
-    // chunks, ballot of the live ones); producer p issues the copies of the
-    // live chunks it_n with it_n % STAGES == p (its own stage). ----
+    // ---- producers: one ring across all tiles of this CTA.  Producer warp 0
+    // first lists the live chunks of each tile (zero maps read 32 chunks per
+    // load, ballot) into the tile-info ring; all producer warps and the
+    // issuer walk that list.  Producer p issues the copies of the live chunks
+    // it_n with it_n % STAGES == p (its own stage: bulk copies serialise per
+    // issuing warp). ----
     static_assert(STAGES == OZP_PRODUCERS, "one producer warp per stage");
     const int pw = warp == 0 ? 0 : warp - 9;
-    int it_n = 0;
-    for (int64_t t = blockIdx.x; t < total; t += step) {
-      int64_t bid = t;
-      const int tn = (int)(bid % a.ntiles);
-      bid /= a.ntiles;
-      const int tm = (int)(bid % a.mtiles);
-      bid /= a.mtiles;
-      const int64_t b = bid % a.batch;
-      const OzItem& it = a.items[(int)(bid / a.batch)];
+    const int64_t t_end = (a.debug & 4) ? 0 : total;  // debug 4: producers idle
+    int it_n = 0, j = 0;
+    for (int64_t t = blockIdx.x; t < t_end; t += step, ++j) {
+      const TileId td = decode_tile(a, (uint32_t)t);
+      const int tn = td.tn, tm = td.tm;
+      const int64_t b = td.b;
+      const OzItem& it = sitems[td.item];
+      const int slot = j % Cfg::NTI;
+      uint32_t* list = tinfo + slot * (Cfg::KMAXCH + 1);
+      if (pw == 0) {
+        mbar_wait(&ti_empty[slot], ((j / Cfg::NTI) & 1) ^ 1);
+        const int8_t* az = it.Az ? it.Az + (int64_t)tm * nch : nullptr;
+        const int8_t* bz = it.Bz ? it.Bz + (int64_t)tn * nch : nullptr;
+        int n = 0;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+          int zal = S + 1, zbl = S + 1;
+          if (c0 + lane < nch) {
+            zal = az ? az[c0 + lane] : 1;
+            zbl = bz ? bz[c0 + lane] : 1;
+          }
+          const bool live_me = zal + zbl <= S + 1;
+          const unsigned live = __ballot_sync(0xffffffffu, live_me);
+          if (live_me)
+            list[1 + n + __popc(live & ((1u << lane) - 1u))] =
+                (uint32_t)(c0 + lane) | ((uint32_t)zal << 16) | ((uint32_t)zbl << 24);
+          n += __popc(live);
+        }
+        if (lane == 0) list[0] = (uint32_t)n;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ti_full[slot]);
+      } else {
+        mbar_wait(&ti_full[slot], (j / Cfg::NTI) & 1);
+      }
       const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * S * Cfg::A_BYTES;
       const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * S * Cfg::B_BYTES;
-      const int8_t* az = it.Az ? it.Az + (int64_t)tm * nch : nullptr;
-      const int8_t* bz = it.Bz ? it.Bz + (int64_t)tn * nch : nullptr;
-      for (int c0 = 0; c0 < nch; c0 += 32) {
-        int zal = S + 1, zbl = S + 1;
-        if (c0 + lane < nch) {
-          zal = az ? az[c0 + lane] : 1;
-          zbl = bz ? bz[c0 + lane] : 1;
-        }
-        unsigned live = __ballot_sync(0xffffffffu, zal + zbl <= S + 1);
-        while (live) {
-          const int l = __ffs(live) - 1;
-          live &= live - 1;
-          const int za = __shfl_sync(0xffffffffu, zal, l), zb = __shfl_sync(0xffffffffu, zbl, l);
-          if (lane == 0 && it_n % STAGES == pw) {
-            const int c = c0 + l;
-            const int st = it_n % STAGES;
-            const uint32_t ph = (it_n / STAGES) & 1;
-            mbar_wait_sleep(&empty[st], ph ^ 1, 64);
-            if (it_n < 8) OZ_TRACE(44 + it_n);
-            if (it_n >= 8 && it_n < 16) OZ_TRACE(96 + it_n);
-            const int na = S + 2 - zb - za;
-            if (a.debug & 2) {
-              mbar_arrive(&full[st]);
-            } else {
-              mbar_expect_tx(&full[st], na * (Cfg::A_BYTES + Cfg::B_BYTES));
-              uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
-              uint8_t* sb = sa + S * Cfg::A_BYTES;
-              bulk_g2s(sa + (za - 1) * Cfg::A_BYTES, A + ((int64_t)c * S + (za - 1)) * Cfg::A_BYTES,
-                       na * Cfg::A_BYTES, &full[st]);
-              bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
-                       na * Cfg::B_BYTES, &full[st]);
-            }
+      const int n = (int)list[0];
+      // this warp's chunks are every STAGES-th live chunk of the CTA's sequence
+      int e = ((pw - it_n) % STAGES + STAGES) % STAGES;
+      for (; e < n; e += STAGES) {
+        const uint32_t ent = list[1 + e];
+        const int c = (int)(ent & 0xFFFFu), za = (int)((ent >> 16) & 0xFF), zb = (int)(ent >> 24);
+        const int itc = it_n + e;
+        const int st = itc % STAGES;
+        const uint32_t ph = (itc / STAGES) & 1;
+        if (lane == 0) {
+          mbar_wait_sleep(&empty[st], ph ^ 1, 64);
+          if (itc < 8) OZ_TRACE(44 + itc);
+          const int na = S + 2 - zb - za;
+          if (a.debug & 2) {
+            mbar_arrive(&full[st]);
+          } else {
+            mbar_expect_tx(&full[st], na * (Cfg::A_BYTES + Cfg::B_BYTES));
+            uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+            uint8_t* sb = sa + S * Cfg::A_BYTES;
+            bulk_g2s(sa + (za - 1) * Cfg::A_BYTES, A + ((int64_t)c * S + (za - 1)) * Cfg::A_BYTES,
+                     na * Cfg::A_BYTES, &full[st]);
+            bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
+                     na * Cfg::B_BYTES, &full[st]);
           }
-          ++it_n;
-          __syncwarp();
         }
+        __syncwarp();
       }
+      it_n += n;
+      __syncwarp();
+      if (pw != 0 && lane == 0) mbar_arrive(&ti_empty[slot]);
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: the whole warp runs the (warp-uniform) loop, one
-    // elected lane issues each tcgen05 instruction ----
+    // ---- MMA issuer: the whole warp runs the (warp-uniform) loop over the
+    // tile's live-chunk list; one lane, elected once, issues every tcgen05
+    // instruction ----
     constexpr uint32_t LBO = 128, SBO = (KC / 16) * 128;
     constexpr int PER = 256 / BN;
+    const uint32_t leader = elect_lane();
     int it_n = 0, j = 0;
     for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
-      int64_t bid = t;
-      const int tn = (int)(bid % a.ntiles);
-      bid /= a.ntiles;
-      const int tm = (int)(bid % a.mtiles);
-      bid /= a.mtiles;
-      const OzItem& it = a.items[(int)(bid / a.batch)];
-      const int8_t* az = it.Az ? it.Az + (int64_t)tm * nch : nullptr;
-      const int8_t* bz = it.Bz ? it.Bz + (int64_t)tn * nch : nullptr;
       const int buf = j & 1;
+      const int slot = j % Cfg::NTI;
+      const uint32_t* list = tinfo + slot * (Cfg::KMAXCH + 1);
+      if (!(a.debug & 4)) mbar_wait(&ti_full[slot], (j / Cfg::NTI) & 1);
+      const int n = (a.debug & 4) ? 0 : (int)list[0];
       mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0 && j < 8) OZ_TRACE(3 + j);
       const uint32_t dt = tmem + buf * Cfg::ACC_COLS;
-      for (int c0 = 0; c0 < nch; c0 += 32) {
-        int zal = S + 1, zbl = S + 1;
-        if (c0 + lane < nch) {
-          zal = az ? az[c0 + lane] : 1;
-          zbl = bz ? bz[c0 + lane] : 1;
-        }
-        unsigned live = __ballot_sync(0xffffffffu, zal + zbl <= S + 1);
-        while (live) {
-          const int l = __ffs(live) - 1;
-          live &= live - 1;
-          const int za = __shfl_sync(0xffffffffu, zal, l), zb = __shfl_sync(0xffffffffu, zbl, l);
-          const int st = it_n % STAGES;
-          const uint32_t ph = (it_n / STAGES) & 1;
-          mbar_wait(&full[st], ph);  // TMA writes -> MMA reads: ordered by complete_tx
-          if (lane == 0 && it_n < 8) OZ_TRACE(52 + it_n);
-          if (lane == 0 && it_n >= 8 && it_n < 16) OZ_TRACE(80 + it_n);
-          if (!(a.debug & 1)) {
-            const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
-            const uint64_t ad0 = make_desc(sa, LBO, SBO), bd0 = make_desc(sa + S * Cfg::A_BYTES, LBO, SBO);
+      for (int e = 0; e < n; ++e) {
+        const uint32_t ent = list[1 + e];
+        const int za = (int)((ent >> 16) & 0xFF), zb = (int)(ent >> 24);
+        const int st = it_n % STAGES;
+        const uint32_t ph = (it_n / STAGES) & 1;
+        mbar_wait(&full[st], ph);  // TMA writes -> MMA reads: ordered by complete_tx
+        if (lane == 0 && it_n < 8) OZ_TRACE(52 + it_n);
+        if (!(a.debug & 1)) {
+          const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+          const uint64_t ad0 = make_desc(sa, LBO, SBO), bd0 = make_desc(sa + S * Cfg::A_BYTES, LBO, SBO);
+          if (zb == 1 && KC == 32 && PER >= S) {
+            // dense data operand: for A slice s one MMA covers B slices 1..S+1-s
+            // (N = (S+1-s) BN) into levels s-1 .. S-1; offsets are compile-time
+#pragma unroll
+            for (int s = 1; s <= S; ++s) {
+              if (s < za) continue;
+              mma_i8_lead(dt + (s - 1) * BN, ad0 + (uint64_t)(((s - 1) * Cfg::A_BYTES) >> 4), bd0,
+                          make_idesc(BM, (S + 1 - s) * BN), leader);
+            }
+          } else {
 #pragma unroll
             for (int ks = 0; ks < KC / 32; ++ks) {
 #pragma unroll
@@ -934,17 +1011,19 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
                   const int cnt = (S + 2 - s - t0) < PER ? (S + 2 - s - t0) : PER;
                   const uint64_t bd = bd0 + (uint64_t)((((t0 - 1) * Cfg::B_BYTES) + ks * 256) >> 4);
                   const uint32_t idesc = make_idesc(BM, BN) + ((uint32_t)((cnt - 1) * BN) >> 3 << 17);
-                  mma_i8_warp(dt + (s + t0 - 2) * BN, ad, bd, idesc);
+                  mma_i8_lead(dt + (s + t0 - 2) * BN, ad, bd, idesc, leader);
                 }
               }
             }
           }
-          mma_commit_warp(&empty[st]);
-          if (lane == 0 && it_n < 16) OZ_TRACE(64 + it_n);
-          ++it_n;
         }
+        mma_commit_lead(&empty[st], leader);
+        if (lane == 0 && it_n < 16) OZ_TRACE(64 + it_n);
+        ++it_n;
       }
-      mma_commit_warp(&acc_full[buf]);
+      mma_commit_lead(&acc_full[buf], leader);
+      __syncwarp();
+      if (lane == 0 && !(a.debug & 4)) mbar_arrive(&ti_empty[slot]);
       if (lane == 0 && j < 8) OZ_TRACE(11 + j);
       if (lane == 0 && j == 0 && a.trace && blockIdx.x == 0) a.trace[63] = it_n;  // chunks of tile 0
     }
@@ -957,13 +1036,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + half * HC;
     int j = 0;
     for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
-      int64_t bid = t;
-      const int tn = (int)(bid % a.ntiles);
-      bid /= a.ntiles;
-      const int tm = (int)(bid % a.mtiles);
-      bid /= a.mtiles;
-      const int64_t b = bid % a.batch;
-      const OzItem& it = a.items[(int)(bid / a.batch)];
+      const TileId td = decode_tile(a, (uint32_t)t);
+      const int tn = td.tn, tm = td.tm;
+      const int64_t b = td.b;
+      const OzItem& it = sitems[td.item];
       const int buf = j & 1;
       // exponents do not depend on the MMAs: fetch them before waiting
       // (one column exponent per lane, shared through shuffles below)
@@ -972,7 +1048,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       const int ea = (i < a.M) ? __ldg(it.Ae + b * a.sAeb + i) : 0;
       const int64_t ccol = (int64_t)tn * BN + lane;
       const int eb_lane = (lane < BN && ccol < a.N) ? __ldg(it.Be + b * a.sBeb + ccol) : 0;
-      mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1, 256);
+      mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1, 32);
       tc_fence_after();
       if (j < 8 && threadIdx.x == 64) OZ_TRACE(19 + j);
       const uint32_t base = lane_base + buf * Cfg::ACC_COLS;
@@ -1205,6 +1281,7 @@ static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
   }
   const int64_t tiles = (int64_t)a.mtiles * a.ntiles * a.batch * nitems;
   if (tiles <= 0) return 0;
+  if (tiles >= (1ll << 31)) return set_error(CGL_ESHAPE, "oz_gemm: more than 2^31 tiles in one launch");
   const int64_t grid = tiles < nsm ? tiles : nsm;
   kern<<<(unsigned)grid, oz::OZP_THREADS, Cfg::SMEM, st>>>(a, tiles);
   return check_launch("ozgemm_persistent_kernel");
@@ -1253,7 +1330,8 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
     const char* e = getenv("CGL_OZ_PERSISTENT");
     return e ? atoi(e) : 1;
   }();
-  if (persistent && S == 8) return oz_launch_persistent<8, BN, 4>(a, nitems, st);
+  if (persistent && S == 8 && a.nchunks <= oz::OzPCfg<8, BN, 4>::KMAXCH)
+    return oz_launch_persistent<8, BN, 4>(a, nitems, st);
   switch (S) {
     case 7: return oz_launch_cfg<7, BN, 2>(a, nitems, st);
     case 8: return oz_launch_cfg<8, BN, 2>(a, nitems, st);

@@ -36,6 +36,9 @@ if persistent:
         names[52 + j] = f"  issuer: chunk {j} data ready"
     for j in range(16):
         names[64 + j] = f"  issuer: chunk {j} MMAs issued"
+    for j in range(8):
+        names[112 + j] = f"tile {j}: issuer loop top"
+        names[120 + j] = f"tile {j}: issuer zero-map prefetch issued"
     for j in range(8, 16):
         names[80 + j] = f"  issuer: chunk {j} data ready"
         names[96 + j] = f"  producer: chunk {j} copy issued"
