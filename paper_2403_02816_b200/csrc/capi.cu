@@ -1,3 +1,4 @@
+#include <cstdlib>
 // extern "C" boundary (include/cgl_b200.h): argument validation, layout
 // mapping of mu-mode products onto the batched GEMM, and error plumbing.
 #include <cstdio>
@@ -56,6 +57,14 @@ __global__ void dmma_probe_kernel(double* sink, int iters) {
   double r = 0;
   for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
   if (r == 1234.5) *sink = r;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CGL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int set_error(int code, const char* msg) {

@@ -33,6 +33,13 @@ __device__ __forceinline__ double2 cexp(double2 z) {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
+// Programmatic dependent launch (kernels launched through launch_k): wait
+// until the preceding kernel in the stream has completed and its writes are
+// visible (a no-op without the launch attribute); trigger lets the next
+// kernel's CTAs start their prologue while this grid finishes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // Sticky divergence record (see include/cgl_b200.h, cgl_flag_t).
 //

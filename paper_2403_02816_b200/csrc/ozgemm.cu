@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   const double2* z = a.srcs[item] + b * src_bs;
   const int tid = threadIdx.x;
   const int rows_here = (int)min((int64_t)CR, a.rows - r0), cols_here = (int)min((int64_t)W, a.cols - c0);
+  if constexpr (FUSED) pdl_wait();  // launched with launch_k: the data come from the previous kernel
   if (a.sc == 1) {
     const double2* zb = z + r0 * a.sr + c0;
 #pragma unroll 4
@@ -408,6 +409,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
     }
   }
   __syncthreads();
+  if constexpr (FUSED) pdl_trigger();  // inputs staged: the GEMM may start its prologue
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item] + b * exp_bs + r0;
   __shared__ int erow[FUSED ? CR : 1];
@@ -829,7 +831,6 @@ __device__ __forceinline__ TileId decode_tile(const OzArgs& a, uint32_t t) {
 template <int S, int BN, int STAGES>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const OzArgs a, int64_t total) {
   using Cfg = OzPCfg<S, BN, STAGES>;
-  if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* stage_base = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::BODY);
@@ -881,10 +882,14 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // prologue done (overlaps the previous kernel's tail under PDL); the data
+  // operand, its exponents and the divergence key come from earlier kernels
+  pdl_wait();
   if (threadIdx.x == 0) OZ_TRACE(1);
 
   const int nch = a.nchunks;
   const int64_t step = gridDim.x;
+  const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
   if (warp == 0 || warp >= 10) {
     // ---- producers: one ring across all tiles of this CTA.  Producer warp 0
     // first lists the live chunks of each tile (zero maps read 32 chunks per
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     // issuing warp). ----
     static_assert(STAGES == OZP_PRODUCERS, "one producer warp per stage");
     const int pw = warp == 0 ? 0 : warp - 9;
-    const int64_t t_end = (a.debug & 4) ? 0 : total;  // debug 4: producers idle
+    const int64_t t_end = (a.debug & 4) ? 0 : total_run;  // debug 4: producers idle
     int it_n = 0, j = 0;
     for (int64_t t = blockIdx.x; t < t_end; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
@@ -968,7 +973,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     constexpr int PER = 256 / BN;
     const uint32_t leader = elect_lane();
     int it_n = 0, j = 0;
-    for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
+    for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const int buf = j & 1;
       const int slot = j % Cfg::NTI;
       const uint32_t* list = tinfo + slot * (Cfg::KMAXCH + 1);
@@ -1027,6 +1032,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       if (lane == 0 && j < 8) OZ_TRACE(11 + j);
       if (lane == 0 && j == 0 && a.trace && blockIdx.x == 0) a.trace[63] = it_n;  // chunks of tile 0
     }
+    pdl_trigger();  // all MMAs issued: only this CTA's epilogue tail remains
   } else if (warp >= 2) {
     // ---- epilogue (8 warps; warp pairs share a TMEM lane quadrant) ----
     constexpr int HC = BN / 2;
@@ -1035,7 +1041,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     const int part = lane & 1;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + half * HC;
     int j = 0;
-    for (int64_t t = blockIdx.x; t < total; t += step, ++j) {
+    for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
       const int tn = td.tn, tm = td.tm;
       const int64_t b = td.b;
@@ -1124,6 +1130,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       if (j < 8 && threadIdx.x == 64) OZ_TRACE(27 + j);
     }
   }
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) OZ_TRACE(42);
@@ -1181,20 +1188,11 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
       cudaFuncSetAttribute(oz::slice_tile_kernel<8, 0, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       attr = true;
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)a.rtiles, (unsigned)cy, (unsigned)zdim);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = (unsigned)cy;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cpb == 4 ? cudaLaunchKernelEx(&cfg, oz::slice_tile_kernel<8, 0, 4, true>, a, src_bs, out_bs, exp_bs)
-                             : cudaLaunchKernelEx(&cfg, oz::slice_tile_kernel<8, 0, 8, true>, a, src_bs, out_bs, exp_bs);
+    const dim3 grid((unsigned)a.rtiles, (unsigned)cy, (unsigned)zdim), cl(1, (unsigned)cy, 1);
+    cudaError_t e = cpb == 4 ? launch_k(oz::slice_tile_kernel<8, 0, 4, true>, grid, dim3(256), smem, st, cl, a, src_bs,
+                                        out_bs, exp_bs)
+                             : launch_k(oz::slice_tile_kernel<8, 0, 8, true>, grid, dim3(256), smem, st, cl, a, src_bs,
+                                        out_bs, exp_bs);
     if (e != cudaSuccess) return set_cuda_error(e, "oz_slice (fused cluster launch)");
     return check_launch("oz_slice_fused");
   }
@@ -1283,7 +1281,8 @@ static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
   if (tiles <= 0) return 0;
   if (tiles >= (1ll << 31)) return set_error(CGL_ESHAPE, "oz_gemm: more than 2^31 tiles in one launch");
   const int64_t grid = tiles < nsm ? tiles : nsm;
-  kern<<<(unsigned)grid, oz::OZP_THREADS, Cfg::SMEM, st>>>(a, tiles);
+  cudaError_t e = launch_k(kern, dim3((unsigned)grid), dim3(oz::OZP_THREADS), Cfg::SMEM, st, dim3(1), a, tiles);
+  if (e != cudaSuccess) return set_cuda_error(e, "ozgemm_persistent launch");
   return check_launch("ozgemm_persistent_kernel");
 }
 

@@ -156,7 +156,11 @@ __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint
 }
 
 __global__ void flag_reset_kernel(cgl_flag_t* f) { f->key = ~0ull; }
-__global__ void flag_advance_kernel(cgl_flag_t* f, unsigned long long n) { f->step += n; }
+__global__ void flag_advance_kernel(cgl_flag_t* f, unsigned long long n) {
+  pdl_wait();
+  f->step += n;
+  pdl_trigger();
+}
 
 __global__ void mul_kernel(int64_t n, const double2* f, const double2* in, double2* out, const cgl_flag_t* flag, uint64_t pos) {
   pos = resolve_pos(flag, pos);
@@ -272,7 +276,8 @@ int pw_flag_reset(cudaStream_t st, cgl_flag_t* f) {
 }
 
 int pw_flag_advance(cudaStream_t st, cgl_flag_t* f, unsigned long long n) {
-  flag_advance_kernel<<<1, 1, 0, st>>>(f, n);
+  cudaError_t e = launch_k(flag_advance_kernel, dim3(1), dim3(1), 0, st, dim3(1), f, n);
+  if (e != cudaSuccess) return set_cuda_error(e, "flag_advance launch");
   return check_launch("flag_advance");
 }
 

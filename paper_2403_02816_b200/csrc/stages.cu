@@ -199,6 +199,7 @@ enum Prog {
 
 template <int NF, int PROG>
 __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a) {
+  pdl_wait();  // inputs and the divergence key come from earlier kernels
   const cgl_flag_t* cf = a.flag;
   const uint64_t step = resolve_pos(cf, a.pos) >> 24;
   // first flow seq of the program (skip position); non-flow programs: 0
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       store<NF>(a.out, 2 * NF, i, axpy<NF>(0.5 * t, g1, out));
     }
   }
+  pdl_trigger();
   raise_min(a.flag, key);
   (void)is_end;
 }
@@ -309,24 +311,26 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
 template <int NF>
 static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
   const int grid = grid_for(a.n, kStageThreads);
+  cudaError_t e = cudaSuccess;
   switch (prog) {
-    case P_IF4_PRE: stage_kernel<NF, P_IF4_PRE><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_IF4_MID: stage_kernel<NF, P_IF4_MID><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_IF4_END: stage_kernel<NF, P_IF4_END><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FLOW1: stage_kernel<NF, P_FLOW1><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FLOW2: stage_kernel<NF, P_FLOW2><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_SPLIT4_MID: stage_kernel<NF, P_SPLIT4_MID><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_SPLIT4_END: stage_kernel<NF, P_SPLIT4_END><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_STRANG_END: stage_kernel<NF, P_STRANG_END><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_IF2_PRE: stage_kernel<NF, P_IF2_PRE><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_IF2_END: stage_kernel<NF, P_IF2_END><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FIF4_S1: stage_kernel<NF, P_FIF4_S1><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FIF4_S2: stage_kernel<NF, P_FIF4_S2><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FIF4_S3: stage_kernel<NF, P_FIF4_S3><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FIF4_S4: stage_kernel<NF, P_FIF4_S4><<<grid, kStageThreads, 0, st>>>(a); break;
-    case P_FLOW_END: stage_kernel<NF, P_FLOW_END><<<grid, kStageThreads, 0, st>>>(a); break;
+    case P_IF4_PRE: e = launch_k(stage_kernel<NF, P_IF4_PRE>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_MID: e = launch_k(stage_kernel<NF, P_IF4_MID>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_END: e = launch_k(stage_kernel<NF, P_IF4_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FLOW1: e = launch_k(stage_kernel<NF, P_FLOW1>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FLOW2: e = launch_k(stage_kernel<NF, P_FLOW2>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_SPLIT4_MID: e = launch_k(stage_kernel<NF, P_SPLIT4_MID>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_SPLIT4_END: e = launch_k(stage_kernel<NF, P_SPLIT4_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_STRANG_END: e = launch_k(stage_kernel<NF, P_STRANG_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF2_PRE: e = launch_k(stage_kernel<NF, P_IF2_PRE>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF2_END: e = launch_k(stage_kernel<NF, P_IF2_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FIF4_S1: e = launch_k(stage_kernel<NF, P_FIF4_S1>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FIF4_S2: e = launch_k(stage_kernel<NF, P_FIF4_S2>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FIF4_S3: e = launch_k(stage_kernel<NF, P_FIF4_S3>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FIF4_S4: e = launch_k(stage_kernel<NF, P_FIF4_S4>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_FLOW_END: e = launch_k(stage_kernel<NF, P_FLOW_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     default: return set_error(CGL_EINVAL, "stage: unknown program");
   }
+  if (e != cudaSuccess) return set_cuda_error(e, "stage_kernel launch");
   return check_launch("stage_kernel");
 }
 
