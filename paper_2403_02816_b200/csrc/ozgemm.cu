@@ -370,6 +370,42 @@ __device__ __forceinline__ void digits8_floor(double x, int e, uint32_t (&w)[8][
   for (int s = 0; s < 8; ++s) w[s][word] |= (d[s] & 0xFFu) << sh;
 }
 
+// floor digits, packed: q = trunc(x 2^(56-e)) split into hi = q >> 28 (signed)
+// and lo = q mod 2^28; the S = 8 base-128 digits of four values are packed
+// into one 32-bit word per slice with byte permutes (same digits as
+// digits8_floor: slice 0 = hi >> 21 two's complement, the others 7-bit).
+__device__ __forceinline__ void q56_floor(double x, int e, int& hi, unsigned& lo) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int E = (int)((bits >> 52) & 0x7FF);
+  long long q = 0;
+  if (E != 0) {
+    const unsigned long long M = (bits & 0xFFFFFFFFFFFFFull) | 0x10000000000000ull;
+    const int k = E - 1019 - e;
+    const unsigned long long mag = k >= 0 ? (M << k) : (k > -64 ? (M >> (-k)) : 0ull);
+    q = (bits >> 63) ? -(long long)mag : (long long)mag;
+  }
+  hi = (int)(q >> 28);
+  lo = (unsigned)q & 0x0FFFFFFFu;
+}
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+__device__ __forceinline__ void words8_floor(const double (&x)[4], int e, uint32_t (&w)[8]) {
+  int h[4];
+  unsigned l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q56_floor(x[i], e, h[i], l[i]);
+  constexpr uint32_t m7 = 0x7F7F7F7Fu;
+  w[0] = pack4(h[0] >> 21, h[1] >> 21, h[2] >> 21, h[3] >> 21);
+  w[1] = pack4(h[0] >> 14, h[1] >> 14, h[2] >> 14, h[3] >> 14) & m7;
+  w[2] = pack4(h[0] >> 7, h[1] >> 7, h[2] >> 7, h[3] >> 7) & m7;
+  w[3] = pack4(h[0], h[1], h[2], h[3]) & m7;
+  w[4] = pack4(l[0] >> 21, l[1] >> 21, l[2] >> 21, l[3] >> 21);
+  w[5] = pack4(l[0] >> 14, l[1] >> 14, l[2] >> 14, l[3] >> 14) & m7;
+  w[6] = pack4(l[0] >> 7, l[1] >> 7, l[2] >> 7, l[3] >> 7) & m7;
+  w[7] = pack4(l[0], l[1], l[2], l[3]) & m7;
+}
+
 // FUSED (data operand, B mode): the CTAs of one row tile form a thread-block
 // cluster spanning the whole K range; each reduces its staged block to
 // partial row exponents, the cluster combines them through distributed
@@ -392,20 +428,34 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   const int tid = threadIdx.x;
   const int rows_here = (int)min((int64_t)CR, a.rows - r0), cols_here = (int)min((int64_t)W, a.cols - c0);
   if constexpr (FUSED) pdl_wait();  // launched with launch_k: the data come from the previous kernel
+  // all CR*W/256 loads of a thread are issued before any store to smem (the
+  // kernel runs as ~one wave: memory-level parallelism decides its speed)
+  static_assert((CR * W) % 256 == 0, "staging tile must be a multiple of the CTA size");
+  constexpr int NLD = CR * W / 256;
+  double2 v[NLD];
   if (a.sc == 1) {
     const double2* zb = z + r0 * a.sr + c0;
-#pragma unroll 4
-    for (int i = tid; i < CR * W; i += 256) {
-      const int rr = i / W, cc = i % W;  // W, CR are powers of two: shifts
-      blk_dyn[rr * (W + 1) + cc] = (rr < rows_here && cc < cols_here) ? zb[rr * a.sr + cc] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = tid + k * 256, rr = i / W, cc = i % W;  // W, CR are powers of two: shifts
+      v[k] = (rr < rows_here && cc < cols_here) ? __ldg(zb + rr * a.sr + cc) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = tid + k * 256;
+      blk_dyn[(i / W) * (W + 1) + i % W] = v[k];
     }
   } else {
     const double2* zb = z + r0 + c0 * a.sc;  // sr == 1
-#pragma unroll 4
-    for (int i = tid; i < CR * W; i += 256) {
-      const int rr = i % CR, cc = i / CR;
-      blk_dyn[rr * (W + 1) + cc] = (rr < rows_here && cc < cols_here) ? zb[rr + (int64_t)cc * a.sc]
-                                                                      : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = tid + k * 256, rr = i % CR, cc = i / CR;
+      v[k] = (rr < rows_here && cc < cols_here) ? __ldg(zb + rr + (int64_t)cc * a.sc) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int i = tid + k * 256;
+      blk_dyn[(i % CR) * (W + 1) + i / CR] = v[k];
     }
   }
   __syncthreads();
@@ -475,17 +525,30 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
 #pragma unroll
     for (int q = 0; q < 8; ++q) wv[q][0] = wv[q][1] = wv[q][2] = wv[q][3] = 0u;
     if (!nonfinite) {
+      const double2* row = blk_dyn + rr * (W + 1) + (gg / NG) * CC + g * 8;
+      if (!AMODE && S == 8 && a.floor_digits) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double2 v = blk_dyn[rr * (W + 1) + (gg / NG) * CC + g * 8 + j];
-        const double x0 = AMODE ? (part ? v.y : v.x) : v.x;
-        const double x1 = AMODE ? (part ? v.x : -v.y) : v.y;
-        if (a.floor_digits) {
-          digits8_floor(x0, e_raw, wv, 2 * j);
-          digits8_floor(x1, e_raw, wv, 2 * j + 1);
-        } else {
-          digits8(x0, e_raw, wv, 2 * j);
-          digits8(x1, e_raw, wv, 2 * j + 1);
+        for (int k = 0; k < 4; ++k) {
+          const double2 v0 = row[2 * k], v1 = row[2 * k + 1];
+          const double x[4] = {v0.x, v0.y, v1.x, v1.y};
+          uint32_t ww[8];
+          words8_floor(x, e_raw, ww);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wv[q][k] = ww[q];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double2 v = row[j];
+          const double x0 = AMODE ? (part ? v.y : v.x) : v.x;
+          const double x1 = AMODE ? (part ? v.x : -v.y) : v.y;
+          if (a.floor_digits) {
+            digits8_floor(x0, e_raw, wv, 2 * j);
+            digits8_floor(x1, e_raw, wv, 2 * j + 1);
+          } else {
+            digits8(x0, e_raw, wv, 2 * j);
+            digits8(x1, e_raw, wv, 2 * j + 1);
+          }
         }
       }
     }

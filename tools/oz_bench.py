@@ -50,5 +50,42 @@ for key, shape, axis, nf in CASES:
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
+
+    # the data slicing alone (same call the product makes first), captured the same way
+    from paper_2403_02816_b200 import _lib
+    lib = _lib.load()
+    n = shape[axis]
+    P = 1
+    for d in shape[:axis]:
+        P *= d
+    Q = 1
+    for d in shape[axis + 1:]:
+        Q *= d
+    bufs = [v for k, v in ws.bufs.items()]
+
+    def slice_only():
+        if Q > 1 and P == 1:
+            _lib.check(lib.cgl_oz_slice_multi(_lib.stream(), ozaki.S, nf, _lib.ptr_array(ins), 1, Q, Q, n, 1, 0, 0,
+                                              _lib.ptr_array([b[0] for b in bufs[:nf]]), 0,
+                                              _lib.ptr_array([b[1] for b in bufs[:nf]]), 0), "slice")
+        elif Q == 1:
+            _lib.check(lib.cgl_oz_slice_multi(_lib.stream(), ozaki.S, nf, _lib.ptr_array(ins), n, 1, P, n, 1, 0, 0,
+                                              _lib.ptr_array([b[0] for b in bufs[:nf]]), 0,
+                                              _lib.ptr_array([b[1] for b in bufs[:nf]]), 0), "slice")
+    us_slice = None
+    if not (Q > 1 and P > 1):
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g2, stream=s):
+                slice_only()
+        torch.cuda.current_stream().wait_stream(s)
+        g2.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            g2.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us_slice = round(e0.elapsed_time(e1) * 1e3 / reps, 2)
     print(json.dumps({"case": key, "shape": shape, "axis": axis, "fields": nf, "us_per_product": round(us, 2),
-                      "lib": os.environ.get("CGL_LIB_OVERRIDE", "default")}), flush=True)
+                      "us_slicing": us_slice, "lib": os.environ.get("CGL_LIB_OVERRIDE", "default")}), flush=True)
