@@ -203,6 +203,20 @@ def _time(torch, fn, reps=20):
     return e0.elapsed_time(e1) / 1e3 / reps
 
 
+def _graphed(torch, fn):
+    """fn captured once into a CUDA graph; returns the replay callable."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    return g.replay
+
+
 def gemm_roofline(torch, w, scheme_fields=4):
     """Dominant kernel of the if4 step: the 4-field axis-0 (left-form) product
     on the INT8 tensor cores (ozgemm_persistent_kernel), timed per launch with CUDA
@@ -231,8 +245,10 @@ def gemm_roofline(torch, w, scheme_fields=4):
                                    _lib.ptr_array([fac.A] * scheme_fields), _lib.ptr_array([fac.Ae] * scheme_fields),
                                    _lib.ptr_array([fac.Az] * scheme_fields), _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                    None, _lib.ptr_array(outs), Q, 1, 0, 0, per, Q, n * Q, None, 0), "oz_gemm")
-    dt = _time(torch, gemm_only)
-    dt_with_slicing = _time(torch, lambda: ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws))
+    # replay captured graphs: eager launches of a ~20 us kernel are host-bound
+    dt = _time(torch, _graphed(torch, gemm_only))
+    dt_with_slicing = _time(torch, _graphed(torch, lambda: ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0,
+                                                                                 ws)))
     bn = ozaki.geometry()[1]
     macs = ozaki.executed_macs_left(fac, (Q + bn - 1) // bn, scheme_fields)
     dense = ozaki.dense_macs(n, Q, n, scheme_fields)
@@ -254,11 +270,11 @@ def gemm_roofline(torch, w, scheme_fields=4):
     fp64_alg = 8.0 * n * w.points * scheme_fields / dt / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS (int8)",
             "frac": achieved / int8_peak,
-            # dram__bytes_read.sum + dram__bytes_write.sum of this launch, ncu --set full
-            # (profiles/r01_ozgemm_ncu_summary.txt; ncu flushes caches, so this is the cold
-            # upper bound -- in the step the operands are L2-resident)
-            "traffic": 23.2e6, "traffic_unit": "bytes per launch",
-            "traffic_source": "profiles/r01_ozgemm_ncu_summary.txt (cold-cache ncu capture)",
+            # dram__bytes_read.sum + dram__bytes_write.sum of one 4-field launch, ncu --set full
+            # (profiles/r01_ozgemm_persistent_ncu_summary.txt; ncu flushes caches, so this is the
+            # cold upper bound -- in the step the operands are L2-resident)
+            "traffic": 19.9e6, "traffic_unit": "bytes per launch",
+            "traffic_source": "profiles/r01_ozgemm_persistent_ncu_summary.txt (cold-cache ncu capture)",
             "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
                       "accumulators): 4-field axis-0 product of the if4 step, M=N=K=512 complex per field, "
                       "S=8 int8 slices",
