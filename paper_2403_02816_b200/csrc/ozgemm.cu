@@ -225,6 +225,25 @@ __device__ __forceinline__ double pow2(int e) {
                "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
                "r"(r[15]))
 
+#define LD32x32b_X8(r, taddr)                                                                               \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"                     \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])  \
+               : "r"(taddr))
+#define ST32x32b_X8(taddr, r)                                                                               \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),       \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]))
+
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t (&r)[N], uint32_t taddr) {
+  static_assert(N == 8 || N == 16, "8 or 16 columns");
+  if constexpr (N == 16) LD32x32b_X16(r, taddr); else LD32x32b_X8(r, taddr);
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
+  static_assert(N == 8 || N == 16, "8 or 16 columns");
+  if constexpr (N == 16) ST32x32b_X16(taddr, r); else ST32x32b_X8(taddr, r);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---- operand slicing ---------------------------------------------------------
@@ -858,7 +877,12 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
 // serialise per issuing warp, ~0.4 us each, so one warp per in-flight stage);
 // warp 1: MMA issuer; warps 2-9: epilogue
 constexpr int OZP_PRODUCERS = 4;
-constexpr int OZP_THREADS = 32 * (10 + OZP_PRODUCERS - 1);
+#ifndef OZP_EPI_GROUPS
+#define OZP_EPI_GROUPS 4
+#endif
+constexpr int OZP_EPI = OZP_EPI_GROUPS;       // epilogue warps per TMEM lane quadrant (column groups)
+constexpr int OZP_EPI_WARPS = 4 * OZP_EPI;    // warps 2 .. 2 + OZP_EPI_WARPS - 1
+constexpr int OZP_THREADS = 32 * (2 + OZP_EPI_WARPS + OZP_PRODUCERS - 1);
 
 template <int S, int BN, int STAGES>
 struct OzPCfg {
@@ -919,7 +943,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 8);
+      mbar_init(&acc_empty[s], OZP_EPI_WARPS);
     }
     for (int s = 0; s < Cfg::NTI; ++s) {
       mbar_init(&ti_full[s], 1);
@@ -932,28 +956,27 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp >= 2 && warp < 10) {
-    const uint32_t q = warp & 3, half = (warp - 2) >> 2;
-    uint32_t zr[16];
+  if (warp >= 2 && warp < 2 + OZP_EPI_WARPS) {
+    constexpr int HC = BN / OZP_EPI;
+    const uint32_t q = warp & 3, grp = (warp - 2) >> 2;
+    uint32_t zr[HC];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) zr[j] = 0u;
+    for (int j = 0; j < HC; ++j) zr[j] = 0u;
 #pragma unroll 1
-    for (int level = 0; level < 2 * S; ++level)
-      ST32x32b_X16(tmem + (q * 32 << 16) + level * BN + half * (BN / 2), zr);
+    for (int level = 0; level < 2 * S; ++level) tmem_st_cols<HC>(tmem + (q * 32 << 16) + level * BN + grp * HC, zr);
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // prologue done (overlaps the previous kernel's tail under PDL); the data
-  // operand, its exponents and the divergence key come from earlier kernels
-  pdl_wait();
   if (threadIdx.x == 0) OZ_TRACE(1);
-
+  // Everything above and the first tile's live-chunk list (constant zero maps)
+  // overlap the previous kernel's tail under PDL; every role executes
+  // griddepcontrol.wait before touching the data operand, its exponents or
+  // the divergence key (written by earlier kernels).
   const int nch = a.nchunks;
   const int64_t step = gridDim.x;
-  const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
-  if (warp == 0 || warp >= 10) {
+  if (warp == 0 || warp >= 2 + OZP_EPI_WARPS) {
     // ---- producers: one ring across all tiles of this CTA.  Producer warp 0
     // first lists the live chunks of each tile (zero maps read 32 chunks per
     // load, ballot) into the tile-info ring; all producer warps and the
@@ -961,8 +984,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     // it_n with it_n % STAGES == p (its own stage: bulk copies serialise per
     // issuing warp). ----
     static_assert(STAGES == OZP_PRODUCERS, "one producer warp per stage");
-    const int pw = warp == 0 ? 0 : warp - 9;
-    const int64_t t_end = (a.debug & 4) ? 0 : total_run;  // debug 4: producers idle
+    const int pw = warp == 0 ? 0 : warp - (1 + OZP_EPI_WARPS);
+    const int64_t t_end = (a.debug & 4) ? 0 : total;  // debug 4: producers idle
     int it_n = 0, j = 0;
     for (int64_t t = blockIdx.x; t < t_end; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
@@ -994,6 +1017,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
         if (lane == 0) mbar_arrive(&ti_full[slot]);
       } else {
         mbar_wait(&ti_full[slot], (j / Cfg::NTI) & 1);
+      }
+      if (j == 0) {
+        pdl_wait();
+        if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) break;  // the issuer skips too
       }
       const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * S * Cfg::A_BYTES;
       const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * S * Cfg::B_BYTES;
@@ -1035,6 +1062,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     constexpr uint32_t LBO = 128, SBO = (KC / 16) * 128;
     constexpr int PER = 256 / BN;
     const uint32_t leader = elect_lane();
+    pdl_wait();
+    const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
     int it_n = 0, j = 0;
     for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const int buf = j & 1;
@@ -1097,12 +1126,14 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     }
     pdl_trigger();  // all MMAs issued: only this CTA's epilogue tail remains
   } else if (warp >= 2) {
-    // ---- epilogue (8 warps; warp pairs share a TMEM lane quadrant) ----
-    constexpr int HC = BN / 2;
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    // ---- epilogue (OZP_EPI warps per TMEM lane quadrant, HC columns each) ----
+    constexpr int HC = BN / OZP_EPI;
+    const int q = warp & 3, half = (warp - 2) >> 2;  // half = column group
     const int row = q * 32 + lane;
     const int part = lane & 1;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + half * HC;
+    pdl_wait();
+    const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
     int j = 0;
     for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
@@ -1127,8 +1158,8 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
 #pragma unroll
       for (int level = 0; level < S; level += 2) {
         uint32_t r0[HC], r1[HC];
-        LD32x32b_X16(r0, base + level * BN);
-        if (level + 1 < S) LD32x32b_X16(r1, base + (level + 1) * BN);
+        tmem_ld_cols<HC>(r0, base + level * BN);
+        if (level + 1 < S) tmem_ld_cols<HC>(r1, base + (level + 1) * BN);
         tmem_wait_ld();
 #pragma unroll
         for (int k = 0; k < HC; ++k) {
@@ -1146,7 +1177,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
 #pragma unroll
         for (int k = 0; k < HC; ++k) zr[k] = 0u;
 #pragma unroll
-        for (int level = 0; level < S; ++level) ST32x32b_X16(base + level * BN, zr);
+        for (int level = 0; level < S; ++level) tmem_st_cols<HC>(base + level * BN, zr);
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tc_fence_before();
         __syncwarp();
