@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
     static_assert(!AMODE && CR == 32, "fused exponents: data operand, 32-row tiles");
     __shared__ double red[8][33];
     __shared__ int redbad[8][32];
-    __shared__ int epart[32];
+    __shared__ int epart[8][32];  // [cluster rank][row]: partials pushed by every CTA of the cluster
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     {
@@ -512,17 +512,21 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
       int e = INT_MIN;
       if (bad) e = NONFINITE;
       else if (m > 0.0) frexp(m, &e);
-      epart[tid] = e;
+      // push this CTA's partial into every peer's slot (DSMEM stores), so after
+      // ONE cluster barrier each CTA reads only its own shared memory and may
+      // exit without waiting for the others
+      const unsigned me = cluster.block_rank(), nb = cluster.num_blocks();
+      for (unsigned rk = 0; rk < nb; ++rk) cluster.map_shared_rank(&epart[0][0], rk)[me * 32 + tid] = e;
     }
     cluster.sync();
     if (tid < 32) {
       int e = INT_MIN;
-      for (unsigned rk = 0; rk < cluster.num_blocks(); ++rk) e = max(e, cluster.map_shared_rank(epart, rk)[tid]);
+      for (unsigned rk = 0; rk < cluster.num_blocks(); ++rk) e = max(e, epart[rk][tid]);
       if (e == INT_MIN) e = 0;  // all-zero row (same convention as rowexp_kernel)
       erow[tid] = e;
       if (blockIdx.y == 0 && tid < rows_here) a.expss[item][b * exp_bs + r0 + tid] = e;
     }
-    cluster.sync();  // partials read before any CTA of the cluster moves on; erow visible
+    __syncthreads();  // erow visible
   }
   constexpr int nreal = AMODE ? 2 : 1;
   constexpr int NG = KC / 16;               // 16-byte groups per chunk
