@@ -104,41 +104,55 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
     Q = math.prod(shape[axis + 1:])
     nf = len(ins)
     dev = ins[0].device
+    # items sharing an input tensor (u with two different factors in the if4
+    # step) share its data slices: slice each distinct input once
+    uniq, idx = [], []
+    for x in ins:
+        for k, y in enumerate(uniq):
+            if y.data_ptr() == x.data_ptr() and y.shape == x.shape:
+                idx.append(k)
+                break
+        else:
+            idx.append(len(uniq))
+            uniq.append(x)
+    nu = len(uniq)
     Aa = _lib.ptr_array([fc.A for fc in factors])
     Ae = _lib.ptr_array([fc.Ae for fc in factors])
     Az = _lib.ptr_array([fc.Az for fc in factors])
     if Q > 1 and P > 1:
         # middle axis: per slab b, Out_b (n x Q) = E In_b; chunk over slabs
         per = _nbytes(Q, n, 0)
-        for b0, b1 in _chunks(P, per, nf, align=1):
+        for b0, b1 in _chunks(P, per, nu, align=1):
             nb = b1 - b0
-            Bs, Be = [], []
-            for f in range(nf):
-                buf, ex = ws.get(("D", f, n), per * nb, Q * nb, dev)
-                Bs.append(buf)
-                Be.append(ex)
-            srcs = [x.view(-1)[b0 * n * Q:] for x in ins]
+            Bu, Beu = [], []
+            for u in range(nu):
+                buf, ex = ws.get(("D", u, n), per * nb, Q * nb, dev)
+                Bu.append(buf)
+                Beu.append(ex)
+            Bs, Be = [Bu[k] for k in idx], [Beu[k] for k in idx]
+            srcs = [x.view(-1)[b0 * n * Q:] for x in uniq]
             dsts = [o.view(-1)[b0 * n * Q:] for o in outs]
-            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), 1, Q, Q, n, nb, n * Q, 0,
-                                              _lib.ptr_array(Bs), per, _lib.ptr_array(Be), Q), "oz_slice(data, B)")
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nu, _lib.ptr_array(srcs), 1, Q, Q, n, nb, n * Q, 0,
+                                              _lib.ptr_array(Bu), per, _lib.ptr_array(Beu), Q), "oz_slice(data, B)")
             _lib.check(lib.cgl_oz_gemm(st, S, n, Q, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                        None, _lib.ptr_array(dsts), Q, nb, 0, 0, per, Q, n * Q,
                                        _lib.flag_ptr(flag), pos), "oz_gemm(middle)")
     elif Q > 1:
         # first axis (P = 1): Out (n x Q) = E In; data Z = In^T rows q; chunk over q
         per_row = _nbytes(1 << 10, n, 0) >> 10 if Q >= (1 << 10) else _nbytes(Q, n, 0) // Q
-        for q0, q1 in _chunks(Q, per_row, nf):
+        for q0, q1 in _chunks(Q, per_row, nu):
             nq = q1 - q0
             per = _nbytes(nq, n, 0)
-            Bs, Be = [], []
-            for f in range(nf):
-                buf, ex = ws.get(("D", f, n), per, nq, dev)
-                Bs.append(buf)
-                Be.append(ex)
-            srcs = [x.view(-1)[q0:] for x in ins]
+            Bu, Beu = [], []
+            for u in range(nu):
+                buf, ex = ws.get(("D", u, n), per, nq, dev)
+                Bu.append(buf)
+                Beu.append(ex)
+            Bs, Be = [Bu[k] for k in idx], [Beu[k] for k in idx]
+            srcs = [x.view(-1)[q0:] for x in uniq]
             dsts = [o.view(-1)[q0:] for o in outs]
-            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), 1, Q, nq, n, 1, 0, 0,
-                                              _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, B)")
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nu, _lib.ptr_array(srcs), 1, Q, nq, n, 1, 0, 0,
+                                              _lib.ptr_array(Bu), 0, _lib.ptr_array(Beu), 0), "oz_slice(data, B)")
             _lib.check(lib.cgl_oz_gemm(st, S, n, nq, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                        None, _lib.ptr_array(dsts), Q, 1, 0, 0, 0, 0, 0,
                                        _lib.flag_ptr(flag), pos), "oz_gemm(first)")
@@ -146,18 +160,19 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
         # last axis: Out (P x n) = In E^T computed as Out^T = E In^T (constant E on the
         # block-skipped A side); data Z = In rows p (K contiguous); chunk over p
         per_row = max(1, _nbytes(min(P, 1 << 10), n, 0) // min(P, 1 << 10))
-        for p0, p1 in _chunks(P, per_row, nf):
+        for p0, p1 in _chunks(P, per_row, nu):
             np_ = p1 - p0
             per = _nbytes(np_, n, 0)
-            Bs, Be = [], []
-            for f in range(nf):
-                buf, ex = ws.get(("D", f, n), per, np_, dev)
-                Bs.append(buf)
-                Be.append(ex)
-            srcs = [x.view(-1)[p0 * n:] for x in ins]
+            Bu, Beu = [], []
+            for u in range(nu):
+                buf, ex = ws.get(("D", u, n), per, np_, dev)
+                Bu.append(buf)
+                Beu.append(ex)
+            Bs, Be = [Bu[k] for k in idx], [Beu[k] for k in idx]
+            srcs = [x.view(-1)[p0 * n:] for x in uniq]
             dsts = [o.view(-1)[p0 * n:] for o in outs]
-            _lib.check(lib.cgl_oz_slice_multi(st, S, nf, _lib.ptr_array(srcs), n, 1, np_, n, 1, 0, 0,
-                                              _lib.ptr_array(Bs), 0, _lib.ptr_array(Be), 0), "oz_slice(data, Bt)")
+            _lib.check(lib.cgl_oz_slice_multi(st, S, nu, _lib.ptr_array(srcs), n, 1, np_, n, 1, 0, 0,
+                                              _lib.ptr_array(Bu), 0, _lib.ptr_array(Beu), 0), "oz_slice(data, Bt)")
             _lib.check(lib.cgl_oz_gemm_t(st, S, n, np_, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                          None, _lib.ptr_array(dsts), n, 1, 0, 0, 0, 0, 0,
                                          _lib.flag_ptr(flag), pos), "oz_gemm(last axis)")
