@@ -156,6 +156,20 @@ int cgl_oz_gemm_t(void* stream, int S, int64_t M, int64_t N, int64_t K, int nite
                   double* const* C, int64_t ldc, int64_t batch,
                   int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
                   const cgl_flag_t* flag, uint64_t pos);
+/* Fused if4 stage + data slicing on a finite-difference grid viewed as
+ * (n0 x Q) (axis 0 x the rest), single-component nonlinearities:
+ *   program CGL_STAGE IF4_MID (1): in = {u2, a}; sliced outputs {g3, s}
+ *     (g2 = g(u2), g3 = g(a + t/2 g2), s = g2 + g3);
+ *   program IF4_END (2): in = {b, c, d, e}; out[0] = u (FP64 state, checked
+ *     finite as cgl_stage); sliced outputs {X1, u, X5} of the next step.
+ * Each sliced output is written as the B-operand slices + row exponents of
+ * the next axis-0 product (exactly cgl_oz_slice_multi's result for Z = In^T,
+ * rows Q, K n0), so X1/X5/g3/s never exist in FP64.  Replaces
+ * integrators.py:205-215 stage arithmetic + the read of the matmul input.
+ * Requires n0 <= 1024. */
+int cgl_stage_slice(void* stream, int program, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl,
+                    double tau, double in_scale, const double* const* in, double* const* out,
+                    cgl_flag_t* flag, uint64_t pos, int8_t* const* slices, int* const* exps);
 /* Tile geometry of the emulated GEMM: A row tile, B row tile, K chunk bytes. */
 int cgl_oz_geometry(int* bm, int* bn, int* kc);
 /* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last

@@ -41,6 +41,8 @@ int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*, int64_t, int64_t);
+int stage_slice_launch(cudaStream_t, int, int64_t, int64_t, const cgl_nonlinear_t*, double, double,
+                       const double* const*, double* const*, cgl_flag_t*, uint64_t, int8_t* const*, int* const*);
 
 static thread_local std::string g_err;
 static unsigned long long g_launches = 0;
@@ -339,6 +341,14 @@ int cgl_oz_slice_multi(void* stream, int S, int nitems, const double* const* src
                        int8_t* const* outs, int64_t out_batch_stride, int* const* exps, int64_t exp_batch_stride) {
   return oz_slice_multi((cudaStream_t)stream, S, nitems, srcs, sr, sc, rows, cols, batch, src_batch_stride, a_mode,
                         outs, out_batch_stride, exps, exp_batch_stride, 1);
+}
+
+int cgl_stage_slice(void* stream, int program, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl, double tau,
+                    double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,
+                    int8_t* const* slices, int* const* exps) {
+  if (!nl || !in || !slices || !exps) return set_error(CGL_EINVAL, "cgl_stage_slice: null argument");
+  return stage_slice_launch((cudaStream_t)stream, program, n0, Q, nl, tau, in_scale, in, out, flag, pos, slices,
+                            exps);
 }
 
 int cgl_oz_geometry(int* bm, int* bn, int* kc) {

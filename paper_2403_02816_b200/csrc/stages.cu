@@ -30,8 +30,12 @@
 // skips if a failure was recorded before its FIRST flow position.
 #include <cstdint>
 
+#include <climits>
+#include <cooperative_groups.h>
+
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
+#include "oz_slice.cuh"
 
 namespace cgl {
 
@@ -306,6 +310,217 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
   pdl_trigger();
   raise_min(a.flag, key);
   (void)is_end;
+}
+
+// ---- fused stage + data slicing (INT8-emulated products, if4 on FD grids) ----
+// The if4 stage outputs X1, X5 (END) and g3, s (MID) are consumed only as the
+// data operands of the next axis-0 mu-mode products, so they are never stored
+// in FP64: a cluster of CTAs spanning the axis-0 range of 32 consecutive
+// columns q of the (n0 x Q) field view computes the stage pointwise on its
+// block, stores the state u (END) in FP64, keeps the sliced outputs in shared
+// memory, exchanges partial column exponents through DSMEM (one cluster
+// barrier) and emits the floor-digit slices in the GEMM's B-operand layout
+// (Z = In^T: rows q, K = axis-0 index; exactly what cgl_oz_slice_multi
+// produces for the same field).  One pass instead of a stage kernel plus a
+// slicing kernel per field.
+struct StageSliceArgs {
+  StageArgs s;        // inputs; s.out[0] = u (END only)
+  int8_t* slices[3];  // per sliced output: B-mode slices (rows Q, K n0)
+  int* exps[3];       // per sliced output: row (= column q) exponents
+  int64_t Q, n0;
+  int nchunks;
+};
+
+template <int PROG, int NSL, int CPBT>
+__global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A) {
+  namespace cg = cooperative_groups;
+  using oz::KC;
+  using oz::NONFINITE;
+  constexpr int CR = 32;                 // Z rows (columns q) per tile = the GEMM's B row tile
+  constexpr int CC = KC / 2;             // complex K per chunk
+  constexpr int W = CC * CPBT;           // complex K per CTA
+  constexpr int PT = CR * W / 256;       // points per thread
+  static_assert(kOzBN == CR, "B row tile");
+  pdl_wait();
+  const StageArgs& a = A.s;
+  const cgl_flag_t* cf = a.flag;
+  const uint64_t step = resolve_pos(cf, a.pos) >> 24;
+  if (flag_skip(cf, step << 24)) return;  // uniform over the grid (the key is read-only here)
+  uint64_t key = ~0ull;
+  const uint64_t check_pos = (step << 24) | (255ull << 8);
+  const double t = a.tau, sc = a.in_scale;
+  extern __shared__ double2 blk[];  // [NSL][CR][W + 1]
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * CR, c0 = (int64_t)blockIdx.y * W;
+  const int rows_here = (int)min((int64_t)CR, A.Q - r0), cols_here = (int)min((int64_t)W, A.n0 - c0);
+  // ---- stage, pointwise (consecutive threads: consecutive q, coalesced) ----
+#pragma unroll 2
+  for (int j = 0; j < PT; ++j) {
+    const int k = tid + 256 * j, rr = k % CR, cc = k / CR;
+    double2 o[NSL];
+#pragma unroll
+    for (int q = 0; q < NSL; ++q) o[q] = make_double2(0.0, 0.0);
+    if (rr < rows_here && cc < cols_here) {
+      const int64_t i = (c0 + cc) * A.Q + (r0 + rr);
+      if (PROG == P_IF4_MID) {
+        const V<1> u2 = load<1>(a.in, 0, i, sc), av = load<1>(a.in, 1, i, sc);
+        const V<1> g2 = gfun<1>(a.nl, u2);
+        const V<1> g3 = gfun<1>(a.nl, axpy<1>(0.5 * t, g2, av));
+        o[0] = g3.c[0];
+        o[1] = axpy<1>(1.0, g2, g3).c[0];
+      } else {  // P_IF4_END
+        const V<1> b = load<1>(a.in, 0, i, sc), c = load<1>(a.in, 1, i, sc);
+        const V<1> d = load<1>(a.in, 2, i, sc), e = load<1>(a.in, 3, i, sc);
+        const V<1> g4 = gfun<1>(a.nl, axpy<1>(t, d, b));
+        const V<1> out = axpy<1>(t / 6.0, g4, axpy<1>(t / 3.0, e, c));
+        if (!finite_all<1>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        store<1>(a.out, 0, i, out);
+        const V<1> g1 = gfun<1>(a.nl, out);
+        o[0] = axpy<1>(0.5 * t, g1, out).c[0];   // X1
+        o[1] = out.c[0];                          // u
+        o[2] = axpy<1>(t / 6.0, g1, out).c[0];    // X5
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NSL; ++q) blk[(q * CR + rr) * (W + 1) + cc] = o[q];
+  }
+  __syncthreads();
+  pdl_trigger();
+  // ---- partial exponents of the 32 Z rows per output, exchanged in the cluster ----
+  __shared__ double red[NSL][8][33];
+  __shared__ int redbad[NSL][8][32];
+  __shared__ int epart[NSL][16][32];  // [output][cluster rank][row]
+  __shared__ int erow[NSL][32];
+  cg::cluster_group cluster = cg::this_cluster();
+  {
+    const int rr = tid & 31, part = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < NSL; ++q) {
+      double m = 0.0;
+      bool bad = false;
+      for (int cc = part; cc < cols_here; cc += 8) {
+        const double2 v = blk[(q * CR + rr) * (W + 1) + cc];
+        bad |= !isfinite(v.x) || !isfinite(v.y);
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+      }
+      red[q][part][rr] = m;
+      redbad[q][part][rr] = bad;
+    }
+  }
+  __syncthreads();
+  if (tid < 32 * NSL) {
+    const int q = tid >> 5, rr = tid & 31;
+    double m = red[q][0][rr];
+    int bad = redbad[q][0][rr];
+    for (int k = 1; k < 8; ++k) {
+      m = fmax(m, red[q][k][rr]);
+      bad |= redbad[q][k][rr];
+    }
+    int e = INT_MIN;
+    if (bad) e = NONFINITE;
+    else if (m > 0.0) frexp(m, &e);
+    const unsigned me = cluster.block_rank(), nb = cluster.num_blocks();
+    for (unsigned rk = 0; rk < nb; ++rk) cluster.map_shared_rank(&epart[0][0][0], rk)[(q * 16 + me) * 32 + rr] = e;
+  }
+  cluster.sync();
+  if (tid < 32 * NSL) {
+    const int q = tid >> 5, rr = tid & 31;
+    int e = INT_MIN;
+    for (unsigned rk = 0; rk < cluster.num_blocks(); ++rk) e = max(e, epart[q][rk][rr]);
+    if (e == INT_MIN) e = 0;  // all-zero row (same convention as the slicing kernels)
+    erow[q][rr] = e;
+    if (blockIdx.y == 0 && rr < rows_here) A.exps[q][r0 + rr] = e;
+  }
+  __syncthreads();
+  // ---- slices (same digits and layout as slice_tile_kernel<8, 0>) ----
+  constexpr int NG = KC / 16, groups = CPBT * NG;
+  const int ch0 = blockIdx.y * CPBT;
+  for (int w = tid; w < NSL * CR * groups; w += 256) {
+    const int q = w / (CR * groups), rem = w % (CR * groups);
+    const int rr = rem % CR, gg = rem / CR;
+    const int ch = ch0 + gg / NG, g = gg % NG;
+    if (rr >= rows_here || ch >= A.nchunks) continue;
+    const int e = erow[q][rr];
+    uint32_t wv[8][4];
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8) wv[s8][0] = wv[s8][1] = wv[s8][2] = wv[s8][3] = 0u;
+    if (e != NONFINITE) {
+      const double2* row = blk + (q * CR + rr) * (W + 1) + (gg / NG) * CC + g * 8;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 v0 = row[2 * k], v1 = row[2 * k + 1];
+        const double x[4] = {v0.x, v0.y, v1.x, v1.y};
+        uint32_t ww[8];
+        oz::words8_floor(x, e, ww);
+#pragma unroll
+        for (int s8 = 0; s8 < 8; ++s8) wv[s8][k] = ww[s8];
+      }
+    }
+    int8_t* dst = A.slices[q] + oz::tile_offset(r0 + rr, (int64_t)ch * KC + g * 16, CR, A.nchunks, 8);
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8)
+      *reinterpret_cast<uint4*>(dst + s8 * (CR * KC)) = make_uint4(wv[s8][0], wv[s8][1], wv[s8][2], wv[s8][3]);
+  }
+  raise_min(a.flag, key);
+}
+
+template <int PROG, int NSL, int CPBT>
+static cudaError_t launch_stage_slice(const StageSliceArgs& A, cudaStream_t st) {
+  constexpr int W = (oz::KC / 2) * CPBT;
+  const int cy = (A.nchunks + CPBT - 1) / CPBT;
+  const size_t smem = (size_t)NSL * 32 * (W + 1) * sizeof(double2);
+  auto kern = stage_slice_kernel<PROG, NSL, CPBT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  const dim3 grid((unsigned)((A.Q + 31) / 32), (unsigned)cy, 1);
+  return launch_k(kern, grid, dim3(256), smem, st, dim3(1, (unsigned)cy, 1), A);
+}
+
+int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl, double tau,
+                       double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,
+                       int8_t* const* slices, int* const* exps) {
+  if (prog != P_IF4_MID && prog != P_IF4_END) return set_error(CGL_EINVAL, "stage_slice: if4 MID/END only");
+  if (n0 <= 0 || Q <= 0) return 0;
+  StageSliceArgs A{};
+  StageArgs& a = A.s;
+  const int nin = prog == P_IF4_MID ? 2 : 4, nsl = prog == P_IF4_MID ? 2 : 3;
+  for (int k = 0; k < nin; ++k) a.in[k] = reinterpret_cast<const double2*>(in[k]);
+  if (prog == P_IF4_END) a.out[0] = reinterpret_cast<double2*>(out[0]);
+  a.n = n0 * Q;
+  a.tau = tau;
+  a.in_scale = in_scale;
+  a.nl.a3 = nl->alpha3;
+  a.nl.b3 = nl->beta3;
+  a.nl.a4 = nl->alpha4;
+  a.nl.b4 = nl->beta4;
+  a.nl.a5 = nl->alpha5;
+  a.nl.kind = nl->kind;
+  if (nl->kind == 2) return set_error(CGL_EINVAL, "stage_slice: single-component nonlinearities only");
+  a.flag = flag;
+  a.pos = pos;
+  a.fw = 1;
+  for (int q = 0; q < nsl; ++q) {
+    A.slices[q] = slices[q];
+    A.exps[q] = exps[q];
+  }
+  A.Q = Q;
+  A.n0 = n0;
+  A.nchunks = (int)((2 * n0 + oz::KC - 1) / oz::KC);
+  // CTAs of a tile's cluster cover all K chunks: <= 16 CTAs (non-portable beyond 8)
+  cudaError_t e;
+  if (A.nchunks <= 32) {
+    e = prog == P_IF4_MID ? launch_stage_slice<P_IF4_MID, 2, 2>(A, st) : launch_stage_slice<P_IF4_END, 3, 2>(A, st);
+  } else if (A.nchunks <= 64) {
+    e = prog == P_IF4_MID ? launch_stage_slice<P_IF4_MID, 2, 4>(A, st) : launch_stage_slice<P_IF4_END, 3, 4>(A, st);
+  } else {
+    return set_error(CGL_ESHAPE, "stage_slice: axis-0 extent above 1024");
+  }
+  if (e != cudaSuccess) return set_cuda_error(e, "stage_slice launch");
+  return check_launch("stage_slice_kernel");
 }
 
 template <int NF>

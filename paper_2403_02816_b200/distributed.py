@@ -132,6 +132,7 @@ class ShardedPlan(FusedPlan):
     (NCCL collectives are not captured)."""
 
     CHUNK = 1 << 30  # never graph-capture
+    FUSE_STAGE_SLICE = False  # products run through the transposes on DMMA
 
     def __init__(self, problem, scheme_name, like, layout, group=None):
         super().__init__(problem, scheme_name, like)

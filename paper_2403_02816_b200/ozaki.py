@@ -74,6 +74,12 @@ class Workspace:
         return b
 
 
+def single_chunk(shape, nfields):
+    """The axis-0 data slices of nfields fields fit one workspace chunk."""
+    n0, Q = shape[0], math.prod(shape[1:])
+    return nfields * _nbytes(Q, n0, 0) <= CHUNK_BYTES
+
+
 def fits(shape, nfields):
     """Small grids (C0 128^2) are launch-latency bound: the DMMA path is faster."""
     return math.prod(shape) >= (1 << 17)
@@ -92,10 +98,11 @@ def _chunks(total, per_unit, nf, align=128):
     return [(a, min(total, a + units)) for a in range(0, total, units)]
 
 
-def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
+def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=None):
     """outs[f] = ins[f] x_axis E_f for square E_f (SlicedFactor), one GEMM
     launch per chunk (one chunk unless the data slices would exceed
-    CHUNK_BYTES, e.g. 1024^3 fields)."""
+    CHUNK_BYTES, e.g. 1024^3 fields).  presliced (first axis only): per item
+    (slices, exponents) already produced (cgl_stage_slice); no slicing."""
     lib = _lib.load()
     st = _lib.stream()
     shape = tuple(ins[0].shape)
@@ -137,6 +144,11 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
             _lib.check(lib.cgl_oz_gemm(st, S, n, Q, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                        None, _lib.ptr_array(dsts), Q, nb, 0, 0, per, Q, n * Q,
                                        _lib.flag_ptr(flag), pos), "oz_gemm(middle)")
+    elif Q > 1 and presliced is not None:
+        Bs, Be = [p_[0] for p_ in presliced], [p_[1] for p_ in presliced]
+        _lib.check(lib.cgl_oz_gemm(st, S, n, Q, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
+                                   None, _lib.ptr_array(outs), Q, 1, 0, 0, 0, 0, 0,
+                                   _lib.flag_ptr(flag), pos), "oz_gemm(first, presliced)")
     elif Q > 1:
         # first axis (P = 1): Out (n x Q) = E In; data Z = In^T rows q; chunk over q
         per_row = _nbytes(1 << 10, n, 0) >> 10 if Q >= (1 << 10) else _nbytes(Q, n, 0) // Q
@@ -179,7 +191,7 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0):
     return outs
 
 
-def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0):
+def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0, pre0=None):
     """Tucker chains of up to 8 fields, one emulated GEMM launch per mode
     (same mode order and ping-pong as cgl_tucker); `ws` is the caller's
     Workspace (per plan: captured graphs keep its pointers)."""
@@ -188,7 +200,8 @@ def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0):
     for axis in range(nd):
         to_out = (nd - axis) % 2 == 1
         dst = outs if to_out else work
-        mode_product_oz(src, [fs[axis] for fs in factor_sets], dst, axis, ws, flag=flag, pos=pos)
+        mode_product_oz(src, [fs[axis] for fs in factor_sets], dst, axis, ws, flag=flag, pos=pos,
+                        presliced=pre0 if axis == 0 else None)
         src = dst
     return outs
 

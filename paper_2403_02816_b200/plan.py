@@ -18,6 +18,8 @@ Per-step launch structure (d = number of dimensions, one GEMM per mode):
 
 import os
 
+import math
+
 import torch
 
 from . import _lib
@@ -50,6 +52,7 @@ def make_plan(problem, scheme_name, like):
 
 class FusedPlan:
     CHUNK = 16
+    FUSE_STAGE_SLICE = True  # if4 stages emit the next axis-0 data slices (cgl_stage_slice)
 
     def __init__(self, problem, scheme_name, like):
         from fractions import Fraction
@@ -87,11 +90,43 @@ class FusedPlan:
         self.replayed_launches = 0     # cgl kernels launched by graph replays (not seen by the C counter)
 
     # -- launch helpers --------------------------------------------------------
-    def _tucker(self, jobs, flag):
+    def _fused_slices(self):
+        """Workspace slots for cgl_stage_slice outputs when the fused if4 path
+        applies (INT8-emulated products, single component, one slice chunk,
+        not lean), else None.  Slots 0-2: END's X1, u, X5; 3-4: MID's g3, s."""
+        if getattr(self, "_fs", False) is not False:
+            return self._fs
+        self._fs = None
+        import os
+        from . import ozaki
+        if self.use_oz is None:
+            self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
+        if (self.FUSE_STAGE_SLICE and self.scheme == "if4" and self.use_oz and not self.lean and self.nf == 1
+                and len(self.shape) >= 2 and self.shape[0] <= 1024 and self.nl.kind != 2
+                and ozaki.single_chunk(self.shape, 4) and os.environ.get("CGL_FUSE_STAGE", "1") != "0"):
+            n0, Q = self.shape[0], math.prod(self.shape[1:])
+            per = _lib.load().cgl_oz_slice_bytes(ozaki.S, Q, n0, 0)
+            dev = self.U[0][0].device
+            self._fs = [self.oz_ws.get(("F", j, n0), per, Q, dev) for j in range(5)]
+        return self._fs
+
+    def _stage_slice(self, name, ins, outs, slots, flag, tau):
+        lib = _lib.load()
+        fin = [t for fs in ins for t in fs]
+        fout = [t for fs in outs for t in fs]
+        n0, Q = self.shape[0], math.prod(self.shape[1:])
+        _lib.check(lib.cgl_stage_slice(_lib.stream(), _lib.STAGE[name], n0, Q, _lib.ctypes.byref(self.nl), tau, 1.0,
+                                       _lib.ptr_array(fin), _lib.ptr_array(fout) if fout else None,
+                                       _lib.flag_ptr(flag), self._pos, _lib.ptr_array([t[0] for t in slots]),
+                                       _lib.ptr_array([t[1] for t in slots])), "cgl_stage_slice")
+
+    def _tucker(self, jobs, flag, pre0=None):
         """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode
         (lean mode: one job at a time through the single scratch field).
         Products run on the INT8 tensor cores (ozaki.py) unless CGL_GEMM=dmma
-        or the data-slice workspace would not fit; else on the DMMA kernel."""
+        or the data-slice workspace would not fit; else on the DMMA kernel.
+        pre0: per job (slices, exponents) of its axis-0 data, already made by
+        cgl_stage_slice (fused if4 path)."""
         if self.lean and len(jobs) > 1:
             for j in jobs:
                 self._tucker([j], flag)
@@ -110,8 +145,9 @@ class FusedPlan:
             for i in range(0, len(ins), 8):
                 sl = slice(i, i + 8)
                 ozaki.tucker_oz(ins[sl], facs[sl], outs[sl], work[sl] if work else None, self.oz_ws, flag=flag,
-                                pos=self._pos)
+                                pos=self._pos, pre0=pre0[sl] if pre0 is not None else None)
             return
+        assert pre0 is None, "pre-sliced operands need the INT8-emulated products"
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
             for c in range(self.nf):
@@ -161,7 +197,19 @@ class FusedPlan:
         """One time step k (1-based); input state_after(k-1), output state_after(k)."""
         self._pos = _lib.rel_pos(k - self._k_base)
         B, H, O = self.B, self.half, self.one
-        if self.scheme == "if4":
+        if self.scheme == "if4" and self._fused_slices() is not None:
+            # X1, u, X5 (after step k-1) and g3, s reach their products only as
+            # slices made by the fused stage kernels; step 1 slices the prologue's X1, X5
+            u = self.U[0]
+            x1, x5, u2, a, b, c = B
+            F = self._fs
+            self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag,
+                         pre0=None if k == 1 else [F[0], F[1], F[1], F[2]])
+            self._stage_slice("if4_mid", [u2, a], [], [F[3], F[4]], flag, tau)
+            self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
+            self._before_end(flag)
+            self._stage_slice("if4_end", [b, c, x1, x5], [u], [F[0], F[1], F[2]], flag, tau)
+        elif self.scheme == "if4":
             u = self.U[0]
             x1, x5, u2, a, b, c = B
             self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag)
