@@ -373,6 +373,54 @@ def test_oz_chunked_products_bit_identical(P, monkeypatch):
         assert torch.equal(res[(1 << 40, axis)], res[(200_000, axis)])
 
 
+@pytest.mark.parametrize("shape", [(512, 512), (64, 48, 40)])
+@pytest.mark.parametrize("prog", ["if4_mid", "if4_end"])
+def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
+    """cgl_stage_slice (fused if4 stage + axis-0 data slicing) is bit-identical
+    to cgl_stage followed by cgl_oz_slice_multi of its outputs."""
+    from paper_2403_02816_b200 import _lib, ozaki, workloads as W
+    lib = _lib.load()
+    st = _lib.stream()
+    prob = W.build_problem(W.CONFIGS["C1"])
+    nl = prob._nl
+    g = torch.Generator().manual_seed(11)
+    nin = 2 if prog == "if4_mid" else 4
+    ins = [(0.3 * torch.complex(torch.randn(shape, generator=g, dtype=torch.float64),
+                                torch.randn(shape, generator=g, dtype=torch.float64))).cuda() for _ in range(nin)]
+    tau = 0.005
+    n0, Q = shape[0], int(np.prod(shape[1:]))
+    # reference: unfused stage, then the data slicing of each sliced output
+    outs = [torch.empty_like(ins[0]) for _ in range(2 if prog == "if4_mid" else 3)]
+    flag = _lib.new_flag(0)
+    _lib.check(lib.cgl_stage(st, _lib.STAGE[prog], 1, n0 * Q, _lib.ctypes.byref(nl), tau, 1.0,
+                             _lib.ptr_array(ins), _lib.ptr_array(outs), _lib.flag_ptr(flag), _lib.rel_pos(1)), "stage")
+    sliced = outs if prog == "if4_mid" else [outs[1], outs[0], outs[2]]  # END: X1, u, X5
+    per = lib.cgl_oz_slice_bytes(ozaki.S, Q, n0, 0)
+    ref = []
+    for x in sliced:
+        b = torch.zeros(per, dtype=torch.int8, device="cuda")
+        e = torch.empty(Q, dtype=torch.int32, device="cuda")
+        _lib.check(lib.cgl_oz_slice_multi(st, ozaki.S, 1, _lib.ptr_array([x]), 1, Q, Q, n0, 1, 0, 0,
+                                          _lib.ptr_array([b]), 0, _lib.ptr_array([e]), 0), "slice")
+        ref.append((b, e))
+    # fused
+    flag2 = _lib.new_flag(0)
+    u = torch.empty_like(ins[0])
+    got = [(torch.zeros(per, dtype=torch.int8, device="cuda"), torch.empty(Q, dtype=torch.int32, device="cuda"))
+           for _ in sliced]
+    _lib.check(lib.cgl_stage_slice(st, _lib.STAGE[prog], n0, Q, _lib.ctypes.byref(nl), tau, 1.0,
+                                   _lib.ptr_array(ins), _lib.ptr_array([u]) if prog == "if4_end" else None,
+                                   _lib.flag_ptr(flag2), _lib.rel_pos(1), _lib.ptr_array([t[0] for t in got]),
+                                   _lib.ptr_array([t[1] for t in got])), "stage_slice")
+    torch.cuda.synchronize()
+    for (rb, re_), (gb, ge) in zip(ref, got):
+        assert torch.equal(re_, ge)
+        assert torch.equal(rb, gb)
+    if prog == "if4_end":
+        assert torch.equal(u, outs[0])
+    assert torch.equal(flag[:1], flag2[:1])
+
+
 @pytest.mark.parametrize("nranks", [1, 2, 4])
 @pytest.mark.parametrize("scheme,tag", [("if4", "C3s32_if4"), ("strang", "C3s32_strang")])
 def test_slab_sharded_fourier_virtual_ranks(P, config_golden, nranks, scheme, tag):
