@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
   const StageArgs& a = A.s;
   const cgl_flag_t* cf = a.flag;
   const uint64_t step = resolve_pos(cf, a.pos) >> 24;
-  if (flag_skip(cf, step << 24)) return;  // uniform over the grid (the key is read-only here)
+  int first = 0;  // first flow seq of the program (as stage_kernel)
+  if (PROG == P_SPLIT4_MID || PROG == P_STRANG_END) first = a.fw;
+  if (PROG == P_SPLIT4_END) first = 4 * a.fw;
+  if (flag_skip(cf, (step << 24) | ((uint64_t)first << 8))) return;  // uniform over the grid
   uint64_t key = ~0ull;
   const uint64_t check_pos = (step << 24) | (255ull << 8);
   const double t = a.tau, sc = a.in_scale;
@@ -368,6 +371,25 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
         const V<1> g3 = gfun<1>(a.nl, axpy<1>(0.5 * t, g2, av));
         o[0] = g3.c[0];
         o[1] = axpy<1>(1.0, g2, g3).c[0];
+      } else if (PROG == P_STRANG_END) {
+        const V<1> w = load<1>(a.in, 0, i, sc);
+        const V<1> out = flow<1>(a.nl, w, 0.5 * t, step, a.fw, key);
+        if (!finite_all<1>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        store<1>(a.out, 0, i, out);
+        o[0] = flow<1>(a.nl, out, 0.5 * t, step + 1, 0, key).c[0];              // v of step + 1
+      } else if (PROG == P_SPLIT4_MID) {
+        const V<1> v = load<1>(a.in, 0, i, sc), f = load<1>(a.in, 1, i, sc);
+        store<1>(a.out, 0, i, flow<1>(a.nl, v, 0.5 * t, step, a.fw, key));     // coarse c (FP64)
+        o[0] = flow<1>(a.nl, f, 0.5 * t, step, 3 * a.fw, key).c[0];             // f (sliced only)
+      } else if (PROG == P_SPLIT4_END) {
+        const V<1> f = load<1>(a.in, 0, i, sc), c = load<1>(a.in, 1, i, sc);
+        const V<1> fine = flow<1>(a.nl, f, 0.25 * t, step, 4 * a.fw, key);
+        V<1> out;
+        out.c[0] = cadd(cscale(4.0 / 3.0, fine.c[0]), cscale(-1.0 / 3.0, c.c[0]));
+        if (!finite_all<1>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        store<1>(a.out, 0, i, out);
+        o[0] = flow<1>(a.nl, out, 0.5 * t, step + 1, 0, key).c[0];              // v of step + 1
+        o[1] = flow<1>(a.nl, out, 0.25 * t, step + 1, 2 * a.fw, key).c[0];      // f of step + 1
       } else {  // P_IF4_END
         const V<1> b = load<1>(a.in, 0, i, sc), c = load<1>(a.in, 1, i, sc);
         const V<1> d = load<1>(a.in, 2, i, sc), e = load<1>(a.in, 3, i, sc);
@@ -483,13 +505,21 @@ static cudaError_t launch_stage_slice(const StageSliceArgs& A, cudaStream_t st) 
 int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl, double tau,
                        double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,
                        int8_t* const* slices, int* const* exps) {
-  if (prog != P_IF4_MID && prog != P_IF4_END) return set_error(CGL_EINVAL, "stage_slice: if4 MID/END only");
+  int nin, nsl, nout;
+  switch (prog) {
+    case P_IF4_MID: nin = 2; nsl = 2; nout = 0; break;
+    case P_IF4_END: nin = 4; nsl = 3; nout = 1; break;
+    case P_STRANG_END: nin = 1; nsl = 1; nout = 1; break;
+    case P_SPLIT4_MID: nin = 2; nsl = 1; nout = 1; break;
+    case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
+    default: return set_error(CGL_EINVAL, "stage_slice: if4 MID/END, strang END, split4 MID/END only");
+  }
   if (n0 <= 0 || Q <= 0) return 0;
+  if (nout && (!out || !out[0])) return set_error(CGL_EINVAL, "stage_slice: program writes an FP64 output");
   StageSliceArgs A{};
   StageArgs& a = A.s;
-  const int nin = prog == P_IF4_MID ? 2 : 4, nsl = prog == P_IF4_MID ? 2 : 3;
   for (int k = 0; k < nin; ++k) a.in[k] = reinterpret_cast<const double2*>(in[k]);
-  if (prog == P_IF4_END) a.out[0] = reinterpret_cast<double2*>(out[0]);
+  if (nout) a.out[0] = reinterpret_cast<double2*>(out[0]);
   a.n = n0 * Q;
   a.tau = tau;
   a.in_scale = in_scale;
@@ -511,14 +541,18 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   A.n0 = n0;
   A.nchunks = (int)((2 * n0 + oz::KC - 1) / oz::KC);
   // CTAs of a tile's cluster cover all K chunks: <= 16 CTAs (non-portable beyond 8)
+  if (A.nchunks > 64) return set_error(CGL_ESHAPE, "stage_slice: axis-0 extent above 1024");
+  const bool small = A.nchunks <= 32;
+#define SS_LAUNCH(P_, N_) (small ? launch_stage_slice<P_, N_, 2>(A, st) : launch_stage_slice<P_, N_, 4>(A, st))
   cudaError_t e;
-  if (A.nchunks <= 32) {
-    e = prog == P_IF4_MID ? launch_stage_slice<P_IF4_MID, 2, 2>(A, st) : launch_stage_slice<P_IF4_END, 3, 2>(A, st);
-  } else if (A.nchunks <= 64) {
-    e = prog == P_IF4_MID ? launch_stage_slice<P_IF4_MID, 2, 4>(A, st) : launch_stage_slice<P_IF4_END, 3, 4>(A, st);
-  } else {
-    return set_error(CGL_ESHAPE, "stage_slice: axis-0 extent above 1024");
+  switch (prog) {
+    case P_IF4_MID: e = SS_LAUNCH(P_IF4_MID, 2); break;
+    case P_IF4_END: e = SS_LAUNCH(P_IF4_END, 3); break;
+    case P_STRANG_END: e = SS_LAUNCH(P_STRANG_END, 1); break;
+    case P_SPLIT4_MID: e = SS_LAUNCH(P_SPLIT4_MID, 1); break;
+    default: e = SS_LAUNCH(P_SPLIT4_END, 2); break;
   }
+#undef SS_LAUNCH
   if (e != cudaSuccess) return set_cuda_error(e, "stage_slice launch");
   return check_launch("stage_slice_kernel");
 }

@@ -101,13 +101,15 @@ class FusedPlan:
         from . import ozaki
         if self.use_oz is None:
             self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
-        if (self.FUSE_STAGE_SLICE and self.scheme == "if4" and self.use_oz and not self.lean and self.nf == 1
+        if (self.FUSE_STAGE_SLICE and self.scheme in ("if4", "strang", "split4") and self.use_oz and not self.lean
+                and self.nf == 1
                 and len(self.shape) >= 2 and self.shape[0] <= 1024 and self.nl.kind != 2
                 and ozaki.single_chunk(self.shape, 4) and os.environ.get("CGL_FUSE_STAGE", "1") != "0"):
             n0, Q = self.shape[0], math.prod(self.shape[1:])
             per = _lib.load().cgl_oz_slice_bytes(ozaki.S, Q, n0, 0)
             dev = self.U[0][0].device
-            self._fs = [self.oz_ws.get(("F", j, n0), per, Q, dev) for j in range(5)]
+            nslots = {"if4": 5, "strang": 1, "split4": 3}[self.scheme]
+            self._fs = [self.oz_ws.get(("F", j, n0), per, Q, dev) for j in range(nslots)]
         return self._fs
 
     def _stage_slice(self, name, ins, outs, slots, flag, tau):
@@ -223,6 +225,23 @@ class FusedPlan:
             self._tucker([(O, x, u2), (O, y, o)], flag)
             self._before_end(flag)
             self._stage("if2_end", [u2, o], [u, x, y], flag, tau)
+        elif self.scheme == "strang" and self._fused_slices() is not None:
+            # v (= flow of the previous state) reaches its product only as slices
+            v, w = B
+            F = self._fs
+            self._tucker([(O, v, w)], flag, pre0=None if k == 1 else [F[0]])
+            self._before_end(flag)
+            self._stage_slice("strang_end", [w], [self.state_after(k)], [F[0]], flag, tau)
+        elif self.scheme == "split4" and self._fused_slices() is not None:
+            # v, f of each step and the fine-path f after its first half step
+            # reach their products only as slices (slots 0, 1 and 2)
+            v, f, v2, f2 = B
+            F = self._fs
+            self._tucker([(O, v, v2), (H, f, f2)], flag, pre0=None if k == 1 else [F[0], F[1]])
+            self._stage_slice("split4_mid", [v2, f2], [v2], [F[2]], flag, tau)   # coarse c -> v2 (FP64)
+            self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
+            self._before_end(flag)
+            self._stage_slice("split4_end", [v, v2], [self.state_after(k)], [F[0], F[1]], flag, tau)
         elif self.scheme == "strang":
             v, w = B
             self._tucker([(O, v, w)], flag)

@@ -374,27 +374,31 @@ def test_oz_chunked_products_bit_identical(P, monkeypatch):
 
 
 @pytest.mark.parametrize("shape", [(512, 512), (64, 48, 40)])
-@pytest.mark.parametrize("prog", ["if4_mid", "if4_end"])
+@pytest.mark.parametrize("prog", ["if4_mid", "if4_end", "strang_end", "split4_mid", "split4_end"])
 def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
-    """cgl_stage_slice (fused if4 stage + axis-0 data slicing) is bit-identical
-    to cgl_stage followed by cgl_oz_slice_multi of its outputs."""
+    """cgl_stage_slice (fused stage + axis-0 data slicing) is bit-identical
+    to cgl_stage followed by cgl_oz_slice_multi of its outputs (divergence
+    key included)."""
     from paper_2403_02816_b200 import _lib, ozaki, workloads as W
     lib = _lib.load()
     st = _lib.stream()
     prob = W.build_problem(W.CONFIGS["C1"])
     nl = prob._nl
     g = torch.Generator().manual_seed(11)
-    nin = 2 if prog == "if4_mid" else 4
+    # inputs, stage outputs, which outputs are sliced (in slot order), which one is stored in FP64
+    spec = {"if4_mid": (2, 2, [0, 1], None), "if4_end": (4, 3, [1, 0, 2], 0), "strang_end": (1, 2, [1], 0),
+            "split4_mid": (2, 2, [1], 0), "split4_end": (2, 3, [1, 2], 0)}[prog]
+    nin, nout, sl_idx, fp_idx = spec
     ins = [(0.3 * torch.complex(torch.randn(shape, generator=g, dtype=torch.float64),
                                 torch.randn(shape, generator=g, dtype=torch.float64))).cuda() for _ in range(nin)]
     tau = 0.005
     n0, Q = shape[0], int(np.prod(shape[1:]))
     # reference: unfused stage, then the data slicing of each sliced output
-    outs = [torch.empty_like(ins[0]) for _ in range(2 if prog == "if4_mid" else 3)]
+    outs = [torch.empty_like(ins[0]) for _ in range(nout)]
     flag = _lib.new_flag(0)
     _lib.check(lib.cgl_stage(st, _lib.STAGE[prog], 1, n0 * Q, _lib.ctypes.byref(nl), tau, 1.0,
                              _lib.ptr_array(ins), _lib.ptr_array(outs), _lib.flag_ptr(flag), _lib.rel_pos(1)), "stage")
-    sliced = outs if prog == "if4_mid" else [outs[1], outs[0], outs[2]]  # END: X1, u, X5
+    sliced = [outs[j] for j in sl_idx]
     per = lib.cgl_oz_slice_bytes(ozaki.S, Q, n0, 0)
     ref = []
     for x in sliced:
@@ -409,15 +413,15 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
     got = [(torch.zeros(per, dtype=torch.int8, device="cuda"), torch.empty(Q, dtype=torch.int32, device="cuda"))
            for _ in sliced]
     _lib.check(lib.cgl_stage_slice(st, _lib.STAGE[prog], n0, Q, _lib.ctypes.byref(nl), tau, 1.0,
-                                   _lib.ptr_array(ins), _lib.ptr_array([u]) if prog == "if4_end" else None,
+                                   _lib.ptr_array(ins), _lib.ptr_array([u]) if fp_idx is not None else None,
                                    _lib.flag_ptr(flag2), _lib.rel_pos(1), _lib.ptr_array([t[0] for t in got]),
                                    _lib.ptr_array([t[1] for t in got])), "stage_slice")
     torch.cuda.synchronize()
     for (rb, re_), (gb, ge) in zip(ref, got):
         assert torch.equal(re_, ge)
         assert torch.equal(rb, gb)
-    if prog == "if4_end":
-        assert torch.equal(u, outs[0])
+    if fp_idx is not None:
+        assert torch.equal(u, outs[fp_idx])
     assert torch.equal(flag[:1], flag2[:1])
 
 
