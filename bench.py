@@ -273,7 +273,7 @@ def gemm_roofline(torch, w, scheme_fields=4):
             # dram__bytes_read.sum + dram__bytes_write.sum of one 4-field launch, ncu --set full
             # (profiles/r01_ozgemm_persistent_ncu_summary.txt; ncu flushes caches, so this is the
             # cold upper bound -- in the step the operands are L2-resident)
-            "traffic": 19.9e6, "traffic_unit": "bytes per launch",
+            "traffic": 15.7e6, "traffic_unit": "bytes per launch",
             "traffic_source": "profiles/r01_ozgemm_persistent_ncu_summary.txt (cold-cache ncu capture)",
             "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
                       "accumulators): 4-field axis-0 product of the if4 step, M=N=K=512 complex per field, "
