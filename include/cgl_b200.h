@@ -170,6 +170,17 @@ int cgl_oz_gemm_t(void* stream, int S, int64_t M, int64_t N, int64_t K, int nite
 int cgl_stage_slice(void* stream, int program, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl,
                     double tau, double in_scale, const double* const* in, double* const* out,
                     cgl_flag_t* flag, uint64_t pos, int8_t* const* slices, int* const* exps);
+/* Seeded inputs on the device (rng.py:21-64): uniforms start..start+count-1
+ * of stream `seed` (bit-identical to the host stream). */
+int cgl_uniforms(void* stream, uint64_t seed, uint64_t start, int64_t count, double* out);
+/* Seeded complex initial condition of a C-order shape (complex128 out):
+ * recipe 0 sech(r)(1 + 0.01 xi), 1 2 exp(-r^2/4)(1 + 0.01 xi), 2 0.1 xi,
+ * 3 xi; xi = xi_r + i xi_i with xi_r = normal_tensor(seed),
+ * xi_i = normal_tensor(seed + 1) (Fortran-order streams, Box-Muller on the
+ * device: a few ulp from numpy); r^2 from the per-axis coordinates axes[d]
+ * (recipes 0 and 1).  Replaces experiments.py's host IC construction. */
+int cgl_seeded_ic(void* stream, int recipe, uint64_t seed, int ndim, const int64_t* shape,
+                  const double* const* axes, double* out);
 /* Tile geometry of the emulated GEMM: A row tile, B row tile, K chunk bytes. */
 int cgl_oz_geometry(int* bm, int* bn, int* kc);
 /* Debug: with CGL_OZ_TRACE=1 in the environment, CTA 0 of the last

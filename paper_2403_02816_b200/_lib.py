@@ -91,6 +91,8 @@ _SIGS = {
     "cgl_oz_gemm_t": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                               c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64]),
     "cgl_oz_zmap": (c_int, [c_ptr, c_int, c_ptr, c_i64, c_i64, c_int, c_ptr]),
+    "cgl_uniforms": (c_int, [c_ptr, c_u64, c_u64, c_i64, c_ptr]),
+    "cgl_seeded_ic": (c_int, [c_ptr, c_int, c_u64, c_int, c_ptr, c_ptr, c_ptr]),
     "cgl_stage_slice": (c_int, [c_ptr, c_int, c_i64, c_i64, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr, c_u64, c_ptr,
                                 c_ptr]),
     "cgl_lincomb": (c_int, [c_ptr, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_u64]),

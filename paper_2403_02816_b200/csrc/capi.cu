@@ -41,6 +41,8 @@ int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
 int stage_launch(cudaStream_t, int, int, int64_t, const cgl_nonlinear_t*, double, double, const double* const*,
                  double* const*, cgl_flag_t*, uint64_t, int, const int64_t*, const double* const*, int64_t, int64_t);
+int rng_uniforms(cudaStream_t, uint64_t, uint64_t, int64_t, double*);
+int rng_seeded_ic(cudaStream_t, int, uint64_t, int, const int64_t*, const double* const*, double*);
 int stage_slice_launch(cudaStream_t, int, int64_t, int64_t, const cgl_nonlinear_t*, double, double,
                        const double* const*, double* const*, cgl_flag_t*, uint64_t, int8_t* const*, int* const*);
 
@@ -349,6 +351,17 @@ int cgl_stage_slice(void* stream, int program, int64_t n0, int64_t Q, const cgl_
   if (!nl || !in || !slices || !exps) return set_error(CGL_EINVAL, "cgl_stage_slice: null argument");
   return stage_slice_launch((cudaStream_t)stream, program, n0, Q, nl, tau, in_scale, in, out, flag, pos, slices,
                             exps);
+}
+
+int cgl_uniforms(void* stream, uint64_t seed, uint64_t start, int64_t count, double* out) {
+  if (count > 0 && !out) return set_error(CGL_EINVAL, "cgl_uniforms: null output");
+  return rng_uniforms((cudaStream_t)stream, seed, start, count, out);
+}
+
+int cgl_seeded_ic(void* stream, int recipe, uint64_t seed, int ndim, const int64_t* shape,
+                  const double* const* axes, double* out) {
+  if (!shape || !out) return set_error(CGL_EINVAL, "cgl_seeded_ic: null argument");
+  return rng_seeded_ic((cudaStream_t)stream, recipe, seed, ndim, shape, axes, out);
 }
 
 int cgl_oz_geometry(int* bm, int* bn, int* kc) {

@@ -124,12 +124,24 @@ def initial_state(w, seed=SEED):
     raise ValueError(w.ic)
 
 
+_IC_RECIPE = {"sech_noise": 0, "gauss_noise": 1, "random_phase": 2}
+
+
 def initial_state_device(w, seed=SEED):
-    """Device-built u0 (CUDA complex128) for large grids.  gaussians8 is
-    separable per Gaussian, so it is assembled from 1D factors on the GPU with
-    the same parameters as initial_state (no 17 GB host array); the noise
-    recipes fall back to the host generator (bit-compatible stream)."""
+    """Device-built u0 (CUDA complex128), no N-sized host array.  The noise
+    recipes run the seeded stream on the GPU (cgl_seeded_ic: uniforms
+    bit-identical to the host, Box-Muller normals within a few ulp);
+    gaussians8 is separable per Gaussian and assembled from 1D factors with
+    the same parameters as initial_state."""
     import torch
+    if w.ic in _IC_RECIPE:
+        from . import _lib
+        out = torch.empty(w.extents, dtype=torch.complex128, device="cuda")
+        ax = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in axes(w)]
+        _lib.check(_lib.load().cgl_seeded_ic(_lib.stream(), _IC_RECIPE[w.ic], seed, len(w.extents),
+                                             _lib.i64_array(w.extents), _lib.ptr_array(ax), _lib.ptr(out)),
+                   "cgl_seeded_ic")
+        return out
     if w.ic != "gaussians8":
         return torch.from_numpy(initial_state(w, seed)).cuda()
     a, b = w.interval
