@@ -943,6 +943,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     const int pw = warp == 0 ? 0 : warp - (1 + OZP_EPI_WARPS);
     const int64_t t_end = (a.debug & 4) ? 0 : total;  // debug 4: producers idle
     int it_n = 0, j = 0;
+    bool waited = false, stop = false;
     for (int64_t t = blockIdx.x; t < t_end; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
       const int tn = td.tn, tm = td.tm;
@@ -974,10 +975,6 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       } else {
         mbar_wait(&ti_full[slot], (j / Cfg::NTI) & 1);
       }
-      if (j == 0) {
-        pdl_wait();
-        if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) break;  // the issuer skips too
-      }
       const int8_t* A = it.A + b * a.sAb + (int64_t)tm * nch * S * Cfg::A_BYTES;
       const int8_t* B = it.B + b * a.sBb + (int64_t)tn * nch * S * Cfg::B_BYTES;
       const int n = (int)list[0];
@@ -989,28 +986,45 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
         const int itc = it_n + e;
         const int st = itc % STAGES;
         const uint32_t ph = (itc / STAGES) & 1;
+        const int na = S + 2 - zb - za;
+        uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + S * Cfg::A_BYTES;
+        // the constant factor slices (A) do not depend on earlier kernels: the
+        // first chunk's A copy is issued before griddepcontrol.wait
         if (lane == 0) {
           mbar_wait_sleep(&empty[st], ph ^ 1, 64);
           if (itc < 8) OZ_TRACE(44 + itc);
-          const int na = S + 2 - zb - za;
           if (a.debug & 2) {
             mbar_arrive(&full[st]);
           } else {
             mbar_expect_tx(&full[st], na * (Cfg::A_BYTES + Cfg::B_BYTES));
-            uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
-            uint8_t* sb = sa + S * Cfg::A_BYTES;
             bulk_g2s(sa + (za - 1) * Cfg::A_BYTES, A + ((int64_t)c * S + (za - 1)) * Cfg::A_BYTES,
                      na * Cfg::A_BYTES, &full[st]);
-            bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
-                     na * Cfg::B_BYTES, &full[st]);
           }
         }
+        bool skip = false;
+        if (!waited) {
+          pdl_wait();
+          waited = true;
+          skip = flag_skip(a.flag, resolve_pos(a.flag, a.pos));  // the issuer skips too
+        }
+        if (lane == 0 && !(a.debug & 2))
+          bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
+                   na * Cfg::B_BYTES, &full[st]);
         __syncwarp();
+        if (skip) {  // nobody consumes this stage: let its copies land before the CTA exits
+          if (lane == 0) mbar_wait(&full[st], ph);
+          __syncwarp();
+          stop = true;
+          break;
+        }
       }
+      if (stop) break;
       it_n += n;
       __syncwarp();
       if (pw != 0 && lane == 0) mbar_arrive(&ti_empty[slot]);
     }
+    if (!waited) pdl_wait();  // (no chunk issued) keep the PDL contract before exiting
   } else if (warp == 1) {
     // ---- MMA issuer: the whole warp runs the (warp-uniform) loop over the
     // tile's live-chunk list; one lane, elected once, issues every tcgen05
