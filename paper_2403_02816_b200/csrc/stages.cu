@@ -331,15 +331,22 @@ struct StageSliceArgs {
   int nchunks;
 };
 
+#ifndef SS_THREADS
+#define SS_THREADS 256
+#endif
+constexpr int kSSThreads = SS_THREADS;  // threads per CTA of the fused stage+slicing kernel
+constexpr int kSSParts = kSSThreads / 32;
+
 template <int PROG, int NSL, int CPBT>
-__global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A) {
+__global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSliceArgs A) {
   namespace cg = cooperative_groups;
   using oz::KC;
   using oz::NONFINITE;
   constexpr int CR = 32;                 // Z rows (columns q) per tile = the GEMM's B row tile
   constexpr int CC = KC / 2;             // complex K per chunk
   constexpr int W = CC * CPBT;           // complex K per CTA
-  constexpr int PT = CR * W / 256;       // points per thread
+  constexpr int PT = CR * W / kSSThreads;  // points per thread
+  static_assert(PT >= 1 && CR * W % kSSThreads == 0, "tile / CTA size");
   static_assert(kOzBN == CR, "B row tile");
   pdl_wait();
   const StageArgs& a = A.s;
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
   // ---- stage, pointwise (consecutive threads: consecutive q, coalesced) ----
 #pragma unroll 2
   for (int j = 0; j < PT; ++j) {
-    const int k = tid + 256 * j, rr = k % CR, cc = k / CR;
+    const int k = tid + kSSThreads * j, rr = k % CR, cc = k / CR;
     double2 o[NSL];
 #pragma unroll
     for (int q = 0; q < NSL; ++q) o[q] = make_double2(0.0, 0.0);
@@ -409,8 +416,8 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
   __syncthreads();
   pdl_trigger();
   // ---- partial exponents of the 32 Z rows per output, exchanged in the cluster ----
-  __shared__ double red[NSL][8][33];
-  __shared__ int redbad[NSL][8][32];
+  __shared__ double red[NSL][kSSParts][33];
+  __shared__ int redbad[NSL][kSSParts][32];
   __shared__ int epart[NSL][16][32];  // [output][cluster rank][row]
   __shared__ int erow[NSL][32];
   cg::cluster_group cluster = cg::this_cluster();
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
     for (int q = 0; q < NSL; ++q) {
       double m = 0.0;
       bool bad = false;
-      for (int cc = part; cc < cols_here; cc += 8) {
+      for (int cc = part; cc < cols_here; cc += kSSParts) {
         const double2 v = blk[(q * CR + rr) * (W + 1) + cc];
         bad |= !isfinite(v.x) || !isfinite(v.y);
         m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
@@ -434,7 +441,7 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
     const int q = tid >> 5, rr = tid & 31;
     double m = red[q][0][rr];
     int bad = redbad[q][0][rr];
-    for (int k = 1; k < 8; ++k) {
+    for (int k = 1; k < kSSParts; ++k) {
       m = fmax(m, red[q][k][rr]);
       bad |= redbad[q][k][rr];
     }
@@ -457,7 +464,7 @@ __global__ void __launch_bounds__(256) stage_slice_kernel(const StageSliceArgs A
   // ---- slices (same digits and layout as slice_tile_kernel<8, 0>) ----
   constexpr int NG = KC / 16, groups = CPBT * NG;
   const int ch0 = blockIdx.y * CPBT;
-  for (int w = tid; w < NSL * CR * groups; w += 256) {
+  for (int w = tid; w < NSL * CR * groups; w += kSSThreads) {
     const int q = w / (CR * groups), rem = w % (CR * groups);
     const int rr = rem % CR, gg = rem / CR;
     const int ch = ch0 + gg / NG, g = gg % NG;
@@ -499,7 +506,7 @@ static cudaError_t launch_stage_slice(const StageSliceArgs& A, cudaStream_t st) 
     attr = true;
   }
   const dim3 grid((unsigned)((A.Q + 31) / 32), (unsigned)cy, 1);
-  return launch_k(kern, grid, dim3(256), smem, st, dim3(1, (unsigned)cy, 1), A);
+  return launch_k(kern, grid, dim3(kSSThreads), smem, st, dim3(1, (unsigned)cy, 1), A);
 }
 
 int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const cgl_nonlinear_t* nl, double tau,
