@@ -48,19 +48,30 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force=False, verbose=False, csrc=CSRC, out=LIB):
+def build(force=False, verbose=False, csrc=CSRC, out=LIB, extra_flags=()):
     """Build `out` from the sources in `csrc` (defaults: the package library;
-    other values only for kernel A/B experiments, see tools/oz_bench.py)."""
+    other values only for kernel A/B experiments and the profiling build,
+    see tools/oz_bench.py and tools/timeline.py).  Translation units compile
+    in parallel."""
     if out == LIB and not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIB_DIR, exist_ok=True)
-    objs = []
     nvcc = nvcc_path()
-    for src in sources(csrc):
-        obj = os.path.join(LIB_DIR, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+    tag = os.path.basename(out)[:-3]
+
+    def compile_one(src):
+        obj = os.path.join(LIB_DIR, f"{tag}.{os.path.basename(src)[:-3]}.o")
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra_flags, "-I", os.path.join(ROOT, "include"), "-I", csrc,
                "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r
+
+    srcs = sources(csrc)
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs = []
+    for src, obj, r in results:
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode:

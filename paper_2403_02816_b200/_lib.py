@@ -65,7 +65,20 @@ class Nonlinear(ctypes.Structure):
                 ("beta4", c_dbl), ("alpha5", c_dbl), ("kind", c_int)]
 
 
+class OzPrologue(ctypes.Structure):
+    """cgl_oz_prologue_t (include/cgl_b200.h): the producer phase of cgl_oz_gemm_fused."""
+    _fields_ = [("program", c_int), ("nitems", c_int), ("src", c_ptr), ("out", c_ptr), ("slices", c_ptr),
+                ("exps", c_ptr), ("rows", c_i64), ("K", c_i64), ("sr", c_i64), ("sk", c_i64), ("batch", c_i64),
+                ("src_bs", c_i64), ("out_bs", c_i64), ("exp_bs", c_i64), ("nl", c_ptr), ("tau", c_dbl),
+                ("in_scale", c_dbl), ("flag", c_ptr), ("pos", c_u64), ("grid_barrier", c_ptr)]
+
+
+PRO_SLICE = -1
+
 _SIGS = {
+    "cgl_oz_gemm_fused": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                                  c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64, c_int,
+                                  ctypes.POINTER(OzPrologue)]),
     "cgl_version": (ctypes.c_char_p, []),
     "cgl_last_error": (ctypes.c_char_p, []),
     "cgl_abi_version": (c_int, []),
@@ -87,6 +100,7 @@ _SIGS = {
     "cgl_oz_slice_multi": (c_int, [c_ptr, c_int, c_int, c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int,
                                    c_ptr, c_i64, c_ptr, c_i64]),
     "cgl_oz_trace": (c_int, [c_ptr]),
+    "cgl_prof_set": (c_int, [c_ptr, c_ptr, ctypes.c_uint]),
     "cgl_oz_geometry": (c_int, [ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "cgl_oz_gemm_t": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                               c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64]),

@@ -12,16 +12,21 @@
 
 namespace cgl {
 
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+// Complex helpers with an explicit rounding structure: every multiply-add is
+// either a written fma() or a non-contractible __dmul_rn/__dadd_rn pair, so
+// the same expression gives the same bits in every kernel it is inlined
+// into (the fused stage+slicing kernels are bit-identical to stage_kernel +
+// slicing; compiler FMA contraction would otherwise depend on the context).
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(__dmul_rn(s, a.x), __dmul_rn(s, a.y)); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(fma(a.x, b.x, -__dmul_rn(a.y, b.y)), fma(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ double2 caxpy(double s, double2 x, double2 y) {  // s*x + y
   return make_double2(fma(s, x.x, y.x), fma(s, x.y, y.y));
 }
-__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, __dmul_rn(a.y, a.y)); }
 __device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
 // exp(z) for complex z
 __device__ __forceinline__ double2 cexp(double2 z) {
@@ -77,6 +82,77 @@ __device__ __forceinline__ void flag_raise_warp(cgl_flag_t* f, uint64_t pos, boo
   unsigned m = __ballot_sync(0xffffffffu, bad);
   if (m && (threadIdx.x & 31) == (__ffs(m) - 1)) flag_raise(f, pos, reason);
 }
+
+// ---------------------------------------------------------------------------
+// In-graph timeline profiling (profiling builds only: -DCGL_PROF, see
+// tools/timeline.py).  Every warp of an instrumented kernel appends one
+// record {kernel id, block, warp, start, end} (globaltimer ns) when it
+// leaves the kernel, so per-launch spans, PDL overlap and per-role warp
+// times are visible inside a replayed CUDA graph.  Each translation unit
+// holds its own copy of the buffer pointer; cgl_prof_set() fills them all.
+// ---------------------------------------------------------------------------
+struct CglProfRec {
+  long long t0, t1;
+  int kid, blk;
+  int warp, pad;
+};
+#ifdef CGL_PROF
+static __device__ CglProfRec* g_prof_buf = nullptr;
+static __device__ unsigned long long* g_prof_n = nullptr;
+static __device__ unsigned g_prof_cap = 0;
+struct ProfScope {
+  long long t0;
+  int kid;
+  __device__ __forceinline__ explicit ProfScope(int k) : kid(k) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  }
+  __device__ __forceinline__ ~ProfScope() { mark(kid); }
+  // one record {t0 = warp start, t1 = now} under id k (lane 0 of the calling warp)
+  __device__ __forceinline__ void mark(int k) const {
+    if ((threadIdx.x & 31) == 0 && g_prof_buf != nullptr) {
+      long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      sm &= 255u;
+      // per-SM counters and buffer regions: no cross-SM atomic contention
+      const unsigned per = g_prof_cap / 256u;
+      const unsigned long long s = atomicAdd(g_prof_n + sm, 1ull);
+      if (s < per) {
+        CglProfRec r;
+        r.t0 = t0;
+        r.t1 = t1;
+        r.kid = k;
+        r.blk = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+        r.warp = (int)(threadIdx.x >> 5);
+        r.pad = 0;
+        g_prof_buf[(unsigned long long)sm * per + s] = r;
+      }
+    }
+  }
+};
+#define CGL_PROF_SCOPE(k) ::cgl::ProfScope cgl_prof_scope_(k)
+#define CGL_PROF_MARK(k) cgl_prof_scope_.mark(k)
+#define CGL_PROF_TU(name)                                                                    \
+  int cgl_prof_set_##name(void* buf, void* n, unsigned cap) {                                \
+    CglProfRec* b = static_cast<CglProfRec*>(buf);                                           \
+    unsigned long long* c = static_cast<unsigned long long*>(n);                             \
+    if (cudaMemcpyToSymbol(g_prof_buf, &b, sizeof(b)) != cudaSuccess) return -1;             \
+    if (cudaMemcpyToSymbol(g_prof_n, &c, sizeof(c)) != cudaSuccess) return -1;               \
+    if (cudaMemcpyToSymbol(g_prof_cap, &cap, sizeof(cap)) != cudaSuccess) return -1;         \
+    return 0;                                                                                \
+  }
+#else
+#define CGL_PROF_SCOPE(k) ((void)0)
+#define CGL_PROF_MARK(k) ((void)0)
+#define CGL_PROF_TU(name) \
+  int cgl_prof_set_##name(void*, void*, unsigned) { return -1; }
+#endif
+// kernel ids (tools/timeline.py)
+enum ProfKid {
+  KID_SLICE = 1, KID_OZP = 2, KID_STAGE = 3, KID_STAGE_SLICE = 4, KID_FLAG_ADV = 5, KID_SEPARABLE = 6,
+  KID_ZGEMM = 7, KID_OZ = 8, KID_ROWEXP = 9, KID_ZMAP = 10, KID_LINCOMB = 11, KID_POINTWISE = 12
+};
 
 inline int grid_for(int64_t n, int threads, int per_thread = 1) {
   int64_t b = (n + (int64_t)threads * per_thread - 1) / ((int64_t)threads * per_thread);

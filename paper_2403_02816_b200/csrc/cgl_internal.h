@@ -43,6 +43,14 @@ struct GemmArgs {
 
 int zgemm_launch(const GemmArgs& a, int nitems, cudaStream_t s);
 
+// full-K data slicing (stages.cu): rows x K complex operand, element (r, k) at
+// src[r * sr + k * sk]; same slices/exponents as the B-mode floor-digit slicing
+bool rows_slice_ok(int64_t K, bool stage);
+int rows_slice_qc(int64_t K, int64_t rows_total, int tpt_max, int* tpt);
+int rows_slice_plain(cudaStream_t st, int nitems, const double* const* srcs, int64_t sr, int64_t sk, int64_t rows,
+                     int64_t K, int64_t batch, int64_t src_bs, int8_t* const* outs, int64_t out_bs,
+                     int* const* exps, int64_t exp_bs);
+
 // error plumbing (capi.cu)
 // Launch with the programmatic-dependent-launch attribute (CGL_PDL=0
 // disables) and an optional thread-block cluster shape.  Every kernel

@@ -44,6 +44,7 @@
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
 #include "oz_slice.cuh"
+#include "rows_slice.cuh"
 
 namespace cgl {
 namespace oz {
@@ -270,6 +271,7 @@ struct SliceArgs {
 // max); exps must be pre-set to a very negative value (0x80 bytes).
 __global__ void rowexp_rows_kernel(const SliceArgs a, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
                                    int64_t src_bs, int64_t exp_bs, int64_t cspan) {
+  CGL_PROF_SCOPE(KID_ROWEXP);
   __shared__ double red[8][33];
   const int64_t b = blockIdx.z % batch;
   const int item = (int)(blockIdx.z / batch);
@@ -283,8 +285,10 @@ __global__ void rowexp_rows_kernel(const SliceArgs a, int64_t sc, int64_t rows, 
 #pragma unroll 4
     for (int64_t c = c0 + ty; c < c1; c += 8) {
       const double2 v = z[r + c * sc];
+      // fmax drops a NaN operand: test both parts explicitly so a NaN sticks
+      const bool nan_v = v.x != v.x || v.y != v.y;
       const double av = fmax(fabs(v.x), fabs(v.y));
-      m = (av != av || m != m) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, av);  // NaN sticks
+      m = (nan_v || m != m) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(m, av);
     }
   }
   red[ty][tx] = m;
@@ -309,6 +313,7 @@ __global__ void rowexp_rows_kernel(const SliceArgs a, int64_t sc, int64_t rows, 
 // K-contiguous rows: warp per row
 __global__ void rowexp_kernel(const SliceArgs a, int64_t sr, int64_t sc, int64_t rows, int64_t cols, int64_t batch,
                               int64_t src_bs, int64_t exp_bs) {
+  CGL_PROF_SCOPE(KID_ROWEXP);
   const int64_t b = blockIdx.y % batch;
   const int item = (int)(blockIdx.y / batch);
   const double2* z = a.srcs[item] + b * src_bs;
@@ -385,6 +390,7 @@ __device__ __forceinline__ void digits8_floor(double x, int e, uint32_t (&w)[8][
 template <int S, int AMODE, int CPBT = CPB, bool FUSED = false>
 __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int64_t src_bs, int64_t out_bs,
                                                          int64_t exp_bs) {
+  CGL_PROF_SCOPE(KID_SLICE);
   constexpr int CC = KC / 2;              // complex columns per chunk
   constexpr int W = CC * CPBT;            // complex columns per CTA
   constexpr int RT = AMODE ? BM : kOzBN;  // real rows per tile
@@ -399,6 +405,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
   const int tid = threadIdx.x;
   const int rows_here = (int)min((int64_t)CR, a.rows - r0), cols_here = (int)min((int64_t)W, a.cols - c0);
   if constexpr (FUSED) pdl_wait();  // launched with launch_k: the data come from the previous kernel
+  CGL_PROF_MARK(301);
   // all CR*W/256 loads of a thread are issued before any store to smem (the
   // kernel runs as ~one wave: memory-level parallelism decides its speed)
   static_assert((CR * W) % 256 == 0, "staging tile must be a multiple of the CTA size");
@@ -430,6 +437,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
     }
   }
   __syncthreads();
+  CGL_PROF_MARK(302);
   if constexpr (FUSED) pdl_trigger();  // inputs staged: the GEMM may start its prologue
   int8_t* outb = a.outs[item] + b * out_bs;
   const int* exps = a.expss[item] + b * exp_bs + r0;
@@ -471,6 +479,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
       for (unsigned rk = 0; rk < nb; ++rk) cluster.map_shared_rank(&epart[0][0], rk)[me * 32 + tid] = e;
     }
     cluster.sync();
+    CGL_PROF_MARK(303);
     if (tid < 32) {
       int e = INT_MIN;
       for (unsigned rk = 0; rk < cluster.num_blocks(); ++rk) e = max(e, epart[rk][tid]);
@@ -542,6 +551,7 @@ __global__ void __launch_bounds__(256) slice_tile_kernel(const SliceArgs a, int6
 // slices vanish first; the GEMM skips those loads and MMAs exactly.
 __global__ void zmap_kernel(const int8_t* sl, int S, int64_t slice_stride, int nchunks, int RT, int64_t nblocks,
                             int8_t* z) {
+  CGL_PROF_SCOPE(KID_ZMAP);
   const int64_t blk = blockIdx.x;  // = rt * nchunks + chunk
   if (blk >= nblocks) return;
   const int bytes = RT * KC;
@@ -586,6 +596,12 @@ struct OzArgs {
   long long* trace;  // optional: CTA 0 phase timestamps (globaltimer ns), see OZ_TRACE
   int debug;         // CGL_OZ_DEBUG (timing experiments only; results invalid): 1 skip MMAs, 2 skip copies
   OzItem items[kMaxItems];
+  // fused prologue (ozgemm_persistent_kernel<..., PRO != 0>): the data slicing
+  // (or stage program + slicing) that produces this GEMM's B operands, run by
+  // the epilogue warps as virtual 128-thread CTAs before one grid barrier
+  RowsSliceArgs pro;
+  int64_t pro_nvbx, pro_nvb;  // virtual CTAs: row blocks x (items x batch)
+  unsigned* gbar;             // grid barrier {count, generation}, zeroed once
 };
 
 __device__ __forceinline__ long long gtime() {
@@ -614,6 +630,7 @@ constexpr int OZ_THREADS = 320;  // warp 0 producer, warp 1 MMA issuer, warps 2-
 
 template <int S, int BN, int STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_kernel(const OzArgs a) {
+  CGL_PROF_SCOPE(KID_OZ);
   using Cfg = OzCfg<S, BN, STAGES>;
   if (flag_skip(a.flag, resolve_pos(a.flag, a.pos))) return;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -823,6 +840,29 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
 }
 
 
+// Grid-wide barrier of a persistent launch (every CTA resident: one per SM).
+// bar[0] counts arrivals (reset by the last arriver), bar[1] is the
+// generation the waiters watch.  Generic writes before the barrier are made
+// visible to the async proxy (cp.async.bulk operand loads) after it.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
 // ---- persistent variant -------------------------------------------------------
 // One CTA per SM walks tiles t = blockIdx.x, +gridDim.x, ...; the S level
 // accumulators are double-buffered in TMEM (2 x S x BN <= 512 columns) so the
@@ -871,8 +911,9 @@ __device__ __forceinline__ TileId decode_tile(const OzArgs& a, uint32_t t) {
   return d;
 }
 
-template <int S, int BN, int STAGES>
+template <int S, int BN, int STAGES, int PRO = 0, int PTPT = 1>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const OzArgs a, int64_t total) {
+  CGL_PROF_SCOPE(KID_OZP);
   using Cfg = OzPCfg<S, BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* stage_base = smem;
@@ -926,6 +967,30 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) OZ_TRACE(1);
+  if (warp == 0) CGL_PROF_MARK(101);  // setup done
+  if constexpr (PRO != 0) {
+    // ---- prologue phase: this GEMM's B operands (data slicing, optionally a
+    // stage program) by the 16 epilogue warps as four 128-thread groups, the
+    // smem ring as their scratch; then one grid barrier ----
+    constexpr int PNSL = PRO == P_SLICE ? 1 : (PRO == P_IF4_END ? 3 : ((PRO == P_IF4_MID || PRO == P_SPLIT4_END) ? 2 : 1));
+    static_assert(OZP_EPI_WARPS == 16 && Cfg::BODY >= 4 * (int)sizeof(RowsSliceSmem), "prologue groups");
+    pdl_wait();
+    if (warp == 0) CGL_PROF_MARK(110);  // pdl wait passed
+    if (warp >= 2 && warp < 2 + OZP_EPI_WARPS) {
+      const int g = (warp - 2) >> 2;
+      RowsSliceSmem* psm = reinterpret_cast<RowsSliceSmem*>(stage_base) + g;
+      int round = 0;
+      for (int64_t vb = g + 4 * (int64_t)blockIdx.x; vb < a.pro_nvb; vb += 4 * (int64_t)gridDim.x, ++round) {
+        if (!rows_slice_block<PRO, PNSL, PTPT>(a.pro, vb % a.pro_nvbx, vb / a.pro_nvbx, threadIdx.x - 64 - 128 * g,
+                                               1 + g, *psm))
+          break;
+        if (round < 2) CGL_PROF_MARK(111 + round);  // virtual CTA done
+      }
+      CGL_PROF_MARK(113);  // prologue work done (before the grid barrier)
+    }
+    grid_barrier(a.gbar);
+    if (warp == 0) CGL_PROF_MARK(102);  // prologue + grid barrier done
+  }
   // Everything above and the first tile's live-chunk list (constant zero maps)
   // overlap the previous kernel's tail under PDL; every role executes
   // griddepcontrol.wait before touching the data operand, its exponents or
@@ -1025,6 +1090,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       if (pw != 0 && lane == 0) mbar_arrive(&ti_empty[slot]);
     }
     if (!waited) pdl_wait();  // (no chunk issued) keep the PDL contract before exiting
+    CGL_PROF_MARK(106);  // producer loop done
   } else if (warp == 1) {
     // ---- MMA issuer: the whole warp runs the (warp-uniform) loop over the
     // tile's live-chunk list; one lane, elected once, issues every tcgen05
@@ -1051,6 +1117,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
         const int st = it_n % STAGES;
         const uint32_t ph = (it_n / STAGES) & 1;
         mbar_wait(&full[st], ph);  // TMA writes -> MMA reads: ordered by complete_tx
+        if (it_n == 0) CGL_PROF_MARK(103);  // first data ready
         if (lane == 0 && it_n < 8) OZ_TRACE(52 + it_n);
         if (!(a.debug & 1)) {
           const uint8_t* sa = stage_base + st * Cfg::STAGE_BYTES;
@@ -1094,6 +1161,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       if (lane == 0 && j < 8) OZ_TRACE(11 + j);
       if (lane == 0 && j == 0 && a.trace && blockIdx.x == 0) a.trace[63] = it_n;  // chunks of tile 0
     }
+    CGL_PROF_MARK(104);  // all MMAs issued
     pdl_trigger();  // all MMAs issued: only this CTA's epilogue tail remains
   } else if (warp >= 2) {
     // ---- epilogue (OZP_EPI warps per TMEM lane quadrant, HC columns each) ----
@@ -1117,7 +1185,9 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       const int64_t i = R >> 1;
       const int ea = (i < a.M) ? __ldg(it.Ae + b * a.sAeb + i) : 0;
       const int64_t ccol = (int64_t)tn * BN + lane;
-      const int eb_lane = (lane < BN && ccol < a.N) ? __ldg(it.Be + b * a.sBeb + ccol) : 0;
+      // (the prologue wrote Be in this launch: coherent L2 load)
+      const int eb_lane = (lane < BN && ccol < a.N) ? (PRO != 0 ? __ldcg(it.Be + b * a.sBeb + ccol)
+                                                                  : __ldg(it.Be + b * a.sBeb + ccol)) : 0;
       mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1, 32);
       tc_fence_after();
       if (j < 8 && threadIdx.x == 64) OZ_TRACE(19 + j);
@@ -1193,6 +1263,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       }
       if (j < 8 && threadIdx.x == 64) OZ_TRACE(27 + j);
     }
+    CGL_PROF_MARK(105);  // epilogue done
   }
   pdl_trigger();
   tc_fence_before();
@@ -1237,10 +1308,16 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   a.floor_digits = floor_digits;
   const int64_t zdim = batch * nitems;
   if (zdim > 65535) return set_error(CGL_ESHAPE, "oz_slice: batch x items too large");
-  static const bool fuse_ok = [] {
-    const char* e = getenv("CGL_OZ_FUSED_SLICE");
-    return !(e && e[0] == '0');
-  }();
+  // variants for A/B runs and tests: CGL_SS_CLUSTER=1 (cluster kernel),
+  // CGL_OZ_FUSED_SLICE=0 (two-pass rowexp + slice_tile)
+  const char* ev_fused = getenv("CGL_OZ_FUSED_SLICE");
+  const char* ev_cluster = getenv("CGL_SS_CLUSTER");
+  const bool fuse_ok = !(ev_fused && ev_fused[0] == '0');
+  const bool rows_ok = fuse_ok && !(ev_cluster && ev_cluster[0] == '1');
+  if (rows_ok && !a_mode && floor_digits && S == 8 && (sr == 1 || sc == 1) && rows_slice_ok(cols, false)) {
+    // full-K CTAs, no cluster (stages.cu rows_slice_kernel); row r of Z = operand row, K = cols
+    return rows_slice_plain(st, nitems, srcs, sr, sc, rows, cols, batch, src_bs, outs, out_bs, exps, exp_bs);
+  }
   if (fuse_ok && !a_mode && floor_digits && S == 8 && a.nchunks <= 64) {
     // one cluster of <= 8 CTAs per row tile covers all K chunks
     const int cpb = a.nchunks <= 32 ? 4 : 8;
@@ -1328,10 +1405,10 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
   return check_launch("ozgemm_kernel");
 }
 
-template <int S, int BN, int STAGES>
+template <int S, int BN, int STAGES, int PRO = 0, int PTPT = 1>
 static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
   using Cfg = oz::OzPCfg<S, BN, STAGES>;
-  auto kern = oz::ozgemm_persistent_kernel<S, BN, STAGES>;
+  auto kern = oz::ozgemm_persistent_kernel<S, BN, STAGES, PRO, PTPT>;
   static int nsm = 0;
   if (!nsm) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1350,13 +1427,14 @@ static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
   return check_launch("ozgemm_persistent_kernel");
 }
 
-int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-            const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
-            const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
-            int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos, int trans_c) {
+static int oz_args(oz::OzArgs& a, cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
+                   const int8_t* const* A, const int* const* Ae, const int8_t* const* Az, const int8_t* const* B,
+                   const int* const* Be, const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch,
+                   int64_t sAb, int64_t sAeb, int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag,
+                   uint64_t pos, int trans_c) {
   constexpr int BN = kOzBN;
+  (void)S;
   if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "oz_gemm: 1..8 items");
-  oz::OzArgs a{};
   a.M = M;
   a.N = N;
   a.mtiles = (int)((2 * M + oz::BM - 1) / oz::BM);
@@ -1389,6 +1467,18 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   for (int f = 0; f < nitems; ++f)
     a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
                             Bz ? Bz[f] : nullptr};
+  return 0;
+}
+
+int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+            const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
+            const int8_t* const* Bz, double* const* C, int64_t ldc, int64_t batch, int64_t sAb, int64_t sAeb,
+            int64_t sBb, int64_t sBeb, int64_t sCb, const cgl_flag_t* flag, uint64_t pos, int trans_c) {
+  constexpr int BN = kOzBN;
+  oz::OzArgs a{};
+  int r = oz_args(a, st, S, M, N, K, nitems, A, Ae, Az, B, Be, Bz, C, ldc, batch, sAb, sAeb, sBb, sBeb, sCb, flag,
+                  pos, trans_c);
+  if (r) return r;
   static const int persistent = [] {
     const char* e = getenv("CGL_OZ_PERSISTENT");
     return e ? atoi(e) : 1;
@@ -1401,6 +1491,103 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
     case 1: return oz_launch_cfg<1, BN, 2>(a, nitems, st);
     default: return set_error(CGL_EINVAL, "oz_gemm: S must be 1, 7 or 8");
   }
+}
+
+// GEMM with its B operands produced in-kernel (prologue phase + grid
+// barrier): pro describes the slicing (PRO = P_SLICE: pro.batch x nitems
+// sources) or the stage program whose sliced outputs are the B operands.
+int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+                  const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
+                  double* const* C, int64_t ldc, int64_t batch, int64_t sBb, int64_t sBeb, int64_t sCb,
+                  const cgl_flag_t* flag, uint64_t pos, int trans_c, const RowsSliceArgs& pro, int prog,
+                  int pro_items, unsigned* gbar) {
+  constexpr int BN = kOzBN;
+  if (S != 8) return set_error(CGL_EINVAL, "oz_gemm_fused: S = 8 only");
+  if (!gbar) return set_error(CGL_EINVAL, "oz_gemm_fused: grid barrier buffer required");
+  oz::OzArgs a{};
+  int r = oz_args(a, st, S, M, N, K, nitems, A, Ae, Az, B, Be, nullptr, C, ldc, batch, 0, 0, sBb, sBeb, sCb, flag,
+                  pos, trans_c);
+  if (r) return r;
+  if (a.nchunks > oz::OzPCfg<8, BN, 4>::KMAXCH) return set_error(CGL_ESHAPE, "oz_gemm_fused: K too large");
+  a.pro = pro;
+  const int64_t gy = prog == P_SLICE ? pro.batch * pro_items : 1;
+  int tpt = 1;
+  a.pro.QC = rows_slice_qc(pro.K, pro.rows * gy, 2, &tpt);
+  if (tpt > 2) return set_error(CGL_ESHAPE, "oz_gemm_fused: prologue K extent too large");
+  a.pro_nvbx = (pro.rows + a.pro.QC - 1) / a.pro.QC;
+  a.pro_nvb = a.pro_nvbx * gy;
+  a.gbar = gbar;
+#define OZF(P_) (tpt == 1 ? oz_launch_persistent<8, BN, 4, P_, 1>(a, nitems, st) \
+                          : oz_launch_persistent<8, BN, 4, P_, 2>(a, nitems, st))
+  switch (prog) {
+    case P_SLICE: return OZF(P_SLICE);
+    case P_IF4_MID: return OZF(P_IF4_MID);
+    case P_IF4_END: return OZF(P_IF4_END);
+    case P_STRANG_END: return OZF(P_STRANG_END);
+    case P_SPLIT4_MID: return OZF(P_SPLIT4_MID);
+    case P_SPLIT4_END: return OZF(P_SPLIT4_END);
+    default: return set_error(CGL_EINVAL, "oz_gemm_fused: unknown prologue program");
+  }
+#undef OZF
+}
+
+int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
+                  const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
+                  double* const* C, int64_t ldc, int64_t batch, int64_t sBb, int64_t sBeb, int64_t sCb,
+                  const cgl_flag_t* flag, uint64_t pos, int trans_c, const cgl_oz_prologue_t* p) {
+  if (!p) return set_error(CGL_EINVAL, "oz_gemm_fused: prologue required");
+  RowsSliceArgs R{};
+  int prog, items = 1;
+  if (p->program == CGL_PRO_SLICE) {
+    prog = P_SLICE;
+    items = p->nitems;
+    if (items < 1 || items > 8) return set_error(CGL_EINVAL, "oz_gemm_fused: 1..8 slicing sources");
+    for (int f = 0; f < items; ++f) {
+      R.srcs[f] = reinterpret_cast<const double2*>(p->src[f]);
+      R.slices[f] = p->slices[f];
+      R.exps[f] = p->exps[f];
+    }
+    R.batch = p->batch;
+    R.src_bs = p->src_bs;
+    R.out_bs = p->out_bs;
+    R.exp_bs = p->exp_bs;
+  } else {
+    int nin, nsl, nout;
+    switch (p->program) {
+      case P_IF4_MID: nin = 2; nsl = 2; nout = 0; break;
+      case P_IF4_END: nin = 4; nsl = 3; nout = 1; break;
+      case P_STRANG_END: nin = 1; nsl = 1; nout = 1; break;
+      case P_SPLIT4_MID: nin = 2; nsl = 1; nout = 1; break;
+      case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
+      default: return set_error(CGL_EINVAL, "oz_gemm_fused: stage program must be if4 MID/END, strang END, split4 MID/END");
+    }
+    if (!p->nl || p->nl->kind == 2) return set_error(CGL_EINVAL, "oz_gemm_fused: single-component nonlinearity required");
+    if (nout && (!p->out || !p->out[0])) return set_error(CGL_EINVAL, "oz_gemm_fused: program writes an FP64 output");
+    prog = p->program;
+    StageArgs& a = R.s;
+    for (int k = 0; k < nin; ++k) a.in[k] = reinterpret_cast<const double2*>(p->src[k]);
+    if (nout) a.out[0] = reinterpret_cast<double2*>(p->out[0]);
+    a.n = p->rows * p->K;
+    a.tau = p->tau;
+    a.in_scale = p->in_scale;
+    a.nl = StageNL{p->nl->alpha3, p->nl->beta3, p->nl->alpha4, p->nl->beta4, p->nl->alpha5, p->nl->kind};
+    a.flag = p->flag;
+    a.pos = p->pos;
+    a.fw = 1;
+    for (int q = 0; q < nsl; ++q) {
+      R.slices[q] = p->slices[q];
+      R.exps[q] = p->exps[q];
+    }
+    R.batch = 1;
+  }
+  R.rows = p->rows;
+  R.K = p->K;
+  R.sr = p->sr;
+  R.sk = p->sk;
+  R.nchunks = (int)((2 * p->K + oz::KC - 1) / oz::KC);
+  if (R.nchunks != (int)((2 * K + oz::KC - 1) / oz::KC)) return set_error(CGL_ESHAPE, "oz_gemm_fused: prologue K != GEMM K");
+  return oz_gemm_fused(st, S, M, N, K, nitems, A, Ae, Az, B, Be, C, ldc, batch, sBb, sBeb, sCb, flag, pos, trans_c, R,
+                       prog, items, p->grid_barrier);
 }
 
 int oz_zmap(cudaStream_t st, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int RT, int8_t* z) {
@@ -1417,5 +1604,7 @@ int64_t oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode, int RT) {
   const int64_t rtiles = ((a_mode ? 2 * rows : rows) + RT - 1) / RT;
   return (int64_t)S * rtiles * nchunks * RT * oz::KC;
 }
+
+CGL_PROF_TU(ozgemm)
 
 }  // namespace cgl

@@ -55,6 +55,7 @@ struct LinArgs {
 };
 
 __global__ void lincomb_kernel(int64_t n, LinArgs a, double2* out, const cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_LINCOMB);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -67,6 +68,7 @@ __global__ void lincomb_kernel(int64_t n, LinArgs a, double2* out, const cgl_fla
 template <int NF>
 __global__ void eval_g_kernel(int64_t n, NL p, const double2* in0, const double2* in1, double s,
                               double2* out0, double2* out1, const cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_POINTWISE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -84,6 +86,7 @@ __global__ void eval_g_kernel(int64_t n, NL p, const double2* in0, const double2
 template <int Q>
 __global__ void exact_flow_kernel(int64_t n, double t, double a, double b, const double2* in, double s,
                                   double2* out, cgl_flag_t* flag, uint64_t pos, unsigned r_blow, unsigned r_nonfinite) {
+  CGL_PROF_SCOPE(KID_POINTWISE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool blow = false, bad = false;
@@ -115,6 +118,7 @@ __global__ void exact_flow_kernel(int64_t n, double t, double a, double b, const
 template <int NF>
 __global__ void rk4_flow_kernel(int64_t n, double t, NL p, const double2* in0, const double2* in1, double s,
                                 double2* out0, double2* out1, cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_POINTWISE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool bad = false;
@@ -147,6 +151,7 @@ __global__ void rk4_flow_kernel(int64_t n, double t, NL p, const double2* in0, c
 struct FinArgs { const double2* x[4]; int nf; };
 
 __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_POINTWISE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   bool bad = false;
@@ -157,12 +162,14 @@ __global__ void check_finite_kernel(int64_t n, FinArgs a, cgl_flag_t* flag, uint
 
 __global__ void flag_reset_kernel(cgl_flag_t* f) { f->key = ~0ull; }
 __global__ void flag_advance_kernel(cgl_flag_t* f, unsigned long long n) {
+  CGL_PROF_SCOPE(KID_FLAG_ADV);
   pdl_wait();
   f->step += n;
   pdl_trigger();
 }
 
 __global__ void mul_kernel(int64_t n, const double2* f, const double2* in, double2* out, const cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_POINTWISE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -186,6 +193,7 @@ struct SepArgs {
 // out[j] = s * prod_mu tab_mu[j_mu] * in[j] (C order: last axis fastest)
 __global__ void separable_kernel(int64_t n, SepArgs a, double s, const double2* in, double2* out,
                                  const cgl_flag_t* flag, uint64_t pos) {
+  CGL_PROF_SCOPE(KID_SEPARABLE);
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -315,5 +323,7 @@ int pw_separable(cudaStream_t st, int nd, const int64_t* shape, const double* co
                                                                reinterpret_cast<double2*>(out), flag, pos);
   return check_launch("separable_mul");
 }
+
+CGL_PROF_TU(pointwise)
 
 }  // namespace cgl

@@ -1,0 +1,175 @@
+// Pointwise stage building blocks shared by the stage kernels (stages.cu)
+// and the stage / slicing prologues of the fused GEMM (ozgemm.cu):
+// nonlinearity g, exact cubic and RK4 flows with the reference's divergence
+// positions (flows.py:62-133), stage-combination helpers, the stage program
+// ids.  See stages.cu for the per-scheme programs.
+#pragma once
+#include <cstdint>
+
+#include "cgl_common.cuh"
+
+namespace cgl {
+
+constexpr int kStageThreads = 256;
+
+struct StageNL {
+  double a3, b3, a4, b4, a5;
+  int kind;  // 0 cubic (exact flow), 1 cubic_quintic, 2 coupled
+};
+
+template <int NF>
+struct V {
+  double2 c[NF];
+};
+
+template <int NF>
+__device__ __forceinline__ V<NF> load(const double2* const* p, int base, int64_t i, double s) {
+  V<NF> v;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) v.c[c] = cscale(s, ld2(p[base + c] + i));
+  return v;
+}
+template <int NF>
+__device__ __forceinline__ void store(double2* const* p, int base, int64_t i, const V<NF>& v) {
+#pragma unroll
+  for (int c = 0; c < NF; ++c) p[base + c][i] = v.c[c];
+}
+template <int NF>
+__device__ __forceinline__ V<NF> axpy(double s, const V<NF>& x, const V<NF>& y) {  // s*x + y
+  V<NF> r;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) r.c[c] = caxpy(s, x.c[c], y.c[c]);
+  return r;
+}
+
+template <int NF>
+__device__ __forceinline__ V<NF> gfun(const StageNL& p, const V<NF>& u) {
+  double m[NF];
+#pragma unroll
+  for (int c = 0; c < NF; ++c) m[c] = cabs2(u.c[c]);
+  V<NF> g;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) {
+    double2 r = cmul(make_double2(p.a3 * m[c], p.b3 * m[c]), u.c[c]);
+    if (p.kind != 0) r = cadd(r, cmul(make_double2(p.a4 * (m[c] * m[c]), p.b4 * (m[c] * m[c])), u.c[c]));
+    if (p.kind == 2 && NF == 2) r = cadd(r, cscale(p.a5 * m[1 - c], u.c[c]));
+    g.c[c] = r;
+  }
+  return g;
+}
+
+__device__ __forceinline__ void note(uint64_t& key, uint64_t pos, unsigned reason) {
+  const uint64_t k = pos | reason;
+  if (k < key) key = k;
+}
+
+// exact cubic flow (flows.py:87-100) of one component at position pos
+__device__ __forceinline__ double2 cubic_exact(const StageNL& p, double2 u, double t, uint64_t pos, uint64_t& key) {
+  const double m = cabs2(u);
+  if (fabs(p.a3) < 1e-14) {
+    double sn, cs;
+    sincos(p.b3 * m * t, &sn, &cs);
+    return cmul(u, make_double2(cs, sn));
+  }
+  const double y = 2.0 * p.a3 * m * t;
+  if (y >= 1.0) note(key, pos, CGL_BLOWUP_CUBIC);
+  const double L = log1p(-y);
+  const double2 v = cmul(u, cexp(make_double2(-0.5 * L, (-p.b3 / (2.0 * p.a3)) * L)));
+  if (!cfinite(v)) note(key, pos, CGL_NONFINITE_CUBIC);
+  return v;
+}
+
+// one flow call of the scheme: seq positions seq0, seq0+1, ... (exact) or seq0 (rk4)
+template <int NF>
+__device__ __forceinline__ V<NF> flow(const StageNL& p, const V<NF>& u, double t, uint64_t step, int seq0,
+                                      uint64_t& key) {
+  V<NF> r;
+  if (p.kind == 0) {
+#pragma unroll
+    for (int c = 0; c < NF; ++c) r.c[c] = cubic_exact(p, u.c[c], t, (step << 24) | ((uint64_t)(seq0 + c) << 8), key);
+    return r;
+  }
+  const double h = 0.5 * t, t6 = t / 6.0;
+  const V<NF> k1 = gfun<NF>(p, u);
+  const V<NF> k2 = gfun<NF>(p, axpy<NF>(h, k1, u));
+  const V<NF> k3 = gfun<NF>(p, axpy<NF>(h, k2, u));
+  const V<NF> k4 = gfun<NF>(p, axpy<NF>(t, k3, u));
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) {
+    const double2 acc = cadd(cadd(cadd(k1.c[c], cscale(2.0, k2.c[c])), cscale(2.0, k3.c[c])), k4.c[c]);
+    r.c[c] = cadd(u.c[c], cscale(t6, acc));
+    bad |= !cfinite(r.c[c]);
+  }
+  if (bad) note(key, (step << 24) | ((uint64_t)seq0 << 8), CGL_NONFINITE_RK4);
+  return r;
+}
+
+template <int NF>
+__device__ __forceinline__ bool finite_all(const V<NF>& v) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) ok &= cfinite(v.c[c]);
+  return ok;
+}
+
+struct StageArgs {
+  const double2* in[12];  // up to 5 operands x 2 components (FIF4_S4, coupled)
+  double2* out[8];
+  int64_t n;
+  double tau;
+  double in_scale;
+  StageNL nl;
+  cgl_flag_t* flag;
+  uint64_t pos;  // CGL_POS_DEVICE form allowed; low bits ignored (each program knows its seqs)
+  int fw;        // flow width: calls per flow() = NF for the exact cubic flow, 1 for RK4
+  // Fourier programs: separable exp(f tau symbol) tables, [fraction 1/2, 1][component][axis]
+  const double2* tab[2][2][4];
+  int64_t ext[4];
+  int nd;
+  // column-block (transposed) layout of a slab-sharded spectral field: local
+  // element (k0, c) of an (n0 x tm) block is global flat k0*t12 + toff + c
+  int64_t tm, toff, t12;
+};
+
+// exp(f tau symbol) at flat index i (C order) for fraction slot fr, component c
+__device__ __forceinline__ double2 sep_factor(const StageArgs& a, int fr, int c, int64_t i) {
+  double2 e = make_double2(1.0, 0.0);
+  int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
+  for (int d = a.nd - 1; d >= 0; --d) {
+    const int64_t j = r % a.ext[d];
+    r /= a.ext[d];
+    e = cmul(e, ld2(a.tab[fr][c][d] + j));
+  }
+  return e;
+}
+
+template <int NF>
+__device__ __forceinline__ V<NF> emul(const StageArgs& a, int fr, int64_t i, const V<NF>& x) {
+  V<NF> r;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) r.c[c] = cmul(sep_factor(a, fr, c, i), x.c[c]);
+  return r;
+}
+
+__device__ __forceinline__ void raise_min(cgl_flag_t* f, uint64_t key) {
+  // warp-min then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other < key ? other : key;
+  }
+  if ((threadIdx.x & 31) == 0 && key != ~0ull && f) atomicMin(reinterpret_cast<unsigned long long*>(&f->key),
+                                                              (unsigned long long)key);
+}
+
+#define STAGE_LOOP for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; \
+                        i += (int64_t)gridDim.x * blockDim.x)
+
+enum Prog {
+  P_IF4_PRE = 0, P_IF4_MID, P_IF4_END, P_FLOW1, P_FLOW2, P_SPLIT4_MID, P_SPLIT4_END, P_STRANG_END,
+  P_IF2_PRE, P_IF2_END,
+  // Fourier (spectral-space) programs; g / flows run in physical space between cuFFT calls
+  P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END, P_NPROG
+};
+
+}  // namespace cgl

@@ -31,178 +31,22 @@
 #include <cstdint>
 
 #include <climits>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
 #include "oz_slice.cuh"
+#include "stage_ops.cuh"
+#include "rows_slice.cuh"
 
 namespace cgl {
 
-constexpr int kStageThreads = 256;
 
-struct StageNL {
-  double a3, b3, a4, b4, a5;
-  int kind;  // 0 cubic (exact flow), 1 cubic_quintic, 2 coupled
-};
-
-template <int NF>
-struct V {
-  double2 c[NF];
-};
-
-template <int NF>
-__device__ __forceinline__ V<NF> load(const double2* const* p, int base, int64_t i, double s) {
-  V<NF> v;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) v.c[c] = cscale(s, ld2(p[base + c] + i));
-  return v;
-}
-template <int NF>
-__device__ __forceinline__ void store(double2* const* p, int base, int64_t i, const V<NF>& v) {
-#pragma unroll
-  for (int c = 0; c < NF; ++c) p[base + c][i] = v.c[c];
-}
-template <int NF>
-__device__ __forceinline__ V<NF> axpy(double s, const V<NF>& x, const V<NF>& y) {  // s*x + y
-  V<NF> r;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) r.c[c] = cadd(cscale(s, x.c[c]), y.c[c]);
-  return r;
-}
-
-template <int NF>
-__device__ __forceinline__ V<NF> gfun(const StageNL& p, const V<NF>& u) {
-  double m[NF];
-#pragma unroll
-  for (int c = 0; c < NF; ++c) m[c] = cabs2(u.c[c]);
-  V<NF> g;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) {
-    double2 r = cmul(make_double2(p.a3 * m[c], p.b3 * m[c]), u.c[c]);
-    if (p.kind != 0) r = cadd(r, cmul(make_double2(p.a4 * (m[c] * m[c]), p.b4 * (m[c] * m[c])), u.c[c]));
-    if (p.kind == 2 && NF == 2) r = cadd(r, cscale(p.a5 * m[1 - c], u.c[c]));
-    g.c[c] = r;
-  }
-  return g;
-}
-
-__device__ __forceinline__ void note(uint64_t& key, uint64_t pos, unsigned reason) {
-  const uint64_t k = pos | reason;
-  if (k < key) key = k;
-}
-
-// exact cubic flow (flows.py:87-100) of one component at position pos
-__device__ __forceinline__ double2 cubic_exact(const StageNL& p, double2 u, double t, uint64_t pos, uint64_t& key) {
-  const double m = cabs2(u);
-  if (fabs(p.a3) < 1e-14) {
-    double sn, cs;
-    sincos(p.b3 * m * t, &sn, &cs);
-    return cmul(u, make_double2(cs, sn));
-  }
-  const double y = 2.0 * p.a3 * m * t;
-  if (y >= 1.0) note(key, pos, CGL_BLOWUP_CUBIC);
-  const double L = log1p(-y);
-  const double2 v = cmul(u, cexp(make_double2(-0.5 * L, (-p.b3 / (2.0 * p.a3)) * L)));
-  if (!cfinite(v)) note(key, pos, CGL_NONFINITE_CUBIC);
-  return v;
-}
-
-// one flow call of the scheme: seq positions seq0, seq0+1, ... (exact) or seq0 (rk4)
-template <int NF>
-__device__ __forceinline__ V<NF> flow(const StageNL& p, const V<NF>& u, double t, uint64_t step, int seq0,
-                                      uint64_t& key) {
-  V<NF> r;
-  if (p.kind == 0) {
-#pragma unroll
-    for (int c = 0; c < NF; ++c) r.c[c] = cubic_exact(p, u.c[c], t, (step << 24) | ((uint64_t)(seq0 + c) << 8), key);
-    return r;
-  }
-  const double h = 0.5 * t, t6 = t / 6.0;
-  const V<NF> k1 = gfun<NF>(p, u);
-  const V<NF> k2 = gfun<NF>(p, axpy<NF>(h, k1, u));
-  const V<NF> k3 = gfun<NF>(p, axpy<NF>(h, k2, u));
-  const V<NF> k4 = gfun<NF>(p, axpy<NF>(t, k3, u));
-  bool bad = false;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) {
-    const double2 acc = cadd(cadd(cadd(k1.c[c], cscale(2.0, k2.c[c])), cscale(2.0, k3.c[c])), k4.c[c]);
-    r.c[c] = cadd(u.c[c], cscale(t6, acc));
-    bad |= !cfinite(r.c[c]);
-  }
-  if (bad) note(key, (step << 24) | ((uint64_t)seq0 << 8), CGL_NONFINITE_RK4);
-  return r;
-}
-
-template <int NF>
-__device__ __forceinline__ bool finite_all(const V<NF>& v) {
-  bool ok = true;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) ok &= cfinite(v.c[c]);
-  return ok;
-}
-
-struct StageArgs {
-  const double2* in[12];  // up to 5 operands x 2 components (FIF4_S4, coupled)
-  double2* out[8];
-  int64_t n;
-  double tau;
-  double in_scale;
-  StageNL nl;
-  cgl_flag_t* flag;
-  uint64_t pos;  // CGL_POS_DEVICE form allowed; low bits ignored (each program knows its seqs)
-  int fw;        // flow width: calls per flow() = NF for the exact cubic flow, 1 for RK4
-  // Fourier programs: separable exp(f tau symbol) tables, [fraction 1/2, 1][component][axis]
-  const double2* tab[2][2][4];
-  int64_t ext[4];
-  int nd;
-  // column-block (transposed) layout of a slab-sharded spectral field: local
-  // element (k0, c) of an (n0 x tm) block is global flat k0*t12 + toff + c
-  int64_t tm, toff, t12;
-};
-
-// exp(f tau symbol) at flat index i (C order) for fraction slot fr, component c
-__device__ __forceinline__ double2 sep_factor(const StageArgs& a, int fr, int c, int64_t i) {
-  double2 e = make_double2(1.0, 0.0);
-  int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
-  for (int d = a.nd - 1; d >= 0; --d) {
-    const int64_t j = r % a.ext[d];
-    r /= a.ext[d];
-    e = cmul(e, ld2(a.tab[fr][c][d] + j));
-  }
-  return e;
-}
-
-template <int NF>
-__device__ __forceinline__ V<NF> emul(const StageArgs& a, int fr, int64_t i, const V<NF>& x) {
-  V<NF> r;
-#pragma unroll
-  for (int c = 0; c < NF; ++c) r.c[c] = cmul(sep_factor(a, fr, c, i), x.c[c]);
-  return r;
-}
-
-__device__ __forceinline__ void raise_min(cgl_flag_t* f, uint64_t key) {
-  // warp-min then one atomic per warp
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t other = __shfl_xor_sync(0xffffffffu, key, o);
-    key = other < key ? other : key;
-  }
-  if ((threadIdx.x & 31) == 0 && key != ~0ull && f) atomicMin(reinterpret_cast<unsigned long long*>(&f->key),
-                                                              (unsigned long long)key);
-}
-
-#define STAGE_LOOP for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; \
-                        i += (int64_t)gridDim.x * blockDim.x)
-
-enum Prog {
-  P_IF4_PRE = 0, P_IF4_MID, P_IF4_END, P_FLOW1, P_FLOW2, P_SPLIT4_MID, P_SPLIT4_END, P_STRANG_END,
-  P_IF2_PRE, P_IF2_END,
-  // Fourier (spectral-space) programs; g / flows run in physical space between cuFFT calls
-  P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END, P_NPROG
-};
 
 template <int NF, int PROG>
 __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a) {
+  CGL_PROF_SCOPE(KID_STAGE);
   pdl_wait();  // inputs and the divergence key come from earlier kernels
   const cgl_flag_t* cf = a.flag;
   const uint64_t step = resolve_pos(cf, a.pos) >> 24;
@@ -339,6 +183,7 @@ constexpr int kSSParts = kSSThreads / 32;
 
 template <int PROG, int NSL, int CPBT>
 __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSliceArgs A) {
+  CGL_PROF_SCOPE(KID_STAGE_SLICE);
   namespace cg = cooperative_groups;
   using oz::KC;
   using oz::NONFINITE;
@@ -349,6 +194,7 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
   static_assert(PT >= 1 && CR * W % kSSThreads == 0, "tile / CTA size");
   static_assert(kOzBN == CR, "B row tile");
   pdl_wait();
+  CGL_PROF_MARK(201);
   const StageArgs& a = A.s;
   const cgl_flag_t* cf = a.flag;
   const uint64_t step = resolve_pos(cf, a.pos) >> 24;
@@ -414,6 +260,7 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
     for (int q = 0; q < NSL; ++q) blk[(q * CR + rr) * (W + 1) + cc] = o[q];
   }
   __syncthreads();
+  CGL_PROF_MARK(202);
   pdl_trigger();
   // ---- partial exponents of the 32 Z rows per output, exchanged in the cluster ----
   __shared__ double red[NSL][kSSParts][33];
@@ -452,6 +299,7 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
     for (unsigned rk = 0; rk < nb; ++rk) cluster.map_shared_rank(&epart[0][0][0], rk)[(q * 16 + me) * 32 + rr] = e;
   }
   cluster.sync();
+  CGL_PROF_MARK(203);
   if (tid < 32 * NSL) {
     const int q = tid >> 5, rr = tid & 31;
     int e = INT_MIN;
@@ -491,6 +339,83 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
       *reinterpret_cast<uint4*>(dst + s8 * (CR * KC)) = make_uint4(wv[s8][0], wv[s8][1], wv[s8][2], wv[s8][3]);
   }
   raise_min(a.flag, key);
+}
+
+
+template <int PROG, int NSL, int TPT>
+__global__ void __launch_bounds__(kRSThreads) rows_slice_kernel(const RowsSliceArgs A) {
+  CGL_PROF_SCOPE(PROG == P_SLICE ? KID_SLICE : KID_STAGE_SLICE);
+  __shared__ RowsSliceSmem sm;
+  pdl_wait();
+  CGL_PROF_MARK(201);
+  if (A.debug & 8) return;  // timing experiment: launch + wait only
+  rows_slice_block<PROG, NSL, TPT>(A, blockIdx.x, blockIdx.y, threadIdx.x, 0, sm);
+  pdl_trigger();
+}
+
+// QC rows per CTA: 128 threads cover QC * KG tasks in TPT rounds; the
+// smallest QC that fills the 128 threads (measured: fewer, larger CTAs are
+// slower; CGL_RS_TARGET > 0 grows QC until the grid is about that many CTAs).
+int rows_slice_qc(int64_t K, int64_t rows_total, int tpt_max, int* tpt) {
+  const int64_t KG = (K + 7) / 8;
+  static const int target = [] {
+    const char* e = getenv("CGL_RS_TARGET");
+    return e ? atoi(e) : 0;
+  }();
+  int qc = 2;
+  while (qc < 32 && qc * KG < kRSThreads) qc <<= 1;
+  while (target > 0 && qc < 32 && rows_total / qc > target && (2 * qc) * KG <= (int64_t)tpt_max * kRSThreads) qc <<= 1;
+  *tpt = (int)((qc * KG + kRSThreads - 1) / kRSThreads);
+  return qc;
+}
+
+template <int PROG, int NSL>
+static cudaError_t launch_rows_slice(RowsSliceArgs& A, int64_t gy, cudaStream_t st) {
+  int tpt = 1;
+  A.QC = rows_slice_qc(A.K, A.rows * gy, PROG == P_SLICE ? 4 : 2, &tpt);
+  const dim3 grid((unsigned)((A.rows + A.QC - 1) / A.QC), (unsigned)gy, 1);
+  switch (tpt) {
+    case 1: return launch_k(rows_slice_kernel<PROG, NSL, 1>, grid, dim3(kRSThreads), 0, st, dim3(1), A);
+    case 2: return launch_k(rows_slice_kernel<PROG, NSL, 2>, grid, dim3(kRSThreads), 0, st, dim3(1), A);
+    default: break;
+  }
+  if constexpr (PROG == P_SLICE) {  // stage programs stop at TPT = 2 (register-resident stage outputs)
+    if (tpt == 3) return launch_k(rows_slice_kernel<PROG, NSL, 3>, grid, dim3(kRSThreads), 0, st, dim3(1), A);
+    if (tpt == 4) return launch_k(rows_slice_kernel<PROG, NSL, 4>, grid, dim3(kRSThreads), 0, st, dim3(1), A);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// plain slicing: K <= 2048 (TPT <= 4); stage programs: K <= 1024 (TPT <= 2)
+bool rows_slice_ok(int64_t K, bool stage) { return K >= 1 && (K + 7) / 8 <= (stage ? 2 : 4) * kRSThreads / 2; }
+
+int rows_slice_plain(cudaStream_t st, int nitems, const double* const* srcs, int64_t sr, int64_t sk, int64_t rows,
+                     int64_t K, int64_t batch, int64_t src_bs, int8_t* const* outs, int64_t out_bs,
+                     int* const* exps, int64_t exp_bs) {
+  if (!rows_slice_ok(K, false)) return set_error(CGL_ESHAPE, "rows_slice: K extent too large");
+  if (batch * nitems > 65535) return set_error(CGL_ESHAPE, "rows_slice: batch x items too large");
+  RowsSliceArgs A{};
+  for (int f = 0; f < nitems; ++f) {
+    A.srcs[f] = reinterpret_cast<const double2*>(srcs[f]);
+    A.slices[f] = outs[f];
+    A.exps[f] = exps[f];
+  }
+  A.src_bs = src_bs;
+  A.out_bs = out_bs;
+  A.exp_bs = exp_bs;
+  A.batch = batch;
+  A.rows = rows;
+  A.K = K;
+  A.sr = sr;
+  A.sk = sk;
+  A.nchunks = (int)((2 * K + oz::KC - 1) / oz::KC);
+  {
+    const char* d = getenv("CGL_RS_DEBUG");
+    A.debug = d ? atoi(d) : 0;
+  }
+  cudaError_t e = launch_rows_slice<P_SLICE, 1>(A, batch * nitems, st);
+  if (e != cudaSuccess) return set_cuda_error(e, "rows_slice launch");
+  return check_launch("rows_slice_kernel");
 }
 
 template <int PROG, int NSL, int CPBT>
@@ -547,6 +472,33 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   A.Q = Q;
   A.n0 = n0;
   A.nchunks = (int)((2 * n0 + oz::KC - 1) / oz::KC);
+  const char* ev = getenv("CGL_SS_CLUSTER");  // 1: the cluster kernel (A/B and tests)
+  const bool old_kernel = ev && ev[0] == '1';
+  if (!old_kernel && rows_slice_ok(n0, true)) {
+    // full-K CTAs (rows_slice_kernel): element (q, i) of the axis-0 data at i * Q + q
+    RowsSliceArgs R{};
+    R.s = a;
+    for (int q = 0; q < nsl; ++q) {
+      R.slices[q] = slices[q];
+      R.exps[q] = exps[q];
+    }
+    R.batch = 1;
+    R.rows = Q;
+    R.K = n0;
+    R.sr = 1;
+    R.sk = Q;
+    R.nchunks = A.nchunks;
+    cudaError_t e;
+    switch (prog) {
+      case P_IF4_MID: e = launch_rows_slice<P_IF4_MID, 2>(R, 1, st); break;
+      case P_IF4_END: e = launch_rows_slice<P_IF4_END, 3>(R, 1, st); break;
+      case P_STRANG_END: e = launch_rows_slice<P_STRANG_END, 1>(R, 1, st); break;
+      case P_SPLIT4_MID: e = launch_rows_slice<P_SPLIT4_MID, 1>(R, 1, st); break;
+      default: e = launch_rows_slice<P_SPLIT4_END, 2>(R, 1, st); break;
+    }
+    if (e != cudaSuccess) return set_cuda_error(e, "stage_slice (rows) launch");
+    return check_launch("rows_slice_kernel");
+  }
   // CTAs of a tile's cluster cover all K chunks: <= 16 CTAs (non-portable beyond 8)
   if (A.nchunks > 64) return set_error(CGL_ESHAPE, "stage_slice: axis-0 extent above 1024");
   const bool small = A.nchunks <= 32;
@@ -634,5 +586,7 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
   }
   return nf == 1 ? launch_prog<1>(prog, a, st) : launch_prog<2>(prog, a, st);
 }
+
+CGL_PROF_TU(stages)
 
 }  // namespace cgl

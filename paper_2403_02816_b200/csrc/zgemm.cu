@@ -210,6 +210,7 @@ __device__ __forceinline__ void finalize(Acc<Cfg>& acc) {
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool M3>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     zgemm_kernel(const GemmArgs args) {
+  CGL_PROF_SCOPE(KID_ZGEMM);
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES, M3>;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, NT = Cfg::NT;
 
@@ -442,5 +443,7 @@ int zgemm_launch(const GemmArgs& a, int nitems, cudaStream_t s) {
   return m3 ? launch_cfg<32, 32, 16, 2, 2, 3, true>(a, nitems, s)
             : launch_cfg<32, 32, 16, 2, 2, 3, false>(a, nitems, s);
 }
+
+CGL_PROF_TU(zgemm)
 
 }  // namespace cgl

@@ -86,6 +86,8 @@ class FusedPlan:
         self._pos = _lib.rel_pos(1)
         self._k_base = 0               # host copy of the flag's step base
         self._flag0 = self.flag.clone()
+        self._pending_end = None       # deferred end-of-step program (ozaki.StagePrologue)
+        self._defer_end = False        # a next step follows in the same chunk
         self.graph_launches = {}       # cgl kernels inside each captured graph
         self.replayed_launches = 0     # cgl kernels launched by graph replays (not seen by the C counter)
 
@@ -122,7 +124,26 @@ class FusedPlan:
                                        _lib.flag_ptr(flag), self._pos, _lib.ptr_array([t[0] for t in slots]),
                                        _lib.ptr_array([t[1] for t in slots])), "cgl_stage_slice")
 
-    def _tucker(self, jobs, flag, pre0=None):
+    def _end_stage(self, name, ins, out, slots, flag, tau):
+        """The end-of-step stage+slicing program of step k: deferred into the
+        next step's first axis-0 product launch (its producer phase,
+        cgl_oz_gemm_fused) when a next step follows in the same chunk, else
+        launched on its own (chunk boundary: the state must be complete)."""
+        if self._defer_end and self._fuse_pro():
+            from .ozaki import StagePrologue
+            self._pending_end = StagePrologue(name, [t for fs in ins for t in fs], out, self.nl, tau, self._pos)
+            return
+        self._stage_slice(name, ins, [[out]] if out is not None else [], slots, flag, tau)
+
+    def _fuse_pro(self):
+        from . import ozaki
+        return ozaki.fuse_enabled() and type(self) is FusedPlan and self._fused_slices() is not None
+
+    def _take_pending(self):
+        p, self._pending_end = self._pending_end, None
+        return p
+
+    def _tucker(self, jobs, flag, pre0=None, pro0=None):
         """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode
         (lean mode: one job at a time through the single scratch field).
         Products run on the INT8 tensor cores (ozaki.py) unless CGL_GEMM=dmma
@@ -147,9 +168,10 @@ class FusedPlan:
             for i in range(0, len(ins), 8):
                 sl = slice(i, i + 8)
                 ozaki.tucker_oz(ins[sl], facs[sl], outs[sl], work[sl] if work else None, self.oz_ws, flag=flag,
-                                pos=self._pos, pre0=pre0[sl] if pre0 is not None else None)
+                                pos=self._pos, pre0=pre0[sl] if pre0 is not None else None,
+                                pro0=pro0 if i == 0 else None)
             return
-        assert pre0 is None, "pre-sliced operands need the INT8-emulated products"
+        assert pre0 is None and pro0 is None, "pre-sliced operands need the INT8-emulated products"
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
             for c in range(self.nf):
@@ -201,16 +223,24 @@ class FusedPlan:
         B, H, O = self.B, self.half, self.one
         if self.scheme == "if4" and self._fused_slices() is not None:
             # X1, u, X5 (after step k-1) and g3, s reach their products only as
-            # slices made by the fused stage kernels; step 1 slices the prologue's X1, X5
+            # slices made by the fused stage kernels; step 1 slices the prologue's X1, X5.
+            # With producer fusion (cgl_oz_gemm_fused) MID runs inside the launch of
+            # the product it feeds, and END inside the next step's first product.
             u = self.U[0]
             x1, x5, u2, a, b, c = B
             F = self._fs
+            fuse = self._fuse_pro()
             self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag,
-                         pre0=None if k == 1 else [F[0], F[1], F[1], F[2]])
-            self._stage_slice("if4_mid", [u2, a], [], [F[3], F[4]], flag, tau)
-            self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
+                         pre0=None if k == 1 else [F[0], F[1], F[1], F[2]], pro0=self._take_pending())
+            if fuse:
+                from .ozaki import StagePrologue
+                mid = StagePrologue("if4_mid", [u2[0], a[0]], None, self.nl, tau, self._pos)
+                self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]], pro0=mid)
+            else:
+                self._stage_slice("if4_mid", [u2, a], [], [F[3], F[4]], flag, tau)
+                self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
             self._before_end(flag)
-            self._stage_slice("if4_end", [b, c, x1, x5], [u], [F[0], F[1], F[2]], flag, tau)
+            self._end_stage("if4_end", [b, c, x1, x5], u[0], [F[0], F[1], F[2]], flag, tau)
         elif self.scheme == "if4":
             u = self.U[0]
             x1, x5, u2, a, b, c = B
@@ -229,19 +259,25 @@ class FusedPlan:
             # v (= flow of the previous state) reaches its product only as slices
             v, w = B
             F = self._fs
-            self._tucker([(O, v, w)], flag, pre0=None if k == 1 else [F[0]])
+            self._tucker([(O, v, w)], flag, pre0=None if k == 1 else [F[0]], pro0=self._take_pending())
             self._before_end(flag)
-            self._stage_slice("strang_end", [w], [self.state_after(k)], [F[0]], flag, tau)
+            self._end_stage("strang_end", [w], self.state_after(k)[0], [F[0]], flag, tau)
         elif self.scheme == "split4" and self._fused_slices() is not None:
             # v, f of each step and the fine-path f after its first half step
             # reach their products only as slices (slots 0, 1 and 2)
             v, f, v2, f2 = B
             F = self._fs
-            self._tucker([(O, v, v2), (H, f, f2)], flag, pre0=None if k == 1 else [F[0], F[1]])
-            self._stage_slice("split4_mid", [v2, f2], [v2], [F[2]], flag, tau)   # coarse c -> v2 (FP64)
-            self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
+            self._tucker([(O, v, v2), (H, f, f2)], flag, pre0=None if k == 1 else [F[0], F[1]],
+                         pro0=self._take_pending())
+            if self._fuse_pro():
+                from .ozaki import StagePrologue
+                mid = StagePrologue("split4_mid", [v2[0], f2[0]], v2[0], self.nl, tau, self._pos)
+                self._tucker([(H, f2, v)], flag, pre0=[F[2]], pro0=mid)          # coarse c -> v2; f3 -> v
+            else:
+                self._stage_slice("split4_mid", [v2, f2], [v2], [F[2]], flag, tau)   # coarse c -> v2 (FP64)
+                self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
             self._before_end(flag)
-            self._stage_slice("split4_end", [v, v2], [self.state_after(k)], [F[0], F[1]], flag, tau)
+            self._end_stage("split4_end", [v, v2], self.state_after(k)[0], [F[0], F[1]], flag, tau)
         elif self.scheme == "strang":
             v, w = B
             self._tucker([(O, v, w)], flag)
@@ -275,7 +311,9 @@ class FusedPlan:
                 with torch.cuda.stream(s):
                     with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                         for j in range(count):
+                            self._defer_end = j < count - 1
                             self.step(k0 + j, flag, tau)
+                        self._defer_end = False
                         _lib.flag_advance(flag, count)
             finally:
                 if was:
@@ -292,6 +330,8 @@ class FusedPlan:
         flag.copy_(self._flag0)
         self._k_base = 0
         self._pos = _lib.rel_pos(1)
+        self._pending_end = None
+        self._defer_end = False
         self.load_state(u0, tau)
         self.prologue(flag, tau)
         stops = sorted(set(int(s) for s in stop_at if 1 <= int(s) <= steps))
@@ -310,7 +350,9 @@ class FusedPlan:
             count = min(self.CHUNK, nxt - k + 1)
             if eager_first or count != self.CHUNK:
                 for j in range(count):
+                    self._defer_end = j < count - 1
                     self.step(k + j, flag, tau)
+                self._defer_end = False
                 _lib.flag_advance(flag, count)
                 eager_first = False
             else:

@@ -373,12 +373,14 @@ def test_oz_chunked_products_bit_identical(P, monkeypatch):
         assert torch.equal(res[(1 << 40, axis)], res[(200_000, axis)])
 
 
-@pytest.mark.parametrize("shape", [(512, 512), (64, 48, 40)])
+@pytest.mark.parametrize("shape", [(512, 512), (64, 48, 40), (37, 50), (1000, 40), (256, 3)])
 @pytest.mark.parametrize("prog", ["if4_mid", "if4_end", "strang_end", "split4_mid", "split4_end"])
-def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
-    """cgl_stage_slice (fused stage + axis-0 data slicing) is bit-identical
-    to cgl_stage followed by cgl_oz_slice_multi of its outputs (divergence
-    key included)."""
+@pytest.mark.parametrize("kernel", ["rows", "cluster"])
+def test_stage_slice_matches_stage_then_slicing(P, shape, prog, kernel, monkeypatch):
+    """cgl_stage_slice (fused stage + axis-0 data slicing; the full-K
+    rows_slice kernel and the cluster kernel, CGL_SS_CLUSTER=1) is
+    bit-identical to cgl_stage followed by the two-pass data slicing
+    (CGL_OZ_FUSED_SLICE=0) of its outputs (divergence key included)."""
     from paper_2403_02816_b200 import _lib, ozaki, workloads as W
     lib = _lib.load()
     st = _lib.stream()
@@ -400,6 +402,7 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
                              _lib.ptr_array(ins), _lib.ptr_array(outs), _lib.flag_ptr(flag), _lib.rel_pos(1)), "stage")
     sliced = [outs[j] for j in sl_idx]
     per = lib.cgl_oz_slice_bytes(ozaki.S, Q, n0, 0)
+    monkeypatch.setenv("CGL_OZ_FUSED_SLICE", "0")
     ref = []
     for x in sliced:
         b = torch.zeros(per, dtype=torch.int8, device="cuda")
@@ -407,6 +410,10 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
         _lib.check(lib.cgl_oz_slice_multi(st, ozaki.S, 1, _lib.ptr_array([x]), 1, Q, Q, n0, 1, 0, 0,
                                           _lib.ptr_array([b]), 0, _lib.ptr_array([e]), 0), "slice")
         ref.append((b, e))
+    torch.cuda.synchronize()
+    monkeypatch.delenv("CGL_OZ_FUSED_SLICE")
+    if kernel == "cluster":
+        monkeypatch.setenv("CGL_SS_CLUSTER", "1")
     # fused
     flag2 = _lib.new_flag(0)
     u = torch.empty_like(ins[0])
@@ -419,10 +426,65 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog):
     torch.cuda.synchronize()
     for (rb, re_), (gb, ge) in zip(ref, got):
         assert torch.equal(re_, ge)
-        assert torch.equal(rb, gb)
+        bad = torch.nonzero(rb != gb).flatten()
+        assert bad.numel() == 0, (bad.numel(), bad[:8].tolist(), rb[bad[:8]].tolist(), gb[bad[:8]].tolist())
     if fp_idx is not None:
         assert torch.equal(u, outs[fp_idx])
     assert torch.equal(flag[:1], flag2[:1])
+
+
+@pytest.mark.parametrize("layout", ["last_axis", "first_axis"])
+@pytest.mark.parametrize("shape,nitems,batch", [((512, 512), 4, 1), ((37, 50), 2, 1), ((8, 300, 20), 3, 8),
+                                                ((2000, 6), 1, 1), ((16, 1500), 2, 2)])
+def test_rows_slicing_matches_two_pass(P, layout, shape, nitems, batch, monkeypatch):
+    """The full-K data slicing (rows_slice_kernel) is bit-identical to the
+    two-pass slicing (per-row exponents, then slice_tile_kernel) for both
+    strided layouts, several items and batches, ragged extents, a NaN row and
+    an all-zero row."""
+    from paper_2403_02816_b200 import _lib, ozaki
+    lib = _lib.load()
+    st = _lib.stream()
+    g = torch.Generator().manual_seed(5)
+    xs = []
+    for _ in range(nitems):
+        x = torch.complex(torch.randn(shape, generator=g, dtype=torch.float64),
+                          torch.randn(shape, generator=g, dtype=torch.float64))
+        x = x * torch.exp(4 * torch.randn(shape, generator=g, dtype=torch.float64))  # wide exponent range
+        xs.append(x.cuda())
+    xs[0].view(-1)[3] = float("nan")
+    if nitems > 1:
+        xs[1].view(-1, shape[-1])[1].zero_()
+    # tiny rows: subnormal values and maxima below 2^-940 (the careful digit path)
+    flat = xs[-1].view(-1, shape[-1])
+    flat[2] *= 1e-305
+    if flat.shape[0] > 4:
+        flat[4] *= 1e-318
+    # batch b of item f: rows x K matrix; last_axis: element (r, k) at r * K + k; first_axis: at k * rows + r
+    tot = int(np.prod(shape))
+    per_b = tot // batch
+    if layout == "last_axis":
+        K = shape[-1]
+        rows = per_b // K
+        sr, sc = K, 1
+    else:
+        K = shape[0] if batch == 1 else shape[1]
+        rows = per_b // K
+        sr, sc = 1, rows
+    per = lib.cgl_oz_slice_bytes(ozaki.S, rows, K, 0)
+
+    def run():
+        outs = [torch.zeros(per * batch, dtype=torch.int8, device="cuda") for _ in range(nitems)]
+        exps = [torch.empty(rows * batch, dtype=torch.int32, device="cuda") for _ in range(nitems)]
+        _lib.check(lib.cgl_oz_slice_multi(st, ozaki.S, nitems, _lib.ptr_array(xs), sr, sc, rows, K, batch, per_b, 0,
+                                          _lib.ptr_array(outs), per, _lib.ptr_array(exps), rows), "slice")
+        torch.cuda.synchronize()
+        return outs, exps
+
+    got = run()
+    monkeypatch.setenv("CGL_OZ_FUSED_SLICE", "0")
+    ref = run()
+    for a, b in zip(got[0] + got[1], ref[0] + ref[1]):
+        assert torch.equal(a, b)
 
 
 def test_device_uniforms_bit_identical(P):
