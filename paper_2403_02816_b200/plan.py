@@ -332,6 +332,16 @@ class FusedPlan:
         self._pos = _lib.rel_pos(1)
         self._pending_end = None
         self._defer_end = False
+        # captured graphs bake tau and the prepared operator factors (pointers):
+        # drop them when either changed since the capture (a re-prepared
+        # operator rebuilds its cache dict; holding the old dicts keeps their
+        # identities unique)
+        sig = (float(tau), [b._cache for b in self.blocks])
+        old = getattr(self, "_graph_sig", None)
+        if old is None or old[0] != sig[0] or any(x is not y for x, y in zip(old[1], sig[1])):
+            self.graphs.clear()
+            self.graph_launches.clear()
+        self._graph_sig = sig
         self.load_state(u0, tau)
         self.prologue(flag, tau)
         stops = sorted(set(int(s) for s in stop_at if 1 <= int(s) <= steps))
@@ -348,7 +358,9 @@ class FusedPlan:
         while k <= steps:
             nxt = next((s for s in stops if s >= k), steps)
             count = min(self.CHUNK, nxt - k + 1)
-            if eager_first or count != self.CHUNK:
+            if eager_first:
+                count = 1  # step 1 (its products slice the prologue's fields) runs eagerly
+            if eager_first:
                 for j in range(count):
                     self._defer_end = j < count - 1
                     self.step(k + j, flag, tau)

@@ -433,6 +433,24 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog, kernel, monkeypa
     assert torch.equal(flag[:1], flag2[:1])
 
 
+@pytest.mark.parametrize("key,scheme", [("C1", "if4"), ("C1", "strang"), ("C3", "strang"), ("C3", "if4")])
+def test_plan_graphs_follow_tau(P, key, scheme):
+    """Captured step graphs bake tau and the prepared factors: a second run on
+    the same problem with another tau (re-prepared operator) must equal a run
+    on a fresh problem, not replay the first run's graphs."""
+    from paper_2403_02816_b200 import workloads as W
+    w = W.CONFIGS[key].scaled(512 if key == "C1" else 32, 40)
+    x0 = W.initial_state_device(w)
+    if w.boundary == "periodic":
+        from paper_2403_02816_b200.spectral import fft_dev
+        x0 = fft_dev(x0)
+    prob = W.build_problem(w)
+    P.integrate(prob, scheme, (x0,), w.tau * 40, 40)
+    again = P.integrate(prob, scheme, (x0,), 0.5 * w.tau * 40, 40)
+    fresh = P.integrate(W.build_problem(w), scheme, (x0,), 0.5 * w.tau * 40, 40)
+    assert torch.equal(torch.as_tensor(again.fields[0]), torch.as_tensor(fresh.fields[0]))
+
+
 @pytest.mark.parametrize("layout", ["last_axis", "first_axis"])
 @pytest.mark.parametrize("shape,nitems,batch", [((512, 512), 4, 1), ((37, 50), 2, 1), ((8, 300, 20), 3, 8),
                                                 ((2000, 6), 1, 1), ((16, 1500), 2, 2)])
