@@ -156,6 +156,8 @@ def load():
                 raise ImportError(f"cgl_b200 CUDA library missing and cannot be built: {e}") from e
     lib = ctypes.CDLL(path)
     for name, (res, args) in _SIGS.items():
+        if override and not hasattr(lib, name):
+            continue  # A/B variant libraries may predate newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -35,8 +35,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-template <int MODE, int TMA = 0, int RND = 0>  // RND: random operand bytes; TMA: concurrent 40 KB/chunk bulk copies from 4 warps; 0: GEMM pattern (8 MMAs N=256..32); 1: 4.5 x N=256; 2: 36 x N=32; 3: pattern, A_BYTES slice stride 0
-__global__ void kern(int chunks, long long* out, const uint8_t* src) {
+template <int MODE, int TMA = 0, int RND = 0, int BG = 0>  // BG: 16 background warps run 1 DFMA / 2 I2F.F64.S64 / 3 IMAD+LOP3 / 4 FFMA / 5 tcgen05.ld loops; RND: random operand bytes; TMA: concurrent 40 KB/chunk bulk copies from 4 warps; 0: GEMM pattern (8 MMAs N=256..32); 1: 4.5 x N=256; 2: 36 x N=32; 3: pattern, A_BYTES slice stride 0
+__global__ void kern(int chunks, long long* out, const uint8_t* src, double* sink) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536 + 4 * 40960);
   uint64_t* tbar = bar + 8;
@@ -81,6 +81,35 @@ __global__ void kern(int chunks, long long* out, const uint8_t* src) {
     }
     mbar_wait(&tbar[w], 0);  // drain is approximate; parity not tracked after stop
   }
+  if (BG && warp >= 5 && warp < 21) {
+    // background work on the same SM while the MMA thread runs
+    double d0 = threadIdx.x * 1e-3, d1 = 1.0000001, d2 = 0.5;
+    long long l0 = threadIdx.x * 977ll;
+    unsigned u0 = threadIdx.x, u1 = 0x9e3779b9u;
+    float f0 = threadIdx.x * 1e-3f, f1 = 1.0000001f;
+    uint32_t acc = 0;
+    const long long tb0 = clock64();
+    for (int it = 0; it < 200; ++it) {
+#pragma unroll 16
+      for (int i = 0; i < 64; ++i) {
+        if (BG == 1) d0 = fma(d0, d1, d2);
+        if (BG == 2) { d0 += (double)(l0 + i); l0 ^= (long long)i << 20; }
+        if (BG == 3) { u0 = u0 * u1 + (unsigned)i; u1 ^= u0 >> 3; }
+        if (BG == 4) f0 = fmaf(f0, f1, 0.5f);
+        if (BG == 5 && (i & 15) == 0) {
+          uint32_t r[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                       : "r"(tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (warp >> 2) * 8));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          acc += r[0] ^ r[7];
+        }
+      }
+    }
+    const long long tb1 = clock64();
+    if (d0 == 12345.0 || f0 == 12345.0f || u0 == 12345u || acc == 7u) sink[0] = d0 + f0 + u0 + acc;
+    if (blockIdx.x == 0 && threadIdx.x == 32 * 5) out[1] = tb1 - tb0;  // background cycles for 200 x 64
+  }
   if (threadIdx.x == 0) {
     constexpr uint32_t LBO = 128, SBO = 256;
     const uint8_t* sa = smem;
@@ -119,17 +148,17 @@ __global__ void kern(int chunks, long long* out, const uint8_t* src) {
   }
 }
 
-template <int MODE, int TMA = 0, int RND = 0>
+template <int MODE, int TMA = 0, int RND = 0, int BG = 0>
 void run(const char* name, int nsm, long long* d_out, const uint8_t* src) {
   const int smem = 65536 + 4 * 40960 + 256;
-  cudaFuncSetAttribute(kern<MODE, TMA, RND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(kern<MODE, TMA, RND, BG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int chunks = 4000;
-  kern<MODE, TMA, RND><<<nsm, 160, smem>>>(100, d_out, src);
+  kern<MODE, TMA, RND, BG><<<nsm, BG ? 672 : 160, smem>>>(100, d_out, src, (double*)d_out + 4);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kern<MODE, TMA, RND><<<nsm, 160, smem>>>(chunks, d_out, src);
+  kern<MODE, TMA, RND, BG><<<nsm, BG ? 672 : 160, smem>>>(chunks, d_out, src, (double*)d_out + 4);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -137,6 +166,9 @@ void run(const char* name, int nsm, long long* d_out, const uint8_t* src) {
   long long cyc;
   cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
   const double macs = 4718592.0 * chunks * nsm;  // 36 x (128 x 32 x 32) per chunk
+  long long bgc = 0;
+  if (BG) cudaMemcpy(&bgc, d_out + 1, 8, cudaMemcpyDeviceToHost);
+  if (BG) printf("   background: %.1f clk per 64-op block while MMAs run\n", (double)bgc / 200);
   printf("%-40s %.3f us/chunk  %.0f clk/chunk  %.1f%% of 8192 MAC/clk  (%s)\n", name, ms * 1e3 / chunks,
          (double)cyc / chunks, 100.0 * 4718592.0 / 8192.0 / ((double)cyc / chunks),
          cudaGetErrorString(cudaGetLastError()));
@@ -158,5 +190,21 @@ int main() {
   run<0, 0, 1>("pattern, random bytes", nsm, d_out, src);
   run<1, 0, 1>("4.5 x N=256, random bytes", nsm, d_out, src);
   run<0, 0, 2>("pattern, random 6-bit magnitudes", nsm, d_out, src);
+  for (int bg = 1; bg <= 5; ++bg) {  // background alone (no MMA chunks)
+    long long bgc = 0;
+    const int smem = 65536 + 4 * 40960 + 256;
+    void (*k)(int, long long*, const uint8_t*, double*) = bg == 1 ? kern<0, 0, 2, 1> : bg == 2 ? kern<0, 0, 2, 2>
+        : bg == 3 ? kern<0, 0, 2, 3> : bg == 4 ? kern<0, 0, 2, 4> : kern<0, 0, 2, 5>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<<<nsm, 672, smem>>>(0, d_out, src, (double*)d_out + 4);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&bgc, d_out + 1, 8, cudaMemcpyDeviceToHost);
+    printf("background %d alone: %.1f clk per 64-op block\n", bg, (double)bgc / 200);
+  }
+  run<0, 0, 2, 1>("pattern + 16 warps DFMA", nsm, d_out, src);
+  run<0, 0, 2, 2>("pattern + 16 warps I2F.F64.S64+DADD", nsm, d_out, src);
+  run<0, 0, 2, 3>("pattern + 16 warps IMAD/LOP3", nsm, d_out, src);
+  run<0, 0, 2, 4>("pattern + 16 warps FFMA", nsm, d_out, src);
+  run<0, 0, 2, 5>("pattern + 16 warps tcgen05.ld (other cols)", nsm, d_out, src);
   return 0;
 }
