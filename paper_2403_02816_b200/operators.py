@@ -254,7 +254,14 @@ class FourierOperator:
         return tabs
 
     def prepare(self, tau, fractions):
-        self._tau = _check_tau(tau)
+        """exp(f tau symbol) per fraction (operators.py:160-167); unchanged
+        (tau, fractions) keep the cached factors (and with them the step
+        graphs of a plan that captured their pointers)."""
+        tau = _check_tau(tau)
+        fr = [_as_fraction(f) for f in fractions]
+        if tau == getattr(self, "_tau", None) and set(fr) == set(getattr(self, "_cache", {})):
+            return
+        self._tau = tau
         self._cache = {}
         _lib.require_cuda()
         for fraction in fractions:

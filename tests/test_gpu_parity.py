@@ -412,8 +412,7 @@ def test_stage_slice_matches_stage_then_slicing(P, shape, prog, kernel, monkeypa
         ref.append((b, e))
     torch.cuda.synchronize()
     monkeypatch.delenv("CGL_OZ_FUSED_SLICE")
-    if kernel == "cluster":
-        monkeypatch.setenv("CGL_SS_CLUSTER", "1")
+    monkeypatch.setenv("CGL_SS_CLUSTER", "1" if kernel == "cluster" else "0")
     # fused
     flag2 = _lib.new_flag(0)
     u = torch.empty_like(ins[0])

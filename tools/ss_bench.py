@@ -59,6 +59,10 @@ def gemm1(nf):
 cases = {
     "stage_slice_mid": lambda: stage_slice("if4_mid", F[:2], [], 2),
     "stage_slice_end": lambda: stage_slice("if4_end", F[:4], [O[0]], 3),
+    "stage_slice_strang_end": lambda: stage_slice("strang_end", F[:1], [O[0]], 1),
+    "stage_slice_split4_mid": lambda: stage_slice("split4_mid", F[:2], [O[0]], 1),
+    "stage_slice_split4_end": lambda: stage_slice("split4_end", F[:2], [O[0]], 2),
+    "slice_last_1f": lambda: slice_last(1),
     "slice_last_4f": lambda: slice_last(4),
     "slice_last_2f": lambda: slice_last(2),
     "gemm0_4f": lambda: gemm0(4),
