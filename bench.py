@@ -245,10 +245,20 @@ def gemm_roofline(torch, w, scheme_fields=4):
                                    _lib.ptr_array([fac.A] * scheme_fields), _lib.ptr_array([fac.Ae] * scheme_fields),
                                    _lib.ptr_array([fac.Az] * scheme_fields), _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                    None, _lib.ptr_array(outs), Q, 1, 0, 0, per, Q, n * Q, None, 0), "oz_gemm")
-    # replay captured graphs: eager launches of a ~20 us kernel are host-bound
-    dt = _time(torch, _graphed(torch, gemm_only))
-    dt_with_slicing = _time(torch, _graphed(torch, lambda: ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0,
-                                                                                 ws)))
+    # per-launch time as in the step: 10 back-to-back launches inside one
+    # captured graph (programmatic dependent launch between them, no
+    # graph-launch gap), event time / 10
+    reps_in_graph = 10
+
+    def gemm_rep():
+        for _ in range(reps_in_graph):
+            gemm_only()
+
+    def product_rep():
+        for _ in range(reps_in_graph):
+            ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws)
+    dt = _time(torch, _graphed(torch, gemm_rep)) / reps_in_graph
+    dt_with_slicing = _time(torch, _graphed(torch, product_rep)) / reps_in_graph
     bn = ozaki.geometry()[1]
     macs = ozaki.executed_macs_left(fac, (Q + bn - 1) // bn, scheme_fields)
     dense = ozaki.dense_macs(n, Q, n, scheme_fields)

@@ -595,6 +595,7 @@ struct OzArgs {
   uint64_t pos;
   long long* trace;  // optional: CTA 0 phase timestamps (globaltimer ns), see OZ_TRACE
   int debug;         // CGL_OZ_DEBUG (timing experiments only; results invalid): 1 skip MMAs, 2 skip copies
+  int m_fastest;     // tile order (persistent kernel): 1 = row tiles fastest (large data operands)
   OzItem items[kMaxItems];
   // fused prologue (ozgemm_persistent_kernel<..., PRO != 0>): the data slicing
   // (or stage program + slicing) that produces this GEMM's B operands, run by
@@ -901,10 +902,20 @@ struct TileId {
 __device__ __forceinline__ TileId decode_tile(const OzArgs& a, uint32_t t) {
   TileId d;
   const uint32_t nt = (uint32_t)a.ntiles, mt = (uint32_t)a.mtiles, nb = (uint32_t)a.batch;
-  uint32_t q = t / nt;
-  d.tn = (int)(t - q * nt);
-  const uint32_t q2 = q / mt;
-  d.tm = (int)(q - q2 * mt);
+  uint32_t q2;
+  if (a.m_fastest) {
+    // tm fastest: the CTAs in flight share few B tiles (read from HBM once,
+    // then from L2) -- for products whose data slices do not fit in L2
+    const uint32_t q = t / mt;
+    d.tm = (int)(t - q * mt);
+    q2 = q / nt;
+    d.tn = (int)(q - q2 * nt);
+  } else {
+    const uint32_t q = t / nt;
+    d.tn = (int)(t - q * nt);
+    q2 = q / mt;
+    d.tm = (int)(q - q2 * mt);
+  }
   const uint32_t q3 = q2 / nb;
   d.b = (int)(q2 - q3 * nb);
   d.item = (int)q3;
@@ -1467,6 +1478,13 @@ static int oz_args(oz::OzArgs& a, cudaStream_t st, int S, int64_t M, int64_t N, 
   for (int f = 0; f < nitems; ++f)
     a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
                             Bz ? Bz[f] : nullptr};
+  {
+    // CGL_OZ_MFAST=1: row tiles fastest (each B tile fetched from HBM once).
+    // Measured on C2/C4 (256^3 / 1024^3 products): no gain (C2 if4 5.82 ->
+    // 6.02 ms/step, C4 483 -> 487) -- off by default.
+    const char* e = getenv("CGL_OZ_MFAST");
+    a.m_fastest = e && e[0] == '1';
+  }
   return 0;
 }
 
