@@ -69,6 +69,13 @@ cases = {
     "gemm0_2f": lambda: gemm0(2),
     "gemm1_4f_incl_slice": lambda: gemm1(4),
 }
+# EVICT=MB: write a buffer of that size before every launch (L2 pressure as in the step)
+evict_mb = int(os.environ.get("EVICT", "0"))
+if evict_mb:
+    ebuf = torch.empty(evict_mb << 20, dtype=torch.uint8, device="cuda")
+    for k in list(cases):
+        f0 = cases[k]
+        cases[k] = (lambda f0: (lambda: (ebuf.fill_(1), f0())))(f0)
 only = sys.argv[1:] or list(cases)
 s = torch.cuda.Stream()
 for name in only:
