@@ -74,7 +74,12 @@ __device__ __forceinline__ double2 cubic_exact(const StageNL& p, double2 u, doub
   const double y = 2.0 * p.a3 * m * t;
   if (y >= 1.0) note(key, pos, CGL_BLOWUP_CUBIC);
   const double L = log1p(-y);
-  const double2 v = cmul(u, cexp(make_double2(-0.5 * L, (-p.b3 / (2.0 * p.a3)) * L)));
+  // |exp(-L/2)| = (1 - y)^(-1/2): one rsqrt instead of exp (same value to ~1 ulp;
+  // 1 - y is exact for y >= 1/2 and rounds once below); the phase needs L
+  double sn, cs;
+  sincos((-p.b3 / (2.0 * p.a3)) * L, &sn, &cs);
+  const double r = rsqrt(1.0 - y);
+  const double2 v = cmul(u, make_double2(__dmul_rn(r, cs), __dmul_rn(r, sn)));
   if (!cfinite(v)) note(key, pos, CGL_NONFINITE_CUBIC);
   return v;
 }
