@@ -187,6 +187,7 @@ struct SepArgs {
   const double2* tab[4];
   int64_t ext[4];
   int nd;
+  int lg[4], pow2;  // power-of-two extents: shift/mask indexing
   int64_t tm, toff, t12;  // optional column-block layout (see stages.cu)
 };
 
@@ -197,12 +198,20 @@ __global__ void separable_kernel(int64_t n, SepArgs a, double s, const double2* 
   pos = resolve_pos(flag, pos);
   if (flag_skip(flag, pos)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
     double2 e = make_double2(s, 0.0);
-    for (int d = a.nd - 1; d >= 0; --d) {
-      const int64_t j = r % a.ext[d];
-      r /= a.ext[d];
-      e = cmul(e, ld2(a.tab[d] + j));
+    if (a.pow2 && a.tm == 0) {
+      uint64_t r = (uint64_t)i;
+      for (int d = a.nd - 1; d >= 0; --d) {
+        e = cmul(e, ld2(a.tab[d] + (r & ((1ull << a.lg[d]) - 1ull))));
+        r >>= a.lg[d];
+      }
+    } else {
+      int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
+      for (int d = a.nd - 1; d >= 0; --d) {
+        const int64_t j = r % a.ext[d];
+        r /= a.ext[d];
+        e = cmul(e, ld2(a.tab[d] + j));
+      }
     }
     out[i] = cmul(e, ld2(in + i));
   }
@@ -310,7 +319,16 @@ int pw_separable(cudaStream_t st, int nd, const int64_t* shape, const double* co
   SepArgs a{};
   a.nd = nd;
   int64_t n = 1;
-  for (int d = 0; d < nd; ++d) { a.tab[d] = reinterpret_cast<const double2*>(tabs[d]); a.ext[d] = shape[d]; n *= shape[d]; }
+  a.pow2 = 1;
+  for (int d = 0; d < nd; ++d) {
+    a.tab[d] = reinterpret_cast<const double2*>(tabs[d]);
+    a.ext[d] = shape[d];
+    n *= shape[d];
+    int lg = 0;
+    while ((1ll << lg) < shape[d]) ++lg;
+    a.lg[d] = lg;
+    a.pow2 &= (1ll << lg) == shape[d];
+  }
   if (tm > 0) {
     a.tm = tm;
     a.toff = toff;

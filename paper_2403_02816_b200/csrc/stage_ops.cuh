@@ -132,6 +132,8 @@ struct StageArgs {
   const double2* tab[2][2][4];
   int64_t ext[4];
   int nd;
+  int lg[4];   // log2 ext[d] when every extent is a power of two (pow2), for shift/mask indexing
+  int pow2;
   // column-block (transposed) layout of a slab-sharded spectral field: local
   // element (k0, c) of an (n0 x tm) block is global flat k0*t12 + toff + c
   int64_t tm, toff, t12;
@@ -140,6 +142,14 @@ struct StageArgs {
 // exp(f tau symbol) at flat index i (C order) for fraction slot fr, component c
 __device__ __forceinline__ double2 sep_factor(const StageArgs& a, int fr, int c, int64_t i) {
   double2 e = make_double2(1.0, 0.0);
+  if (a.pow2 && a.tm == 0) {  // power-of-two extents: shifts and masks, no 64-bit divisions
+    uint64_t r = (uint64_t)i;
+    for (int d = a.nd - 1; d >= 0; --d) {
+      e = cmul(e, ld2(a.tab[fr][c][d] + (r & ((1ull << a.lg[d]) - 1ull))));
+      r >>= a.lg[d];
+    }
+    return e;
+  }
   int64_t r = a.tm > 0 ? (i / a.tm) * a.t12 + a.toff + (i % a.tm) : i;
   for (int d = a.nd - 1; d >= 0; --d) {
     const int64_t j = r % a.ext[d];

@@ -574,7 +574,15 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
     if (ndim < 1 || ndim > 4 || !shape || !tables) return set_error(CGL_EINVAL, "stage: Fourier programs need tables");
     a.nd = ndim;
     int64_t tot = 1;
-    for (int d = 0; d < ndim; ++d) { a.ext[d] = shape[d]; tot *= shape[d]; }
+    a.pow2 = 1;
+    for (int d = 0; d < ndim; ++d) {
+      a.ext[d] = shape[d];
+      tot *= shape[d];
+      int lg = 0;
+      while ((1ll << lg) < shape[d]) ++lg;
+      a.lg[d] = lg;
+      a.pow2 &= (1ll << lg) == shape[d];
+    }
     if (tm > 0) {
       // local (n0 x tm) column block of a global shape (sharded spectral layout)
       a.tm = tm;
