@@ -441,10 +441,12 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   switch (prog) {
     case P_IF4_MID: nin = 2; nsl = 2; nout = 0; break;
     case P_IF4_END: nin = 4; nsl = 3; nout = 1; break;
+    case P_IF4_MIDH: nin = 3; nsl = 2; nout = 0; break;
+    case P_IF4_ENDH: nin = 2; nsl = 3; nout = 1; break;
     case P_STRANG_END: nin = 1; nsl = 1; nout = 1; break;
     case P_SPLIT4_MID: nin = 2; nsl = 1; nout = 1; break;
     case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
-    default: return set_error(CGL_EINVAL, "stage_slice: if4 MID/END, strang END, split4 MID/END only");
+    default: return set_error(CGL_EINVAL, "stage_slice: if4 MID/END (+ half-step forms), strang END, split4 MID/END only");
   }
   if (n0 <= 0 || Q <= 0) return 0;
   if (nout && (!out || !out[0])) return set_error(CGL_EINVAL, "stage_slice: program writes an FP64 output");
@@ -479,7 +481,8 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   // kernel (256 threads x 4 points: C1 strang END 14.7 vs 18.9 us).
   // CGL_SS_CLUSTER=1 / =0 force either kernel (A/B and tests).
   const char* ev = getenv("CGL_SS_CLUSTER");
-  const bool old_kernel = ev ? ev[0] == '1' : !(prog == P_IF4_MID || prog == P_IF4_END || nl->kind != 0);
+  const bool half = prog == P_IF4_MIDH || prog == P_IF4_ENDH;  // rows kernel only
+  const bool old_kernel = !half && (ev ? ev[0] == '1' : !(prog == P_IF4_MID || prog == P_IF4_END || nl->kind != 0));
   if (!old_kernel && rows_slice_ok(n0, true)) {
     // full-K CTAs (rows_slice_kernel): element (q, i) of the axis-0 data at i * Q + q
     RowsSliceArgs R{};
@@ -498,6 +501,8 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
     switch (prog) {
       case P_IF4_MID: e = launch_rows_slice<P_IF4_MID, 2>(R, 1, st); break;
       case P_IF4_END: e = launch_rows_slice<P_IF4_END, 3>(R, 1, st); break;
+      case P_IF4_MIDH: e = launch_rows_slice<P_IF4_MIDH, 2>(R, 1, st); break;
+      case P_IF4_ENDH: e = launch_rows_slice<P_IF4_ENDH, 3>(R, 1, st); break;
       case P_STRANG_END: e = launch_rows_slice<P_STRANG_END, 1>(R, 1, st); break;
       case P_SPLIT4_MID: e = launch_rows_slice<P_SPLIT4_MID, 1>(R, 1, st); break;
       default: e = launch_rows_slice<P_SPLIT4_END, 2>(R, 1, st); break;
@@ -505,6 +510,7 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
     if (e != cudaSuccess) return set_cuda_error(e, "stage_slice (rows) launch");
     return check_launch("rows_slice_kernel");
   }
+  if (half) return set_error(CGL_ESHAPE, "stage_slice: the if4 half-step programs need an axis-0 extent <= 1024");
   // CTAs of a tile's cluster cover all K chunks: <= 16 CTAs (non-portable beyond 8)
   if (A.nchunks > 64) return set_error(CGL_ESHAPE, "stage_slice: axis-0 extent above 1024");
   const bool small = A.nchunks <= 32;

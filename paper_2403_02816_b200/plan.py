@@ -221,7 +221,22 @@ class FusedPlan:
         """One time step k (1-based); input state_after(k-1), output state_after(k)."""
         self._pos = _lib.rel_pos(k - self._k_base)
         B, H, O = self.B, self.half, self.one
-        if self.scheme == "if4" and self._fused_slices() is not None:
+        if (self.scheme == "if4" and self._fused_slices() is not None and not self._fuse_pro()
+                and os.environ.get("CGL_IF4_HALF", "1") != "0"):
+            # semigroup form E1 = E1/2 E1/2 (SURVEY 8(c): parity headroom covers it):
+            # [u2, a, w] = E1/2 [X1, u, X5]; MIDH -> p = a + t g3, r = w + t/3 s;
+            # [u4, q] = E1/2 [p, r]; ENDH -> out = q + t/6 g(u4).  Five half-step
+            # Tuckers per step instead of four half + two full ones.
+            u = self.U[0]
+            x1, x5, u2, a, b, c = B
+            F = self._fs
+            self._tucker([(H, x1, u2), (H, u, a), (H, x5, b)], flag,
+                         pre0=None if k == 1 else [F[0], F[1], F[2]])
+            self._stage_slice("if4_midh", [u2, a, b], [], [F[3], F[4]], flag, tau)
+            self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])     # u4 -> x1, q -> x5
+            self._before_end(flag)
+            self._stage_slice("if4_endh", [x1, x5], [u], [F[0], F[1], F[2]], flag, tau)
+        elif self.scheme == "if4" and self._fused_slices() is not None:
             # X1, u, X5 (after step k-1) and g3, s reach their products only as
             # slices made by the fused stage kernels; step 1 slices the prologue's X1, X5.
             # With producer fusion (cgl_oz_gemm_fused) MID runs inside the launch of

@@ -450,6 +450,40 @@ def test_plan_graphs_follow_tau(P, key, scheme):
     assert torch.equal(torch.as_tensor(again.fields[0]), torch.as_tensor(fresh.fields[0]))
 
 
+def test_if4_semigroup_form_matches_reference_form(P, monkeypatch):
+    """The fused if4 plan runs the step on E1 = E1/2 E1/2 (five half-step
+    Tuckers, MIDH/ENDH programs); the reference's form (E1 Tuckers,
+    CGL_IF4_HALF=0) and the CPU oracle agree with it to rounding level."""
+    from paper_2403_02816_b200 import workloads as W
+    w = W.CONFIGS["C1"].scaled(512, 60)
+    x0 = W.initial_state_device(w)
+    res = {}
+    for half in ("1", "0"):
+        monkeypatch.setenv("CGL_IF4_HALF", half)
+        res[half] = P.integrate(W.build_problem(w), "if4", (x0,), w.tau * 60, 60).fields[0]
+    a, b = torch.as_tensor(res["1"]), torch.as_tensor(res["0"])
+    # E1/2 E1/2 vs the Pade E1: ~2e-15 per step, 1.3e-13 observed after 60 steps
+    assert float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) <= 1e-12
+
+
+@pytest.mark.parametrize("scheme", ["if4", "strang", "split4"])
+def test_fused_producer_launch_matches_separate_launches(P, scheme, monkeypatch):
+    """cgl_oz_gemm_fused (CGL_OZ_FUSE=1: the data slicing / stage program runs
+    as the product launch's producer phase, END deferred into the next step's
+    first product) gives the same bits as separate slicing / stage launches."""
+    from paper_2403_02816_b200 import workloads as W
+    w = W.CONFIGS["C1"].scaled(512, 40)
+    x0 = W.initial_state_device(w)
+    monkeypatch.setenv("CGL_IF4_HALF", "0")  # the producer fusion covers the reference-form if4
+    res = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CGL_OZ_FUSE", fuse)
+        r = P.integrate(W.build_problem(w), scheme, (x0,), w.tau * 40, 40)
+        assert not r.diverged
+        res[fuse] = torch.as_tensor(r.fields[0])
+    assert torch.equal(res["1"], res["0"])
+
+
 @pytest.mark.parametrize("layout", ["last_axis", "first_axis"])
 @pytest.mark.parametrize("shape,nitems,batch", [((512, 512), 4, 1), ((37, 50), 2, 1), ((8, 300, 20), 3, 8),
                                                 ((2000, 6), 1, 1), ((16, 1500), 2, 2)])

@@ -1,0 +1,43 @@
+"""Achieved parity against the reference's recorded outputs (tests/golden):
+relative L2 of every BASELINE-config fixture and the full-size C1 runs, for the
+default plans and (if4) the reference-form plan (CGL_IF4_HALF=0).
+`python tools/parity_report.py` -> one line per case."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+
+import paper_2403_02816_b200 as P  # noqa: E402
+from conftest import GOLDEN, rel_l2  # noqa: E402
+from paper_2403_02816_b200 import workloads as W  # noqa: E402
+
+arrays = np.load(os.path.join(GOLDEN, "configs.npz"))
+meta = {m["tag"]: m for m in json.load(open(os.path.join(GOLDEN, "configs.json")))}
+
+
+def run(tag):
+    m = meta[tag]
+    w = W.CONFIGS[m["workload"].split("-")[0]]
+    if "@" in m["workload"]:
+        w = w.scaled(m["extents"][0], m["steps"])
+    x0 = W.state_for_problem(w, W.initial_state(w))
+    return P.integrate(W.build_problem(w), m["scheme"], (x0,), w.t_final, w.steps)
+
+
+cases = ["C0_strang", "C1s64_if4", "C1s64_rk4", "C2s24_split4", "C3s32_if4", "C3s32_strang", "C4s24_if4",
+         "C1_if4", "C1_strang", "C1_rk4"]
+for half in ("1", "0"):
+    os.environ["CGL_IF4_HALF"] = half
+    for tag in cases:
+        if half == "0" and "if4" not in tag:
+            continue
+        want = arrays[f"{tag}_out"] if f"{tag}_out" in arrays else np.load(os.path.join(GOLDEN, f"{tag}_out.npy"))
+        r = run(tag)
+        fin = np.isfinite(want)
+        err = rel_l2(r.fields[0][fin], want[fin]) if fin.any() else 0.0
+        print(json.dumps({"case": tag, "if4_form": "semigroup" if half == "1" else "reference", "rel_l2": err,
+                          "diverged": r.diverged, "diverged_at": r.diverged_at}), flush=True)
