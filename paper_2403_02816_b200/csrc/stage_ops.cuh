@@ -184,13 +184,13 @@ enum Prog {
   P_IF4_PRE = 0, P_IF4_MID, P_IF4_END, P_FLOW1, P_FLOW2, P_SPLIT4_MID, P_SPLIT4_END, P_STRANG_END,
   P_IF2_PRE, P_IF2_END,
   // Fourier (spectral-space) programs; g / flows run in physical space between cuFFT calls
-  P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END, P_NPROG,
-  // if4 on the semigroup form E1 = E1/2 E1/2 (fused stage+slicing only, cgl_stage_slice):
+  P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END,
+  // if4 on the semigroup form E1 = E1/2 E1/2 (stage kernels and cgl_stage_slice):
   //   [u2, a, w] = E1/2 [X1, u, X5]
   //   MIDH: g2 = g(u2); u3 = a + t/2 g2; g3 = g(u3); s = g2 + g3;  p = a + t g3; r = w + t/3 s
   //   [u4, q] = E1/2 [p, r]          (u4 = E1 u + t E1/2 g3,  q = E1 X5 + t/3 E1/2 s)
   //   ENDH: g4 = g(u4); out = q + t/6 g4; check; X1 = out + t/2 g(out), X5 = out + t/6 g(out)
-  P_IF4_MIDH = 15, P_IF4_ENDH = 16
+  P_IF4_MIDH = 15, P_IF4_ENDH = 16, P_NPROG
 };
 
 }  // namespace cgl

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
   if (PROG == P_SPLIT4_END) first = 4 * a.fw;       // seq 4w
   if (PROG == P_STRANG_END || PROG == P_FLOW_END) first = a.fw;  // seq w
   const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END ||
-                       PROG == P_FIF4_S4 || PROG == P_FLOW_END);
+                       PROG == P_FIF4_S4 || PROG == P_FLOW_END || PROG == P_IF4_ENDH);
   if (flag_skip(cf, (step << 24) | ((uint64_t)first << 8))) return;  // all CTAs agree (key only grows later)
 
   uint64_t key = ~0ull;
@@ -79,6 +79,22 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       const V<NF> d = load<NF>(a.in, 2 * NF, i, s), e = load<NF>(a.in, 3 * NF, i, s);
       const V<NF> g4 = gfun<NF>(a.nl, axpy<NF>(t, d, b));
       const V<NF> out = axpy<NF>(t / 6.0, g4, axpy<NF>(t / 3.0, e, c));
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      const V<NF> g1 = gfun<NF>(a.nl, out);
+      store<NF>(a.out, NF, i, axpy<NF>(0.5 * t, g1, out));
+      store<NF>(a.out, 2 * NF, i, axpy<NF>(t / 6.0, g1, out));
+    } else if (PROG == P_IF4_MIDH) {
+      // semigroup form: p = a + t g3, r = w + t/3 (g2 + g3)   (stage_ops.cuh Prog)
+      const V<NF> u2 = load<NF>(a.in, 0, i, s), av = load<NF>(a.in, NF, i, s), w = load<NF>(a.in, 2 * NF, i, s);
+      const V<NF> g2 = gfun<NF>(a.nl, u2);
+      const V<NF> g3 = gfun<NF>(a.nl, axpy<NF>(0.5 * t, g2, av));
+      store<NF>(a.out, 0, i, axpy<NF>(t, g3, av));
+      store<NF>(a.out, NF, i, axpy<NF>(t / 3.0, axpy<NF>(1.0, g2, g3), w));
+    } else if (PROG == P_IF4_ENDH) {
+      // semigroup form: out = q + t/6 g(u4); check; PRE(out)
+      const V<NF> u4 = load<NF>(a.in, 0, i, s), q = load<NF>(a.in, NF, i, s);
+      const V<NF> out = axpy<NF>(t / 6.0, gfun<NF>(a.nl, u4), q);
       if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
       store<NF>(a.out, 0, i, out);
       const V<NF> g1 = gfun<NF>(a.nl, out);
@@ -548,6 +564,8 @@ static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
     case P_FIF4_S3: e = launch_k(stage_kernel<NF, P_FIF4_S3>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     case P_FIF4_S4: e = launch_k(stage_kernel<NF, P_FIF4_S4>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     case P_FLOW_END: e = launch_k(stage_kernel<NF, P_FLOW_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_MIDH: e = launch_k(stage_kernel<NF, P_IF4_MIDH>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_ENDH: e = launch_k(stage_kernel<NF, P_IF4_ENDH>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     default: return set_error(CGL_EINVAL, "stage: unknown program");
   }
   if (e != cudaSuccess) return set_cuda_error(e, "stage_kernel launch");
@@ -555,8 +573,8 @@ static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
 }
 
 // inputs/outputs per program, in units of component groups
-static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2, 2, 2, 2, 5, 1};
-static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1};
+static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2, 2, 2, 2, 5, 1, 3, 2};
+static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1, 2, 3};
 
 int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonlinear_t* nl, double tau,
                  double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,

@@ -256,6 +256,15 @@ class FusedPlan:
                 self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
             self._before_end(flag)
             self._end_stage("if4_end", [b, c, x1, x5], u[0], [F[0], F[1], F[2]], flag, tau)
+        elif self.scheme == "if4" and not self._fuse_pro() and os.environ.get("CGL_IF4_HALF", "1") != "0":
+            # semigroup form without fused slicing (lean 1024^3 plans, DMMA grids)
+            u = self.U[0]
+            x1, x5, u2, a, b, c = B
+            self._tucker([(H, x1, u2), (H, u, a), (H, x5, b)], flag)
+            self._stage("if4_midh", [u2, a, b], [u2, a], flag, tau)        # p -> u2, r -> a
+            self._tucker([(H, u2, x1), (H, a, x5)], flag)                  # u4 -> x1, q -> x5
+            self._before_end(flag)
+            self._stage("if4_endh", [x1, x5], [u, x1, x5], flag, tau)
         elif self.scheme == "if4":
             u = self.U[0]
             x1, x5, u2, a, b, c = B
