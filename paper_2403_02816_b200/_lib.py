@@ -38,7 +38,8 @@ POS_DEVICE = 1 << 63
 
 STAGE = {"if4_pre": 0, "if4_mid": 1, "if4_end": 2, "flow1": 3, "flow2": 4, "split4_mid": 5,
          "split4_end": 6, "strang_end": 7, "if2_pre": 8, "if2_end": 9, "fif4_s1": 10, "fif4_s2": 11,
-         "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14, "if4_midh": 15, "if4_endh": 16}
+         "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14, "if4_midh": 15, "if4_endh": 16, "if4_midq": 17,
+         "if4_endq": 18}
 
 
 def new_flag(base=0):

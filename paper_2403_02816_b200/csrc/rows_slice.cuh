@@ -140,7 +140,26 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
 #pragma unroll
       for (int q = 0; q < NO; ++q) o[j][q][p] = make_double2(0.0, 0.0);
       if (!ok) continue;
-      if (PROG == P_IF4_MIDH) {
+      if (PROG == P_IF4_MIDQ) {
+        V<1> A, G;
+        A.c[0] = cscale(sc, in[0][p]);
+        G.c[0] = cscale(sc, in[NIN > 1 ? 1 : 0][p]);
+        const V<1> u2 = axpy<1>(0.5 * t, G, A), w = axpy<1>(t / 6.0, G, A);
+        const V<1> g2 = gfun<1>(a.nl, u2);
+        const V<1> g3 = gfun<1>(a.nl, axpy<1>(0.5 * t, g2, A));
+        const V<1> sv = axpy<1>(1.0, g2, g3);
+        o[j][0][p] = axpy<1>(t, g3, A).c[0];                     // p = a + t g3
+        o[j][NO > 1 ? 1 : 0][p] = axpy<1>(t / 3.0, sv, w).c[0];  // r = w + t/3 s
+      } else if (PROG == P_IF4_ENDQ) {
+        V<1> u4, q;
+        u4.c[0] = cscale(sc, in[0][p]);
+        q.c[0] = cscale(sc, in[NIN > 1 ? 1 : 0][p]);
+        const V<1> out = axpy<1>(t / 6.0, gfun<1>(a.nl, u4), q);
+        if (!finite_all<1>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        *dout = out.c[0];
+        o[j][0][p] = out.c[0];                                   // u
+        o[j][NO > 1 ? 1 : 0][p] = gfun<1>(a.nl, out).c[0];       // g1 of the next step
+      } else if (PROG == P_IF4_MIDH) {
         V<1> u2, av, w;
         u2.c[0] = cscale(sc, in[0][p]);
         av.c[0] = cscale(sc, in[NIN > 1 ? 1 : 0][p]);

@@ -190,7 +190,14 @@ enum Prog {
   //   MIDH: g2 = g(u2); u3 = a + t/2 g2; g3 = g(u3); s = g2 + g3;  p = a + t g3; r = w + t/3 s
   //   [u4, q] = E1/2 [p, r]          (u4 = E1 u + t E1/2 g3,  q = E1 X5 + t/3 E1/2 s)
   //   ENDH: g4 = g(u4); out = q + t/6 g4; check; X1 = out + t/2 g(out), X5 = out + t/6 g(out)
-  P_IF4_MIDH = 15, P_IF4_ENDH = 16, P_NPROG
+  P_IF4_MIDH = 15, P_IF4_ENDH = 16,
+  // ... and with linearity on top (E1/2 X1 = E1/2 u + t/2 E1/2 g1, same for X5):
+  //   [A, G] = E1/2 [u, g1]
+  //   MIDQ: u2 = A + t/2 G, w = A + t/6 G; g2 = g(u2); u3 = A + t/2 g2; g3 = g(u3); s = g2 + g3;
+  //         p = A + t g3; r = w + t/3 s
+  //   [u4, q] = E1/2 [p, r]
+  //   ENDQ: out = q + t/6 g(u4); check; g1' = g(out)        -> four half-step Tuckers per step
+  P_IF4_MIDQ = 17, P_IF4_ENDQ = 18, P_NPROG
 };
 
 }  // namespace cgl

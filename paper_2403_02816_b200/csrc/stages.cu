@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
   if (PROG == P_SPLIT4_END) first = 4 * a.fw;       // seq 4w
   if (PROG == P_STRANG_END || PROG == P_FLOW_END) first = a.fw;  // seq w
   const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END ||
-                       PROG == P_FIF4_S4 || PROG == P_FLOW_END || PROG == P_IF4_ENDH);
+                       PROG == P_FIF4_S4 || PROG == P_FLOW_END || PROG == P_IF4_ENDH || PROG == P_IF4_ENDQ);
   if (flag_skip(cf, (step << 24) | ((uint64_t)first << 8))) return;  // all CTAs agree (key only grows later)
 
   uint64_t key = ~0ull;
@@ -84,6 +84,21 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       const V<NF> g1 = gfun<NF>(a.nl, out);
       store<NF>(a.out, NF, i, axpy<NF>(0.5 * t, g1, out));
       store<NF>(a.out, 2 * NF, i, axpy<NF>(t / 6.0, g1, out));
+    } else if (PROG == P_IF4_MIDQ) {
+      // semigroup + linearity form: [A, G] = E1/2 [u, g1] -> p, r   (stage_ops.cuh Prog)
+      const V<NF> A = load<NF>(a.in, 0, i, s), G = load<NF>(a.in, NF, i, s);
+      const V<NF> u2 = axpy<NF>(0.5 * t, G, A), w = axpy<NF>(t / 6.0, G, A);
+      const V<NF> g2 = gfun<NF>(a.nl, u2);
+      const V<NF> g3 = gfun<NF>(a.nl, axpy<NF>(0.5 * t, g2, A));
+      store<NF>(a.out, 0, i, axpy<NF>(t, g3, A));
+      store<NF>(a.out, NF, i, axpy<NF>(t / 3.0, axpy<NF>(1.0, g2, g3), w));
+    } else if (PROG == P_IF4_ENDQ) {
+      // out = q + t/6 g(u4); check; g1 of the next step
+      const V<NF> u4 = load<NF>(a.in, 0, i, s), q = load<NF>(a.in, NF, i, s);
+      const V<NF> out = axpy<NF>(t / 6.0, gfun<NF>(a.nl, u4), q);
+      if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      store<NF>(a.out, 0, i, out);
+      store<NF>(a.out, NF, i, gfun<NF>(a.nl, out));
     } else if (PROG == P_IF4_MIDH) {
       // semigroup form: p = a + t g3, r = w + t/3 (g2 + g3)   (stage_ops.cuh Prog)
       const V<NF> u2 = load<NF>(a.in, 0, i, s), av = load<NF>(a.in, NF, i, s), w = load<NF>(a.in, 2 * NF, i, s);
@@ -459,6 +474,8 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
     case P_IF4_END: nin = 4; nsl = 3; nout = 1; break;
     case P_IF4_MIDH: nin = 3; nsl = 2; nout = 0; break;
     case P_IF4_ENDH: nin = 2; nsl = 3; nout = 1; break;
+    case P_IF4_MIDQ: nin = 2; nsl = 2; nout = 0; break;
+    case P_IF4_ENDQ: nin = 2; nsl = 2; nout = 1; break;
     case P_STRANG_END: nin = 1; nsl = 1; nout = 1; break;
     case P_SPLIT4_MID: nin = 2; nsl = 1; nout = 1; break;
     case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
@@ -497,7 +514,7 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   // kernel (256 threads x 4 points: C1 strang END 14.7 vs 18.9 us).
   // CGL_SS_CLUSTER=1 / =0 force either kernel (A/B and tests).
   const char* ev = getenv("CGL_SS_CLUSTER");
-  const bool half = prog == P_IF4_MIDH || prog == P_IF4_ENDH;  // rows kernel only
+  const bool half = prog == P_IF4_MIDH || prog == P_IF4_ENDH || prog == P_IF4_MIDQ || prog == P_IF4_ENDQ;  // rows kernel only
   const bool old_kernel = !half && (ev ? ev[0] == '1' : !(prog == P_IF4_MID || prog == P_IF4_END || nl->kind != 0));
   if (!old_kernel && rows_slice_ok(n0, true)) {
     // full-K CTAs (rows_slice_kernel): element (q, i) of the axis-0 data at i * Q + q
@@ -519,6 +536,8 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
       case P_IF4_END: e = launch_rows_slice<P_IF4_END, 3>(R, 1, st); break;
       case P_IF4_MIDH: e = launch_rows_slice<P_IF4_MIDH, 2>(R, 1, st); break;
       case P_IF4_ENDH: e = launch_rows_slice<P_IF4_ENDH, 3>(R, 1, st); break;
+      case P_IF4_MIDQ: e = launch_rows_slice<P_IF4_MIDQ, 2>(R, 1, st); break;
+      case P_IF4_ENDQ: e = launch_rows_slice<P_IF4_ENDQ, 2>(R, 1, st); break;
       case P_STRANG_END: e = launch_rows_slice<P_STRANG_END, 1>(R, 1, st); break;
       case P_SPLIT4_MID: e = launch_rows_slice<P_SPLIT4_MID, 1>(R, 1, st); break;
       default: e = launch_rows_slice<P_SPLIT4_END, 2>(R, 1, st); break;
@@ -566,6 +585,8 @@ static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
     case P_FLOW_END: e = launch_k(stage_kernel<NF, P_FLOW_END>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     case P_IF4_MIDH: e = launch_k(stage_kernel<NF, P_IF4_MIDH>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     case P_IF4_ENDH: e = launch_k(stage_kernel<NF, P_IF4_ENDH>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_MIDQ: e = launch_k(stage_kernel<NF, P_IF4_MIDQ>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
+    case P_IF4_ENDQ: e = launch_k(stage_kernel<NF, P_IF4_ENDQ>, dim3(grid), dim3(kStageThreads), 0, st, dim3(1), a); break;
     default: return set_error(CGL_EINVAL, "stage: unknown program");
   }
   if (e != cudaSuccess) return set_cuda_error(e, "stage_kernel launch");
@@ -573,8 +594,8 @@ static int launch_prog(int prog, const StageArgs& a, cudaStream_t st) {
 }
 
 // inputs/outputs per program, in units of component groups
-static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2, 2, 2, 2, 5, 1, 3, 2};
-static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1, 2, 3};
+static const int kIns[P_NPROG] = {1, 2, 4, 1, 1, 2, 2, 1, 1, 2, 2, 2, 2, 5, 1, 3, 2, 2, 2};
+static const int kOuts[P_NPROG] = {2, 2, 3, 1, 2, 2, 3, 2, 2, 3, 1, 1, 1, 1, 1, 2, 3, 2, 2};
 
 int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonlinear_t* nl, double tau,
                  double in_scale, const double* const* in, double* const* out, cgl_flag_t* flag, uint64_t pos,

@@ -135,6 +135,17 @@ class FusedPlan:
             return
         self._stage_slice(name, ins, [[out]] if out is not None else [], slots, flag, tau)
 
+    def _if4_form(self):
+        """if4 step form: "quad" (default: [A, G] = E1/2 [u, g1], four half-step
+        Tuckers), "half" (E1 = E1/2 E1/2, five), "ref" (the reference's six;
+        also CGL_IF4_HALF=0).  The producer-fusion path keeps "ref"."""
+        f = os.environ.get("CGL_IF4_FORM")
+        if f is None:
+            f = "ref" if os.environ.get("CGL_IF4_HALF", "1") == "0" else "quad"
+        if f not in ("quad", "half", "ref"):
+            raise ValueError(f"CGL_IF4_FORM must be quad, half or ref, not {f!r}")
+        return "ref" if self._fuse_pro() else f
+
     def _fuse_pro(self):
         from . import ozaki
         return ozaki.fuse_enabled() and type(self) is FusedPlan and self._fused_slices() is not None
@@ -208,7 +219,10 @@ class FusedPlan:
 
     def prologue(self, flag, tau):
         u, B = self.U[0], self.B
-        if self.scheme == "if4":
+        if self.scheme == "if4" and self._if4_form() == "quad":
+            from .flows import eval_g_dev
+            eval_g_dev(self.nl, u, outs=B[1], flag=flag, pos=self._pos)   # g1 = g(u0)
+        elif self.scheme == "if4":
             self._stage("if4_pre", [u], [B[0], B[1]], flag, tau)          # X1, X5
         elif self.scheme == "if2":
             self._stage("if2_pre", [u], [B[0], B[1]], flag, tau)          # X, Y
@@ -221,8 +235,19 @@ class FusedPlan:
         """One time step k (1-based); input state_after(k-1), output state_after(k)."""
         self._pos = _lib.rel_pos(k - self._k_base)
         B, H, O = self.B, self.half, self.one
-        if (self.scheme == "if4" and self._fused_slices() is not None and not self._fuse_pro()
-                and os.environ.get("CGL_IF4_HALF", "1") != "0"):
+        if self.scheme == "if4" and self._fused_slices() is not None and self._if4_form() == "quad":
+            # [A, G] = E1/2 [u, g1] (E1/2 X1 = A + t/2 G, E1/2 X5 = A + t/6 G by
+            # linearity); MIDQ -> p, r sliced; [u4, q] = E1/2 [p, r]; ENDQ -> u, g1'
+            # sliced (F0, F1).  Four half-step Tuckers per step.
+            u = self.U[0]
+            g1, A, G = B[1], B[2], B[3]
+            F = self._fs
+            self._tucker([(H, u, A), (H, g1, G)], flag, pre0=None if k == 1 else [F[0], F[1]])
+            self._stage_slice("if4_midq", [A, G], [], [F[3], F[4]], flag, tau)
+            self._tucker([(H, A, B[4]), (H, G, B[5])], flag, pre0=[F[3], F[4]])   # u4 -> B4, q -> B5
+            self._before_end(flag)
+            self._stage_slice("if4_endq", [B[4], B[5]], [u], [F[0], F[1]], flag, tau)
+        elif (self.scheme == "if4" and self._fused_slices() is not None and self._if4_form() == "half"):
             # semigroup form E1 = E1/2 E1/2 (SURVEY 8(c): parity headroom covers it):
             # [u2, a, w] = E1/2 [X1, u, X5]; MIDH -> p = a + t g3, r = w + t/3 s;
             # [u4, q] = E1/2 [p, r]; ENDH -> out = q + t/6 g(u4).  Five half-step
@@ -256,7 +281,15 @@ class FusedPlan:
                 self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
             self._before_end(flag)
             self._end_stage("if4_end", [b, c, x1, x5], u[0], [F[0], F[1], F[2]], flag, tau)
-        elif self.scheme == "if4" and not self._fuse_pro() and os.environ.get("CGL_IF4_HALF", "1") != "0":
+        elif self.scheme == "if4" and self._if4_form() == "quad":
+            u = self.U[0]
+            g1, A, G, u4, q = B[1], B[2], B[3], B[4], B[5]
+            self._tucker([(H, u, A), (H, g1, G)], flag)
+            self._stage("if4_midq", [A, G], [A, G], flag, tau)             # p -> A, r -> G
+            self._tucker([(H, A, u4), (H, G, q)], flag)
+            self._before_end(flag)
+            self._stage("if4_endq", [u4, q], [u, g1], flag, tau)
+        elif self.scheme == "if4" and self._if4_form() == "half":
             # semigroup form without fused slicing (lean 1024^3 plans, DMMA grids)
             u = self.U[0]
             x1, x5, u2, a, b, c = B

@@ -451,19 +451,20 @@ def test_plan_graphs_follow_tau(P, key, scheme):
 
 
 def test_if4_semigroup_form_matches_reference_form(P, monkeypatch):
-    """The fused if4 plan runs the step on E1 = E1/2 E1/2 (five half-step
-    Tuckers, MIDH/ENDH programs); the reference's form (E1 Tuckers,
-    CGL_IF4_HALF=0) and the CPU oracle agree with it to rounding level."""
+    """The fused if4 plan runs the step on E1 = E1/2 E1/2 plus linearity (four
+    half-step Tuckers, MIDQ/ENDQ; "half": five, MIDH/ENDH); the reference's
+    form (E1 Tuckers, CGL_IF4_FORM=ref) agrees with both to rounding level."""
     from paper_2403_02816_b200 import workloads as W
     w = W.CONFIGS["C1"].scaled(512, 60)
     x0 = W.initial_state_device(w)
     res = {}
-    for half in ("1", "0"):
-        monkeypatch.setenv("CGL_IF4_HALF", half)
-        res[half] = P.integrate(W.build_problem(w), "if4", (x0,), w.tau * 60, 60).fields[0]
-    a, b = torch.as_tensor(res["1"]), torch.as_tensor(res["0"])
-    # E1/2 E1/2 vs the Pade E1: ~2e-15 per step, 1.3e-13 observed after 60 steps
-    assert float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) <= 1e-12
+    for form in ("quad", "half", "ref"):
+        monkeypatch.setenv("CGL_IF4_FORM", form)
+        res[form] = torch.as_tensor(P.integrate(W.build_problem(w), "if4", (x0,), w.tau * 60, 60).fields[0])
+    b = res["ref"]
+    for form in ("quad", "half"):
+        # E1/2 E1/2 vs the Pade E1: ~2e-15 per step, 1.3e-13 observed after 60 steps
+        assert float(torch.linalg.norm(res[form] - b) / torch.linalg.norm(b)) <= 1e-12, form
 
 
 @pytest.mark.parametrize("scheme", ["if4", "strang", "split4"])

@@ -1,6 +1,6 @@
 """Achieved parity against the reference's recorded outputs (tests/golden):
 relative L2 of every BASELINE-config fixture and the full-size C1 runs, for the
-default plans and (if4) the reference-form plan (CGL_IF4_HALF=0).
+default plans (if4 in the "quad" form) and (if4) the reference-form plan (CGL_IF4_FORM=ref).
 `python tools/parity_report.py` -> one line per case."""
 import json
 import os
@@ -30,14 +30,14 @@ def run(tag):
 
 cases = ["C0_strang", "C1s64_if4", "C1s64_rk4", "C2s24_split4", "C3s32_if4", "C3s32_strang", "C4s24_if4",
          "C1_if4", "C1_strang", "C1_rk4"]
-for half in ("1", "0"):
-    os.environ["CGL_IF4_HALF"] = half
+for form in ("quad", "ref"):
+    os.environ["CGL_IF4_FORM"] = form
     for tag in cases:
-        if half == "0" and "if4" not in tag:
+        if form == "ref" and "if4" not in tag:
             continue
         want = arrays[f"{tag}_out"] if f"{tag}_out" in arrays else np.load(os.path.join(GOLDEN, f"{tag}_out.npy"))
         r = run(tag)
         fin = np.isfinite(want)
         err = rel_l2(r.fields[0][fin], want[fin]) if fin.any() else 0.0
-        print(json.dumps({"case": tag, "if4_form": "semigroup" if half == "1" else "reference", "rel_l2": err,
+        print(json.dumps({"case": tag, "if4_form": form, "rel_l2": err,
                           "diverged": r.diverged, "diverged_at": r.diverged_at}), flush=True)
