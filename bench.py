@@ -217,9 +217,10 @@ def _graphed(torch, fn):
     return g.replay
 
 
-def gemm_roofline(torch, w, scheme_fields=3):
-    """Dominant kernel of the if4 step: the 3-field axis-0 (left-form) product
-    of the semigroup-form step ([u2, a, w] = E1/2 [X1, u, X5])
+def gemm_roofline(torch, w, scheme_fields=2):
+    """Dominant kernel of the if4 step: the 2-field axis-0 (left-form) product
+    of the quad-form step ([A, G] = E1/2 [u, g1]; all four products of a step
+    are 2-field)
     on the INT8 tensor cores (ozgemm_persistent_kernel), timed per launch with CUDA
     events on the workload shapes, data pre-sliced as in the step.  Reported
     against the INT8 dense tensor peak on EXECUTED int8 MACs (block skipping
@@ -281,13 +282,13 @@ def gemm_roofline(torch, w, scheme_fields=3):
     fp64_alg = 8.0 * n * w.points * scheme_fields / dt / 1e12
     return {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS (int8)",
             "frac": achieved / int8_peak,
-            # dram__bytes_read.sum + dram__bytes_write.sum of one 3-field launch, ncu --set full
+            # dram__bytes_read.sum + dram__bytes_write.sum of one 2-field launch, ncu --set full
             # (profiles/r01c_ncu_full_step_kernels.txt; ncu flushes caches, so this is the
             # cold upper bound -- in the step the operands are L2-resident)
-            "traffic": 14.14e6, "traffic_unit": "bytes per launch",
+            "traffic": 9.94e6, "traffic_unit": "bytes per launch",
             "traffic_source": "profiles/r01c_ncu_full_step_kernels.txt (cold-cache ncu capture)",
             "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
-                      "accumulators): 3-field axis-0 product of the if4 step (E1/2 [X1, u, X5]), M=N=K=512 complex "
+                      "accumulators): 2-field axis-0 product of the if4 step (E1/2 [u, g1]), M=N=K=512 complex "
                       "per field, "
                       "S=8 int8 slices",
             "per_launch_ms": dt * 1e3, "per_launch_ms_incl_data_slicing": dt_with_slicing * 1e3,
