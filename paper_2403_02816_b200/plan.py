@@ -144,7 +144,7 @@ class FusedPlan:
             f = "ref" if os.environ.get("CGL_IF4_HALF", "1") == "0" else "quad"
         if f not in ("quad", "half", "ref"):
             raise ValueError(f"CGL_IF4_FORM must be quad, half or ref, not {f!r}")
-        return "ref" if self._fuse_pro() else f
+        return f
 
     def _fuse_pro(self):
         from . import ozaki

@@ -59,6 +59,8 @@ def gemm1(nf):
 cases = {
     "stage_slice_mid": lambda: stage_slice("if4_mid", F[:2], [], 2),
     "stage_slice_end": lambda: stage_slice("if4_end", F[:4], [O[0]], 3),
+    "stage_slice_midq": lambda: stage_slice("if4_midq", F[:2], [], 2),
+    "stage_slice_endq": lambda: stage_slice("if4_endq", F[:2], [O[0]], 2),
     "stage_slice_strang_end": lambda: stage_slice("strang_end", F[:1], [O[0]], 1),
     "stage_slice_split4_mid": lambda: stage_slice("split4_mid", F[:2], [O[0]], 1),
     "stage_slice_split4_end": lambda: stage_slice("split4_end", F[:2], [O[0]], 2),
