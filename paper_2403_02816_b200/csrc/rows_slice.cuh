@@ -45,12 +45,14 @@ struct RowsSliceArgs {
 
 // Shared-memory scratch of one 128-thread group.
 struct RowsSliceSmem {
-  double red[3][kRSThreads / 32][32];
-  int redbad[3][kRSThreads / 32][32];
+  double red[3][8][32];   // up to 8 warps per group (NT <= 256)
+  int redbad[3][8][32];
   int erow[3][32];
 };
 
-__device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(kRSThreads) : "memory"); }
+__device__ __forceinline__ void group_bar(int id, int nt = kRSThreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nt) : "memory");
+}
 
 // One virtual CTA (bx = row block, by = item * batch + b) of the full-K
 // slicing, run by a 128-thread group (tid 0..127) synchronising on named
@@ -61,7 +63,7 @@ __device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %
 // field 0x7FF (>= 0x7FF00000) marks Inf/NaN
 __device__ __forceinline__ unsigned absbits_hi(double x) { return (unsigned)__double2hiint(x) & 0x7FFFFFFFu; }
 
-template <int PROG, int NSL, int TPT>
+template <int PROG, int NSL, int TPT, int PP = 8, int NT = kRSThreads>
 __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t bx, int64_t by, int tid, int bar,
                                                  RowsSliceSmem& sm) {
   using oz::KC;
@@ -75,7 +77,8 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
   const int64_t R0 = bx * QC;
   const int item = PROG == P_SLICE ? (A.batch == 1 ? (int)by : (int)(by / A.batch)) : 0;
   const int64_t bb = PROG == P_SLICE ? (A.batch == 1 ? 0 : (int64_t)(by % A.batch)) : 0;
-  const int64_t KG = (A.K + 7) >> 3;  // 16-byte K groups
+  static_assert(PP == 8 || PP == 4, "points per task: one 16-byte (PP = 8) or 8-byte (PP = 4) K group");
+  const int64_t KG = (A.K + PP - 1) / PP;  // K groups of PP complex
   const int64_t sk = A.sk;
   // flag state (written by earlier kernels: plain loads after griddepcontrol.wait)
   uint64_t step = 0, fkey = ~0ull;
@@ -85,7 +88,7 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
     const uint64_t base = __ldcg(reinterpret_cast<const unsigned long long*>(&cf->step));
     step = (a.pos & CGL_POS_DEVICE) ? base + ((a.pos & ~CGL_POS_DEVICE) >> 24) : (a.pos >> 24);
   }
-  double2 o[TPT][NO][8];
+  double2 o[TPT][NO][PP];
   const double t = a.tau, sc = a.in_scale;
   uint64_t key = ~0ull;
   const uint64_t check_pos = (step << 24) | (255ull << 8);
@@ -94,26 +97,26 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
   (void)check_pos;
 #pragma unroll
   for (int j = 0; j < TPT; ++j) {
-    const int task = tid + kRSThreads * j;
+    const int task = tid + NT * j;
     const int qi = task & (QC - 1);
     const int64_t g = task >> lqc, R = R0 + qi;
     const bool live = g < KG && R < A.rows;
-    const bool full = live && 8 * g + 7 < A.K;  // common case: no per-point bounds
-    const int64_t i0 = live ? R * A.sr + 8 * g * sk : 0;  // element offset of the task's first point
+    const bool full = live && PP * g + PP - 1 < A.K;  // common case: no per-point bounds
+    const int64_t i0 = live ? R * A.sr + PP * g * sk : 0;  // element offset of the task's first point
     // ---- loads (the first task's are in flight together with the flag reads) ----
-    double2 in[NIN][8];
+    double2 in[NIN][PP];
     const double2* srcs[NIN];
 #pragma unroll
     for (int q = 0; q < NIN; ++q) srcs[q] = (PROG == P_SLICE ? A.srcs[item] + bb * A.src_bs : a.in[q]) + i0;
     if (full) {
 #pragma unroll
-      for (int p = 0; p < 8; ++p)
+      for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int q = 0; q < NIN; ++q) in[q][p] = __ldg(srcs[q] + p * sk);
     } else {
-      const int64_t nk = live ? A.K - 8 * g : 0;  // points of this task inside K
+      const int64_t nk = live ? A.K - PP * g : 0;  // points of this task inside K
 #pragma unroll
-      for (int p = 0; p < 8; ++p)
+      for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int q = 0; q < NIN; ++q) in[q][p] = p < nk ? __ldg(srcs[q] + p * sk) : make_double2(0.0, 0.0);
     }
@@ -127,15 +130,15 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
     }
     if (PROG == P_SLICE) {
 #pragma unroll
-      for (int p = 0; p < 8; ++p) o[j][0][p] = in[0][p];
+      for (int p = 0; p < PP; ++p) o[j][0][p] = in[0][p];
       continue;
     }
     // ---- stage program in registers; FP64 outputs stored here ----
     double2* dout = a.out[0] + i0;
 #pragma unroll
-    const int64_t nk = full ? 8 : (live ? A.K - 8 * g : 0);
+    const int64_t nk = full ? PP : (live ? A.K - PP * g : 0);
 #pragma unroll
-    for (int p = 0; p < 8; ++p, dout += sk) {
+    for (int p = 0; p < PP; ++p, dout += sk) {
       const bool ok = p < nk;
 #pragma unroll
       for (int q = 0; q < NO; ++q) o[j][q][p] = make_double2(0.0, 0.0);
@@ -241,20 +244,20 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
 #pragma unroll
     for (int j = 0; j < TPT; ++j)
 #pragma unroll
-      for (int p = 0; p < 8; ++p) mh = max(mh, max(absbits_hi(o[j][q][p].x), absbits_hi(o[j][q][p].y)));
+      for (int p = 0; p < PP; ++p) mh = max(mh, max(absbits_hi(o[j][q][p].x), absbits_hi(o[j][q][p].y)));
     for (int off = 16; off >= QC; off >>= 1) mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
     if (lane < QC) redbad[q][wid][lane] = (int)mh;
   }
-  group_bar(bar);
+  group_bar(bar, NT);
   if (tid < QC * NO) {
     const int q = tid >> lqc, qi = tid & (QC - 1);
     unsigned mh = (unsigned)redbad[q][0][qi];
-    for (int k = 1; k < kRSThreads / 32; ++k) mh = max(mh, (unsigned)redbad[q][k][qi]);
+    for (int k = 1; k < NT / 32; ++k) mh = max(mh, (unsigned)redbad[q][k][qi]);
     // normal max: frexp exponent = E - 1022; all zero / subnormal (E = 0): resolved below
     const int E = (int)(mh >> 20);
     erow[q][qi] = E == 0x7FF ? NONFINITE : (E == 0 ? INT_MIN : E - 1022);
   }
-  group_bar(bar);
+  group_bar(bar, NT);
   // rows whose max is zero or subnormal (rare): the exact frexp of the double max
   bool sub = false;
 #pragma unroll
@@ -267,22 +270,22 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
 #pragma unroll
       for (int j = 0; j < TPT; ++j)
 #pragma unroll
-        for (int p = 0; p < 8; ++p) m = fmax(m, fmax(fabs(o[j][q][p].x), fabs(o[j][q][p].y)));
+        for (int p = 0; p < PP; ++p) m = fmax(m, fmax(fabs(o[j][q][p].x), fabs(o[j][q][p].y)));
       for (int off = 16; off >= QC; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
       if (lane < QC) red[q][wid][lane] = m;
     }
-    group_bar(bar);
+    group_bar(bar, NT);
     if (tid < QC * NO) {
       const int q = tid >> lqc, qi = tid & (QC - 1);
       if (erow[q][qi] == INT_MIN) {
         double m = red[q][0][qi];
-        for (int k = 1; k < kRSThreads / 32; ++k) m = fmax(m, red[q][k][qi]);
+        for (int k = 1; k < NT / 32; ++k) m = fmax(m, red[q][k][qi]);
         int e = 0;  // all-zero row: 0 (same convention as the slicing kernels)
         if (m > 0.0) frexp(m, &e);
         erow[q][qi] = e;
       }
     }
-    group_bar(bar);
+    group_bar(bar, NT);
   }
   if (tid < QC * NO) {
     const int q = tid >> lqc, qi = tid & (QC - 1);
@@ -291,24 +294,27 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
       else A.exps[q][R0 + qi] = erow[q][qi];
     }
   }
-  // ---- digits: one 16-byte store per slice and task ----
+  // ---- digits: one 16-byte (PP = 8) or 8-byte (PP = 4) store per slice and task ----
+  constexpr int NW = PP / 2;  // 32-bit words per slice per task (two complex per word)
 #pragma unroll
   for (int j = 0; j < TPT; ++j) {
-    const int task = tid + kRSThreads * j;
+    const int task = tid + NT * j;
     const int qi = task & (QC - 1);
     const int64_t g = task >> lqc, R = R0 + qi;
     if (g >= KG || R >= A.rows) continue;  // padding stays zero (buffer zeroed once)
 #pragma unroll
     for (int q = 0; q < NO; ++q) {
       const int e = erow[q][qi];
-      uint32_t wv[8][4];
+      uint32_t wv[8][NW];
 #pragma unroll
-      for (int s8 = 0; s8 < 8; ++s8) wv[s8][0] = wv[s8][1] = wv[s8][2] = wv[s8][3] = 0u;
+      for (int s8 = 0; s8 < 8; ++s8)
+#pragma unroll
+        for (int k = 0; k < NW; ++k) wv[s8][k] = 0u;
       if (e != NONFINITE && !(A.debug & 1)) {
         const double2 s2p = oz::pow2_split(e);
         if (e >= -940) {  // uniform per row: one scaling factor, no subnormal checks
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < NW; ++k) {
             const double2 v0 = o[j][q][2 * k], v1 = o[j][q][2 * k + 1];
             const double x[4] = {v0.x, v0.y, v1.x, v1.y};
             uint32_t ww[8];
@@ -318,7 +324,7 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < NW; ++k) {
             const double2 v0 = o[j][q][2 * k], v1 = o[j][q][2 * k + 1];
             const double x[4] = {v0.x, v0.y, v1.x, v1.y};
             uint32_t ww[8];
@@ -329,11 +335,15 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
         }
       }
       int8_t* base = PROG == P_SLICE ? A.slices[item] + bb * A.out_bs : A.slices[q];
-      int8_t* dst = base + oz::tile_offset(R, 16 * g, kOzBN, A.nchunks, 8);
+      int8_t* dst = base + oz::tile_offset(R, 2 * PP * g, kOzBN, A.nchunks, 8);
       if (!(A.debug & 2)) {
 #pragma unroll
-        for (int s8 = 0; s8 < 8; ++s8)
-          *reinterpret_cast<uint4*>(dst + s8 * (kOzBN * KC)) = make_uint4(wv[s8][0], wv[s8][1], wv[s8][2], wv[s8][3]);
+        for (int s8 = 0; s8 < 8; ++s8) {
+          if constexpr (PP == 8)
+            *reinterpret_cast<uint4*>(dst + s8 * (kOzBN * KC)) = make_uint4(wv[s8][0], wv[s8][1], wv[s8][2], wv[s8][NW - 1]);
+          else
+            *reinterpret_cast<uint2*>(dst + s8 * (kOzBN * KC)) = make_uint2(wv[s8][0], wv[s8][NW - 1]);
+        }
       }
     }
   }

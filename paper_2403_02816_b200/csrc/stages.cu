@@ -373,36 +373,72 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
 }
 
 
-template <int PROG, int NSL, int TPT>
-__global__ void __launch_bounds__(kRSThreads) rows_slice_kernel(const RowsSliceArgs A) {
+template <int PROG, int NSL, int TPT, int PP = 8, int NT = kRSThreads>
+__global__ void __launch_bounds__(NT) rows_slice_kernel(const RowsSliceArgs A) {
   CGL_PROF_SCOPE(PROG == P_SLICE ? KID_SLICE : KID_STAGE_SLICE);
   __shared__ RowsSliceSmem sm;
   pdl_wait();
   CGL_PROF_MARK(201);
   if (A.debug & 8) return;  // timing experiment: launch + wait only
-  rows_slice_block<PROG, NSL, TPT>(A, blockIdx.x, blockIdx.y, threadIdx.x, 0, sm);
+  rows_slice_block<PROG, NSL, TPT, PP, NT>(A, blockIdx.x, blockIdx.y, threadIdx.x, 0, sm);
   pdl_trigger();
 }
 
-// QC rows per CTA: 128 threads cover QC * KG tasks in TPT rounds; the
-// smallest QC that fills the 128 threads (measured: fewer, larger CTAs are
-// slower; CGL_RS_TARGET > 0 grows QC until the grid is about that many CTAs).
-int rows_slice_qc(int64_t K, int64_t rows_total, int tpt_max, int* tpt) {
-  const int64_t KG = (K + 7) / 8;
+// QC rows per CTA: NT threads cover QC * KG tasks (PP complex each) in TPT
+// rounds; the smallest QC that fills the threads (measured: fewer, larger CTAs
+// are slower; CGL_RS_TARGET > 0 grows QC until the grid is about that many CTAs).
+int rows_slice_qc(int64_t K, int64_t rows_total, int tpt_max, int* tpt, int pp, int nt) {
+  const int64_t KG = (K + pp - 1) / pp;
   static const int target = [] {
     const char* e = getenv("CGL_RS_TARGET");
     return e ? atoi(e) : 0;
   }();
   int qc = 2;
-  while (qc < 32 && qc * KG < kRSThreads) qc <<= 1;
-  while (target > 0 && qc < 32 && rows_total / qc > target && (2 * qc) * KG <= (int64_t)tpt_max * kRSThreads) qc <<= 1;
-  *tpt = (int)((qc * KG + kRSThreads - 1) / kRSThreads);
+  while (qc < 32 && qc * KG < nt) qc <<= 1;
+  while (target > 0 && qc < 32 && rows_total / qc > target && (2 * qc) * KG <= (int64_t)tpt_max * nt) qc <<= 1;
+  *tpt = (int)((qc * KG + nt - 1) / nt);
   return qc;
+}
+int rows_slice_qc(int64_t K, int64_t rows_total, int tpt_max, int* tpt) {
+  return rows_slice_qc(K, rows_total, tpt_max, tpt, 8, kRSThreads);
+}
+
+// 4-point tasks on 256-thread CTAs: twice the warps of the 8-point /
+// 128-thread form at the same rows per CTA.  Measured on C1: MIDQ 7.4 -> 6.4,
+// ENDQ 7.6 -> 7.1, MID 6.6 -> 6.2, END 10.6 -> 9.6, 2-field slicing 5.9 -> 5.0
+// us; at 256^3 the stage programs are 3-11 % faster but the HBM-bound plain
+// slicing slower (90 -> 80 % of HBM).  Stage programs: always; plain slicing:
+// when the launch's data are L2-sized.  CGL_RS_PP (stage) / CGL_RS_PP_SLICE
+// (plain) = 4 or 8 force.
+static int rows_pp(bool stage, double bytes) {
+  static const int pp_stage = [] {
+    const char* e = getenv("CGL_RS_PP");
+    return e ? atoi(e) : 4;
+  }();
+  static const int pp_slice = [] {
+    const char* e = getenv("CGL_RS_PP_SLICE");
+    return e ? atoi(e) : 0;
+  }();
+  if (stage) return pp_stage;
+  return pp_slice ? pp_slice : (bytes <= 64.0 * (1 << 20) ? 4 : 8);
 }
 
 template <int PROG, int NSL>
 static cudaError_t launch_rows_slice(RowsSliceArgs& A, int64_t gy, cudaStream_t st) {
   int tpt = 1;
+  {
+    const double bytes = 16.0 * (double)A.rows * (double)gy * (double)A.K;
+    int tpt4 = 1;
+    const int qc4 = rows_slice_qc(A.K, A.rows * gy, 2, &tpt4, 4, 256);
+    if (rows_pp(PROG != P_SLICE, bytes) == 4 && tpt4 <= 2) {
+      A.QC = qc4;
+      tpt = tpt4;
+      const dim3 grid((unsigned)((A.rows + A.QC - 1) / A.QC), (unsigned)gy, 1);
+      if (tpt == 1) return launch_k(rows_slice_kernel<PROG, NSL, 1, 4, 256>, grid, dim3(256), 0, st, dim3(1), A);
+      if (tpt == 2) return launch_k(rows_slice_kernel<PROG, NSL, 2, 4, 256>, grid, dim3(256), 0, st, dim3(1), A);
+      return cudaErrorInvalidValue;
+    }
+  }
   A.QC = rows_slice_qc(A.K, A.rows * gy, PROG == P_SLICE ? 4 : 2, &tpt);
   const dim3 grid((unsigned)((A.rows + A.QC - 1) / A.QC), (unsigned)gy, 1);
   switch (tpt) {
