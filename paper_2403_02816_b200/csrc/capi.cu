@@ -162,12 +162,18 @@ int cgl_abi_version(void) { return CGL_ABI_VERSION; }
 unsigned long long cgl_launch_count(void) { return g_launches; }
 
 int cgl_prof_set(void* records, void* counter, unsigned capacity) {
-  int r = 0;
-  r |= cgl_prof_set_ozgemm(records, counter, capacity);
-  r |= cgl_prof_set_stages(records, counter, capacity);
-  r |= cgl_prof_set_pointwise(records, counter, capacity);
-  r |= cgl_prof_set_zgemm(records, counter, capacity);
-  return r ? set_error(CGL_EINVAL, "cgl_prof_set: not a profiling build (-DCGL_PROF)") : 0;
+  // every translation unit holds its own copy of the record pointers
+  static char msg[160];
+  msg[0] = 0;
+  if (cgl_prof_set_ozgemm(records, counter, capacity)) strcat(msg, " ozgemm");
+  if (cgl_prof_set_stages(records, counter, capacity)) strcat(msg, " stages");
+  if (cgl_prof_set_pointwise(records, counter, capacity)) strcat(msg, " pointwise");
+  if (cgl_prof_set_zgemm(records, counter, capacity)) strcat(msg, " zgemm");
+  if (!msg[0]) return 0;
+  static char full[256];
+  snprintf(full, sizeof full, "cgl_prof_set: not a profiling build (-DCGL_PROF) or symbol copy failed in:%s (%s)",
+           msg, cudaGetErrorString(cudaGetLastError()));
+  return set_error(CGL_EINVAL, full);
 }
 
 double cgl_probe_dmma(void* stream, int iters) {

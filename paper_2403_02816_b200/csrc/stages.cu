@@ -48,6 +48,7 @@ template <int NF, int PROG>
 __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a) {
   CGL_PROF_SCOPE(KID_STAGE);
   pdl_wait();  // inputs and the divergence key come from earlier kernels
+  pdl_trigger();  // the next kernel may take SMs as this grid drains (its own wait orders the data)
   const cgl_flag_t* cf = a.flag;
   const uint64_t step = resolve_pos(cf, a.pos) >> 24;
   // first flow seq of the program (skip position); non-flow programs: 0
@@ -182,7 +183,6 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       store<NF>(a.out, 2 * NF, i, axpy<NF>(0.5 * t, g1, out));
     }
   }
-  pdl_trigger();
   raise_min(a.flag, key);
   (void)is_end;
 }
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
   static_assert(PT >= 1 && CR * W % kSSThreads == 0, "tile / CTA size");
   static_assert(kOzBN == CR, "B row tile");
   pdl_wait();
+  pdl_trigger();  // as rows_slice_kernel: the GEMM's setup overlaps this grid's tail
   CGL_PROF_MARK(201);
   const StageArgs& a = A.s;
   const cgl_flag_t* cf = a.flag;
@@ -292,7 +293,6 @@ __global__ void __launch_bounds__(kSSThreads) stage_slice_kernel(const StageSlic
   }
   __syncthreads();
   CGL_PROF_MARK(202);
-  pdl_trigger();
   // ---- partial exponents of the 32 Z rows per output, exchanged in the cluster ----
   __shared__ double red[NSL][kSSParts][33];
   __shared__ int redbad[NSL][kSSParts][32];
@@ -378,10 +378,13 @@ __global__ void __launch_bounds__(NT) rows_slice_kernel(const RowsSliceArgs A) {
   CGL_PROF_SCOPE(PROG == P_SLICE ? KID_SLICE : KID_STAGE_SLICE);
   __shared__ RowsSliceSmem sm;
   pdl_wait();
+  // every CTA of this grid is resident by now at the step sizes: let the next
+  // kernel (the GEMM) take SMs as they drain -- its setup (barriers, TMEM,
+  // first live-chunk list, constant-factor copy) then overlaps this tail
+  pdl_trigger();
   CGL_PROF_MARK(201);
   if (A.debug & 8) return;  // timing experiment: launch + wait only
   rows_slice_block<PROG, NSL, TPT, PP, NT>(A, blockIdx.x, blockIdx.y, threadIdx.x, 0, sm);
-  pdl_trigger();
 }
 
 // QC rows per CTA: NT threads cover QC * KG tasks (PP complex each) in TPT
