@@ -72,6 +72,16 @@ __device__ __forceinline__ bool flag_skip(const cgl_flag_t* f, uint64_t pos) {
   return k < pos;
 }
 
+// flag_skip(f, resolve_pos(f, pos)) with key and step read by one 16-byte load
+__device__ __forceinline__ bool flag_skip_at(const cgl_flag_t* f, uint64_t pos) {
+  if (f == nullptr) return false;
+  if (reinterpret_cast<uintptr_t>(f) & 15) return flag_skip(f, resolve_pos(f, pos));  // C callers: 8-byte aligned
+  unsigned long long key, base;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(key), "=l"(base) : "l"(f) : "memory");
+  if (pos & CGL_POS_DEVICE) pos = ((base + ((pos & ~CGL_POS_DEVICE) >> 24)) << 24) | (pos & 0xFFFFFFull);
+  return key < pos;
+}
+
 __device__ __forceinline__ void flag_raise(cgl_flag_t* f, uint64_t pos, unsigned reason) {
   if (f != nullptr) atomicMin(reinterpret_cast<unsigned long long*>(&f->key),
                               (unsigned long long)(pos | reason));

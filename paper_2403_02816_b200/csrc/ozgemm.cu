@@ -1078,15 +1078,19 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
                      na * Cfg::A_BYTES, &full[st]);
           }
         }
-        bool skip = false;
-        if (!waited) {
+        const bool first = !waited;
+        if (first) {
           pdl_wait();
+          if (pw == 0) CGL_PROF_MARK(107);  // producer: pdl wait passed
           waited = true;
-          skip = flag_skip(a.flag, resolve_pos(a.flag, a.pos));  // the issuer skips too
         }
         if (lane == 0 && !(a.debug & 2))
           bulk_g2s(sb + (zb - 1) * Cfg::B_BYTES, B + ((int64_t)c * S + (zb - 1)) * Cfg::B_BYTES,
                    na * Cfg::B_BYTES, &full[st]);
+        // the divergence key is read after the first data copy is in flight
+        // (one L2 round trip off the critical path); the issuer skips too
+        const bool skip = first && flag_skip_at(a.flag, a.pos);
+        if (first && pw == 0) CGL_PROF_MARK(108);  // producer: flag read
         __syncwarp();
         if (skip) {  // nobody consumes this stage: let its copies land before the CTA exits
           if (lane == 0) mbar_wait(&full[st], ph);
@@ -1110,7 +1114,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     constexpr int PER = 256 / BN;
     const uint32_t leader = elect_lane();
     pdl_wait();
-    const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
+    const int64_t total_run = flag_skip_at(a.flag, a.pos) ? 0 : total;
     int it_n = 0, j = 0;
     for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const int buf = j & 1;
@@ -1182,7 +1186,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     const int part = lane & 1;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + half * HC;
     pdl_wait();
-    const int64_t total_run = flag_skip(a.flag, resolve_pos(a.flag, a.pos)) ? 0 : total;
+    const int64_t total_run = flag_skip_at(a.flag, a.pos) ? 0 : total;
     int j = 0;
     for (int64_t t = blockIdx.x; t < total_run; t += step, ++j) {
       const TileId td = decode_tile(a, (uint32_t)t);
