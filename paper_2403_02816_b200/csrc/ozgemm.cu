@@ -943,27 +943,53 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
   // item table in shared memory: a dynamically indexed kernel-parameter load
   // misses the constant cache, and the dependent global loads would stall on it
   __shared__ OzItem sitems[kMaxItems];
-  if (threadIdx.x < kMaxItems) sitems[threadIdx.x] = a.items[threadIdx.x];
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], OZP_EPI_WARPS);
-    }
-    for (int s = 0; s < Cfg::NTI; ++s) {
-      mbar_init(&ti_full[s], 1);
-      mbar_init(&ti_empty[s], OZP_PRODUCERS);  // issuer + the 3 other producer warps
-    }
-    fence_barrier_init();
+  static_assert(kMaxItems <= 32, "one warp writes the item table");
+  // warp 0: the first tile's zero-map words (constant factors, read before
+  // griddepcontrol.wait as below) are loaded first, their latency hidden
+  // behind the barrier init
+  int pre_za = S + 1, pre_zb = S + 1;
+  if (warp == 0 && (int64_t)blockIdx.x < total && lane < a.nchunks) {
+    const TileId td0 = decode_tile(a, blockIdx.x);
+    const int8_t* az0 = a.items[td0.item].Az;
+    const int8_t* bz0 = a.items[td0.item].Bz;
+    pre_za = az0 ? az0[(int64_t)td0.tm * a.nchunks + lane] : 1;
+    pre_zb = bz0 ? bz0[(int64_t)td0.tn * a.nchunks + lane] : 1;
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    // warp 0 (barrier init, then producer 0) never touches TMEM: with PRO == 0
+    // it starts the first tile's live-chunk list and copies right after the
+    // barrier init instead of waiting for the TMEM allocation and zeroing
+    // (named barrier 1: warp 0 arrives, the other warps sync)
+    if (lane < kMaxItems) sitems[lane] = a.items[lane];
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(&acc_full[s], 1);
+        mbar_init(&acc_empty[s], OZP_EPI_WARPS);
+      }
+      for (int s = 0; s < Cfg::NTI; ++s) {
+        mbar_init(&ti_full[s], 1);
+        mbar_init(&ti_empty[s], OZP_PRODUCERS);  // issuer + the 3 other producer warps
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    CGL_PROF_MARK(109);  // warp 0: barriers initialised
+    if constexpr (PRO == 0) {
+      asm volatile("bar.arrive 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
+    } else {
+      asm volatile("bar.sync 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
+    }
+  } else {
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
+    tc_fence_after();
+  }
+  const uint32_t tmem = warp == 0 ? 0u : *tmem_slot;
   if (warp >= 2 && warp < 2 + OZP_EPI_WARPS) {
     constexpr int HC = BN / OZP_EPI;
     const uint32_t q = warp & 3, grp = (warp - 2) >> 2;
@@ -975,10 +1001,15 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PRO == 0) {
+    // zeroed accumulators -> the issuer's first MMA (warps 1 .. last; not warp 0)
+    if (warp != 0) asm volatile("bar.sync 2, %0;\n" ::"n"(OZP_THREADS - 32) : "memory");
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   if (threadIdx.x == 0) OZ_TRACE(1);
-  if (warp == 0) CGL_PROF_MARK(101);  // setup done
+  if (warp == 1) CGL_PROF_MARK(101);  // setup done (TMEM ready)
   if constexpr (PRO != 0) {
     // ---- prologue phase: this GEMM's B operands (data slicing, optionally a
     // stage program) by the 16 epilogue warps as four 128-thread groups, the
@@ -1034,7 +1065,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
         int n = 0;
         for (int c0 = 0; c0 < nch; c0 += 32) {
           int zal = S + 1, zbl = S + 1;
-          if (c0 + lane < nch) {
+          if (j == 0 && c0 == 0) {
+            zal = pre_za;  // prefetched at kernel entry
+            zbl = pre_zb;
+          } else if (c0 + lane < nch) {
             zal = az ? az[c0 + lane] : 1;
             zbl = bz ? bz[c0 + lane] : 1;
           }
@@ -1048,6 +1082,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
         if (lane == 0) list[0] = (uint32_t)n;
         __syncwarp();
         if (lane == 0) mbar_arrive(&ti_full[slot]);
+        if (j == 0) CGL_PROF_MARK(114);  // first live-chunk list built
       } else {
         mbar_wait(&ti_full[slot], (j / Cfg::NTI) & 1);
       }
@@ -1079,6 +1114,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
           }
         }
         const bool first = !waited;
+        if (first && pw == 0) CGL_PROF_MARK(115);  // first constant-factor copy issued
         if (first) {
           pdl_wait();
           if (pw == 0) CGL_PROF_MARK(107);  // producer: pdl wait passed

@@ -64,10 +64,10 @@ print(f"# {key} {scheme}: {steps} steps, device {1e3 * r.device_seconds / steps:
 
 # in-kernel marks (ids >= 100) are reported with the launch they fall in
 MARKS = {101: "setup done", 110: "pro pdl passed", 111: "pro vb1", 112: "pro vb2", 113: "pro work done",
-         102: "prologue+barrier done", 103: "issuer first data", 104: "issuer done", 105: "epilogue done", 106: "producers done", 107: "producer pdl passed", 108: "producer flag read",
+         102: "prologue+barrier done", 103: "issuer first data", 104: "issuer done", 105: "epilogue done", 106: "producers done", 107: "producer pdl passed", 109: "w0 init", 114: "list built", 115: "A copy issued", 108: "producer flag read",
          201: "pdl wait passed", 202: "stage computed", 203: "exponents known",
          301: "pdl wait passed", 302: "staged", 303: "cluster synced"}
-MARKS_OF = {"ozgemm_persistent": (101, 110, 111, 112, 113, 102, 107, 108, 103, 104, 105, 106), "stage_slice": (201, 202, 203),
+MARKS_OF = {"ozgemm_persistent": (109, 101, 114, 115, 110, 111, 112, 113, 102, 107, 108, 103, 104, 105, 106), "stage_slice": (201, 202, 203),
             "slice_tile": (301, 302, 303, 201, 203)}
 is_mark = kid >= 100
 mk_t1, mk_kid = t1[is_mark], kid[is_mark]
