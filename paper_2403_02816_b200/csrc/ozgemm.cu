@@ -1277,19 +1277,32 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       if (j < 2 && threadIdx.x == 64) OZ_TRACE(37 + 3 * j);
       constexpr int HL = S < 4 ? S : 4;
       const double whi = pow2(-7 * (HL + 1)), wlo = pow2(-7 * (S + 1));
-      // value = ((hi 2^-35 + lo 2^-7(S+1)) 2^ea) 2^eb: one rounding in the fma,
-      // then exact power-of-two scalings (row scale first); NONFINITE
-      // exponents give NaN
+      // value = (hi 2^-35 + lo 2^-7(S+1)) 2^(ea+eb): one rounding in the fma,
+      // then one power-of-two scaling -- exact, and the same value as scaling
+      // by the row and then the column factor, whenever every exponent of the
+      // warp lies in [-450, 500] (no subnormal or overflow possible); one FP64
+      // multiply fewer per output (FP64 issue is the epilogue's bottleneck
+      // while the next tile's MMAs run).  Otherwise (or NONFINITE exponents:
+      // NaN) the general two-step path.
       const int64_t cbase = (int64_t)tn * BN + half * HC;
       static_assert(BN <= 32, "one column exponent per lane");
-      const double rs = pow2(ea);
       double v[HC];
+      if (__all_sync(0xffffffffu, ea >= -450 && ea <= 500 && eb_lane >= -450 && eb_lane <= 500)) {
 #pragma unroll
-      for (int k = 0; k < HC; ++k) {
-        const int eb = __shfl_sync(0xffffffffu, eb_lane, half * HC + k);
-        const double x = fma((double)hi[k], whi, (double)lo[k] * wlo);
-        const double y = (x * rs) * pow2(eb);
-        v[k] = (ea == NONFINITE || eb == NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll) : y;
+        for (int k = 0; k < HC; ++k) {
+          const int es = ea + __shfl_sync(0xffffffffu, eb_lane, half * HC + k) + 1023;
+          const double x = fma((double)hi[k], whi, (double)lo[k] * wlo);
+          v[k] = x * __longlong_as_double((long long)es << 52);
+        }
+      } else {
+        const double rs = pow2(ea);
+#pragma unroll
+        for (int k = 0; k < HC; ++k) {
+          const int eb = __shfl_sync(0xffffffffu, eb_lane, half * HC + k);
+          const double x = fma((double)hi[k], whi, (double)lo[k] * wlo);
+          const double y = (x * rs) * pow2(eb);
+          v[k] = (ea == NONFINITE || eb == NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll) : y;
+        }
       }
       if (j < 2 && threadIdx.x == 64) OZ_TRACE(38 + 3 * j);
       double2 out[HC / 2];
