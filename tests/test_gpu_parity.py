@@ -373,6 +373,28 @@ def test_oz_chunked_products_bit_identical(P, monkeypatch):
         assert torch.equal(res[(1 << 40, axis)], res[(200_000, axis)])
 
 
+@pytest.mark.parametrize("scale_exp", [-600, -300, 300, 600])
+def test_oz_products_power_of_two_scaling_exact(P, scale_exp):
+    """x 2^k in gives (u x_mu E) 2^k out bit for bit on the emulated path: the
+    slices are scale-free and the epilogue's scaling is exact for normal
+    results -- the one-multiply fast path (exponents in [-450, 500]) and the
+    general row-then-column path (|k| = 600) agree with each other."""
+    from paper_2403_02816_b200 import ozaki
+    g = torch.Generator().manual_seed(11)
+    for shape in ((512, 512), (48, 80, 96)):
+        x = torch.complex(torch.randn(shape, generator=g, dtype=torch.float64),
+                          torch.randn(shape, generator=g, dtype=torch.float64)).cuda()
+        ws = ozaki.Workspace()
+        for axis, n in enumerate(shape):
+            E = torch.complex(torch.randn(n, n, generator=g, dtype=torch.float64),
+                              torch.randn(n, n, generator=g, dtype=torch.float64)).cuda()
+            fac = ozaki.SlicedFactor(E)
+            ref, out = torch.empty_like(x), torch.empty_like(x)
+            ozaki.mode_product_oz([x], [fac], [ref], axis, ws)
+            ozaki.mode_product_oz([x * 2.0 ** scale_exp], [fac], [out], axis, ws)
+            assert torch.equal(out, ref * 2.0 ** scale_exp), (shape, axis)
+
+
 @pytest.mark.parametrize("shape", [(512, 512), (64, 48, 40), (37, 50), (1000, 40), (256, 3)])
 @pytest.mark.parametrize("prog", ["if4_mid", "if4_end", "strang_end", "split4_mid", "split4_end"])
 @pytest.mark.parametrize("kernel", ["rows", "cluster"])
