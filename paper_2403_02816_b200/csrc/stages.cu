@@ -546,15 +546,15 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   A.Q = Q;
   A.n0 = n0;
   A.nchunks = (int)((2 * n0 + oz::KC - 1) / oz::KC);
-  // full-K rows kernel for the if4 programs (measured: MID 6.6 vs 9.8 us, END
-  // 10.6 vs 14.7 us on C1; 77 / 64 % of HBM vs 54 / 50 % at 256^3) and for the
-  // RK4-flow (cubic-quintic) strang/split4 programs (split4 END 517 vs 611 us at
-  // 256^3); the exact cubic flows (log1p/exp/sincos per point) keep the cluster
-  // kernel (256 threads x 4 points: C1 strang END 14.7 vs 18.9 us).
-  // CGL_SS_CLUSTER=1 / =0 force either kernel (A/B and tests).
+  // full-K rows kernel for every program (measured: if4 MID 6.6 vs 9.8 us, END
+  // 10.6 vs 14.7 us on C1; split4 END 517 vs 611 us at 256^3; since its 4-point
+  // tasks on 256-thread CTAs and the early PDL trigger also the exact cubic
+  // flows: C1 strang 0.0417 -> 0.0354, split4 0.0947 -> 0.0813 ms/step, C2
+  // split4 3.67 -> 3.32 ms/step).  CGL_SS_CLUSTER=1 forces the cluster kernel
+  // (A/B and tests; not for the half-step if4 programs, rows kernel only).
   const char* ev = getenv("CGL_SS_CLUSTER");
   const bool half = prog == P_IF4_MIDH || prog == P_IF4_ENDH || prog == P_IF4_MIDQ || prog == P_IF4_ENDQ;  // rows kernel only
-  const bool old_kernel = !half && (ev ? ev[0] == '1' : !(prog == P_IF4_MID || prog == P_IF4_END || nl->kind != 0));
+  const bool old_kernel = !half && ev != nullptr && ev[0] == '1';
   if (!old_kernel && rows_slice_ok(n0, true)) {
     // full-K CTAs (rows_slice_kernel): element (q, i) of the axis-0 data at i * Q + q
     RowsSliceArgs R{};
