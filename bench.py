@@ -285,8 +285,8 @@ def gemm_roofline(torch, w, scheme_fields=2):
             # dram__bytes_read.sum + dram__bytes_write.sum of one 2-field launch, ncu --set full
             # (profiles/r01f_ncu_full_step_kernels.txt; ncu flushes caches, so this is the
             # cold upper bound -- in the step the operands are L2-resident)
-            "traffic": 9.94e6, "traffic_unit": "bytes per launch",
-            "traffic_source": "profiles/r01f_ncu_full_step_kernels.txt (cold-cache ncu capture)",
+            "traffic": 9.947392e6, "traffic_unit": "bytes per launch",
+            "traffic_source": "profiles/r01g_ncu_full_step_kernels.txt (cold-cache ncu capture)",
             "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
                       "accumulators): 2-field axis-0 product of the if4 step (E1/2 [u, g1]), M=N=K=512 complex "
                       "per field, "

@@ -7,4 +7,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 bash tools/all_configs.sh > gpurun_out/g_configs.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/g_launches.csv python tools/prof_step.py if4 40 > gpurun_out/g_ncu1.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ozgemm_persistent|rows_slice" --launch-skip 40 -c 8 -o gpurun_out/g_full python tools/prof_step.py if4 40 > gpurun_out/g_ncu2.log 2>&1
-tail -3 gpurun_out/g_pytest.log gpurun_out/g_bench.log gpurun_out/g_ref.log gpurun_out/g_smoke.log
+tail -n 3 gpurun_out/g_pytest.log gpurun_out/g_bench.log gpurun_out/g_ref.log gpurun_out/g_smoke.log
