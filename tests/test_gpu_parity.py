@@ -320,6 +320,35 @@ def test_c2_full_size_one_step_vs_oracle(P):
     assert rel_l2(res.fields[0], ref.fields[0]) <= 1e-12
 
 
+def test_c2_full_run_vs_reference(P):
+    """C2 in full (256^3 Neumann, split4, tau = 0.01, 100 steps) against the
+    REAL reference's run (tests/golden/make_golden_c2_full.py): relative L2 on
+    a fixed strided sample of the final field (4096 points spread over every
+    axis residue) and on the global squared norm and sum (checksums that see
+    every point); bar 1e-10 (north star)."""
+    path = os.path.join(GOLDEN, "C2_full_split4.npz")
+    if not os.path.exists(path):
+        pytest.skip("C2 full-run fixture not generated")
+    from paper_2403_02816_b200 import workloads as W
+    g = np.load(path)
+    meta = json.loads(str(g["meta"]))
+    w = W.CONFIGS["C2"]
+    assert meta["steps"] == w.steps and meta["extents"] == list(w.extents)
+    u0 = W.initial_state(w)
+    res = P.integrate(W.build_problem(w), "split4", (u0,), w.tau * w.steps, w.steps)
+    assert res.diverged == meta["diverged"] and res.diverged_at == meta["diverged_at"]
+    out = res.fields[0]
+    s = out.reshape(-1, order="F")[meta["offset"]::meta["stride"]]
+    assert s.shape == g["sample"].shape
+    assert rel_l2(s, g["sample"]) <= 1e-10
+    norm2 = float(np.vdot(out, out).real)
+    assert abs(norm2 - float(g["norm2"])) <= 1e-10 * float(g["norm2"])
+    total, ref_total = complex(out.sum()), complex(g["total"])
+    assert abs(total - ref_total) <= 1e-10 * np.sqrt(out.size * float(g["norm2"]))
+    del out, res
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("gemm", ["oz", "dmma"])
 def test_nonfinite_input_propagates(P, gemm, monkeypatch):
     """A NaN in the state must surface as "non-finite state" at step 1 on both
