@@ -349,6 +349,33 @@ def test_c2_full_run_vs_reference(P):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("scheme", ["strang", "if4"])
+def test_c3_full_grid_steps_vs_reference(P, scheme):
+    """C3 on its full 512^3 Fourier grid: the first steps of if4 and strang
+    against the REAL reference's run of the same steps
+    (tests/golden/make_golden_c3_steps.py; the 100-step reference run is
+    hours on pocketfft).  Strided sample + global norm and sum, bar 1e-10."""
+    path = os.path.join(GOLDEN, "C3_steps.npz")
+    if not os.path.exists(path):
+        pytest.skip("C3 full-grid fixture not generated")
+    from paper_2403_02816_b200 import workloads as W
+    g = np.load(path)
+    meta = {m["scheme"]: m for m in json.loads(str(g["meta"]))}[scheme]
+    w = W.CONFIGS["C3"]
+    assert meta["extents"] == list(w.extents)
+    x0 = W.state_for_problem(w, W.initial_state(w))
+    res = P.integrate(W.build_problem(w), scheme, (x0,), w.tau * meta["steps"], meta["steps"])
+    assert res.diverged == meta["diverged"] and res.diverged_at == meta["diverged_at"]
+    out = res.fields[0]
+    s = out.reshape(-1, order="F")[meta["offset"]::meta["stride"]]
+    assert rel_l2(s, g[f"{scheme}_sample"]) <= 1e-10
+    ref_norm2 = float(g[f"{scheme}_norm2"])
+    assert abs(float(np.vdot(out, out).real) - ref_norm2) <= 1e-10 * ref_norm2
+    assert abs(complex(out.sum()) - complex(g[f"{scheme}_total"])) <= 1e-10 * np.sqrt(out.size * ref_norm2)
+    del out, res, x0
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("gemm", ["oz", "dmma"])
 def test_nonfinite_input_propagates(P, gemm, monkeypatch):
     """A NaN in the state must surface as "non-finite state" at step 1 on both
