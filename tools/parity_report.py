@@ -41,3 +41,29 @@ for form in ("quad", "ref"):
         err = rel_l2(r.fields[0][fin], want[fin]) if fin.any() else 0.0
         print(json.dumps({"case": tag, "if4_form": form, "rel_l2": err,
                           "diverged": r.diverged, "diverged_at": r.diverged_at}), flush=True)
+
+# Full-size runs from the real reference kept as strided samples + checksums
+# (tests/golden/make_golden_c2_full.py, make_golden_c3_steps.py).
+os.environ["CGL_IF4_FORM"] = "quad"
+sampled = []
+p2 = os.path.join(GOLDEN, "C2_full_split4.npz")
+if os.path.exists(p2):
+    g = np.load(p2)
+    sampled.append(("C2_full_split4", "C2", "split4", json.loads(str(g["meta"])), g["sample"], g["norm2"]))
+p3 = os.path.join(GOLDEN, "C3_steps.npz")
+if os.path.exists(p3):
+    g = np.load(p3)
+    for m in json.loads(str(g["meta"])):
+        s = m["scheme"]
+        sampled.append((f"C3_full_{s}_{m['steps']}steps", "C3", s, m, g[f"{s}_sample"], g[f"{s}_norm2"]))
+for tag, key, scheme, m, want, norm2 in sampled:
+    w = W.CONFIGS[key]
+    x0 = W.state_for_problem(w, W.initial_state(w))
+    r = P.integrate(W.build_problem(w), scheme, (x0,), w.tau * m["steps"], m["steps"])
+    out = r.fields[0]
+    got = out.reshape(-1, order="F")[m["offset"]::m["stride"]]
+    print(json.dumps({"case": tag, "if4_form": "quad", "rel_l2_sample": rel_l2(got, want),
+                      "rel_norm2": abs(float(np.vdot(out, out).real) - float(norm2)) / float(norm2),
+                      "sample_points": int(want.size), "diverged": r.diverged,
+                      "diverged_at": r.diverged_at}), flush=True)
+    del out, r, x0
