@@ -1,35 +1,45 @@
 """Benchmark of the CGL hot path on B200 (driver contract: one JSON line).
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-2D cubic CGL, 512x512 interior points, 2nd-order FD Dirichlet, complex128,
-Lawson-RK4 (`if4`), tau = 0.005, 400 time steps, seeded u0 (workloads.C1).
+Headline workload (one workload for every N): BASELINE.json
+configs[3] = C3, the 3D periodic cubic CGL on a 512^3 Fourier grid,
+complex128, seeded random-phase u0, Lawson-RK4 (`if4`), tau = 0.01, 100 time
+steps -- the largest configuration BASELINE times on one GPU, and slab-sharded
+(distributed 3D FFT, NCCL all-to-all) at N > 1.  BASELINE quotes its metric on
+no single config; C0, C1, C2 and C4 are reported as driver-clocked extras in
+the same line (`per_config`).
 
-One bench "step" = one full `integrate()` run of that workload (400 time
-steps).  Metric = grid-point-steps/s = N_points * time_steps / second over
-the stepping loop (the reference's own timing scope, integrators.py:258-281,
-prepare excluded).
-  value   device time (CUDA events) of the loop, state resident in HBM, L2
-          flushed between bench steps (256 MiB write); max over ranks.
-  e2e     the public API with HOST input/output (pinned host tensor in,
-          numpy out): H2D + loop + D2H inside the timed region.
-  roofline  the DMMA mu-mode-product GEMM (dominant kernel): algorithmic
-          8*n flops per point per product, timed per launch with CUDA events
-          on the C1 shapes, against the FP64 DMMA peak measured live by
-          cgl_probe_dmma in the same process.
-  cpu_baseline  the CPU oracle port (numpy/OpenBLAS, same algorithm as the
-          reference) on a bounded sample of the same workload, rank 0, N=1.
+One bench "step" = one full `integrate()` run of the workload (100 time
+steps).  Metric = grid-point-steps/s = N_points * time_steps / second over the
+stepping loop (the reference's timing scope, integrators.py:258-281; prepare
+excluded).
+  value   device time (CUDA events) of the loop, state resident in HBM (the
+          2 GiB state is larger than L2; L2 is also flushed between runs);
+          max over ranks.
+  e2e     the public API with HOST buffers: pinned host state in, numpy out
+          (H2D + loop + D2H inside the timed region).
+  roofline  the dominant kernel of the step, timed live with CUDA events on its
+          stream, against the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+          algorithmic bytes per launch are DESIGN.md's per-point figure x points.
+  cpu_baseline  the CPU oracle port (numpy/OpenBLAS + pocketfft on all host
+          threads; the reference algorithm, pinned to its outputs) on a bounded
+          sample: time steps of the same workload, rank 0, N = 1.
 
---impl reference runs that CPU port instead (the reference is pure Python
-+ numpy and cannot travel to the box; oracle/cgl_oracle.py restates it and
-is pinned to the reference's own outputs by tests/test_oracle_golden.py).
+--impl reference: the reference's CPU implementation of the path (the oracle
+port; the reference is pure Python + numpy, /root/reference does not travel to
+the box) on the same workload, rank 0 only.  That arm never imports the product
+library.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (one process per GPU, NCCL).
 """
 
 import argparse
+import dataclasses
 import json
 import os
+import socket
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -37,28 +47,58 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-FP64_PEAK_RECORDED = 37.06  # TFLOP/s, tools/fp64_peak.cu on this pool (profiles/fp64_peak_r01.txt)
 METRIC = "grid-point-steps/s"
 UNIT = "gp-steps/s"
+# algorithmic HBM bytes per grid point per time step:
+# Fourier if4 = 8 FFTs x 32 B + 7 extra 16-B operand reads; strang = 4 x 32 B
+FOURIER_BYTES = {"if4": 368, "strang": 128}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="C1")
+    ap.add_argument("--workload", default="C3")
     ap.add_argument("--scheme", default=None)
-    ap.add_argument("--no-extras", action="store_true", help="skip strang/rk4 side runs and the CPU sample")
-    ap.add_argument("--cpu-sample-steps", type=int, default=24)
-    ap.add_argument("--time-steps", type=int, default=0, help="override the workload's step count (3D configs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip per_config side runs and the CPU sample")
+    ap.add_argument("--cpu-sample-steps", type=int, default=1,
+                    help="time steps of the workload per CPU bench step (scaled up for small grids)")
+    ap.add_argument("--time-steps", type=int, default=0, help="override the workload's step count")
     ap.add_argument("--sharded", action="store_true", help="use the slab-sharded 3D path even at N = 1")
     return ap.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def spawn_ranks(args):
+    """`--gpus N` under plain python: re-exec under torch.distributed.run (one
+    rank per GPU, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def workload(args):
+    from paper_2403_02816_b200 import workloads as W  # host-side only: maps no library
+    w = W.CONFIGS[args.workload]
+    if args.time_steps:
+        w = dataclasses.replace(w, steps=args.time_steps)
+    return w, args.scheme or w.schemes[0]
+
+
+def config_dict(w, scheme, world, parallelism=None):
+    return {"workload": w.name, "grid": list(w.extents), "boundary": w.boundary, "scheme": scheme,
+            "tau": w.tau, "time_steps": w.steps, "dtype": "complex128",
+            "bench_step": f"one integrate() run = {w.steps} {scheme} time steps",
+            "l2": "inputs larger than L2 (16 B x points per field); L2 also flushed (256 MiB write) between runs",
+            "parallelism": parallelism or (f"replicas x{world}" if world > 1 else "single")}
 
 
 # ---------------------------------------------------------------------------
@@ -72,34 +112,52 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def cpu_sample_steps(w, per_bench_step):
+    """Time steps per CPU sample: `per_bench_step` at 512^3-class grids, more
+    for small grids (about the same CPU work)."""
+    return max(1, min(w.steps, int(per_bench_step * (1 << 27) / w.points)))
+
+
 def oracle_run(w, scheme, max_steps):
+    """The oracle port of the reference `integrate` on the workload's seeded
+    input for at most `max_steps` steps; returns (loop seconds, steps done)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import cgl_oracle as O
     from paper_2403_02816_b200 import workloads as W
     from threadpoolctl import threadpool_limits
+    O.FFT_WORKERS = cpu_cores()
     p = O.Params(**{k: getattr(w.params, k) for k in O.Params.NAMES})
     u0 = W.initial_state(w)
     if w.boundary == "periodic":
         blocks = [O.FourierOp(O.symbol(w.extents, (w.interval,) * len(w.extents), p))]
-        x0 = np.fft.fftn(u0)
+        x0 = O._fftn(u0)
     else:
         a, b = w.interval
         d = len(w.extents)
         blocks = [O.KronOp([p.diffusion * O.FD_BUILDERS[w.boundary](n, b - a) + (p.alpha2 / d) * np.eye(n)
                             for n in w.extents])]
         x0 = u0
+    del u0
     with threadpool_limits(limits=cpu_cores()):
         res = O.integrate(O.Prob(blocks, w.kind, p), scheme, (x0,), w.t_final, w.steps, max_steps=max_steps)
     done = res.diverged_at if res.diverged else min(w.steps, max_steps)
     return res.seconds, done
 
 
+def cpu_sample_desc(w, scheme, n, cores):
+    return (f"{n} of {w.steps} {scheme} time steps per sample on {list(w.extents)} (oracle/cgl_oracle.py: the "
+            f"reference algorithm on numpy {np.__version__} + OpenBLAS zgemm, pocketfft via scipy.fft, "
+            f"{cores} host threads)")
+
+
 def reference_arm(args, w, scheme):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sample = max(1, int((args.cpu_sample_steps // 3) * (1 << 18) / w.points))
-    for _ in range(args.warmup):
+    sample = cpu_sample_steps(w, args.cpu_sample_steps)
+    # numpy has nothing to warm beyond the first call: one warm-up sample at most
+    # (a 512^3 time step is tens of seconds of CPU work)
+    for _ in range(min(args.warmup, 1)):
         oracle_run(w, scheme, sample)
     tot_s, tot_steps = 0.0, 0
     for _ in range(args.steps):
@@ -110,23 +168,15 @@ def reference_arm(args, w, scheme):
     cores = cpu_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": config_dict(w, scheme, world),
+        "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot_s / args.steps,
+        "ms_per_time_step": 1e3 * tot_s / max(tot_steps, 1),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic", "config": config_dict(w, scheme, world),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} of {w.steps} {scheme} time steps per bench step on {w.extents} "
-                                   f"(oracle/cgl_oracle.py, numpy {np.__version__}, OpenBLAS {cores} threads)"},
+                         "sample": cpu_sample_desc(w, scheme, sample, cores)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def config_dict(w, scheme, world):
-    return {"workload": w.name, "grid": list(w.extents), "boundary": w.boundary, "scheme": scheme,
-            "tau": w.tau, "time_steps": w.steps, "dtype": "complex128",
-            "bench_step": f"one integrate() run = {w.steps} {scheme} time steps",
-            "l2": "flushed (256 MiB write) between bench steps; within a run the state stays resident",
-            "parallelism": f"replicas x{world}" if world > 1 else "single"}
 
 
 # ---------------------------------------------------------------------------
@@ -182,8 +232,21 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def flush_l2(buf):
-    buf.zero_()
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def hbm_peak():
+    """(GB/s, source): the measured copy bandwidth, else the recipe's fallback."""
+    pk = peaks()
+    for k in ("hbm_gbs", "hbm_gbps", "hbm_copy_gbps"):
+        if k in pk:
+            return float(pk[k]), f"MEASURED_PEAKS.json {k}"
+    return 6540.5, "fallback (SURVEY.md 0.5 measured copy bandwidth)"
 
 
 def _events(torch):
@@ -217,15 +280,52 @@ def _graphed(torch, fn):
     return g.replay
 
 
+def fourier_roofline(torch, w, scheme, step_seconds):
+    """Dominant kernel of the Fourier step: the pencil-FFT pass (csrc/fftpass.cu)
+    along the strided middle axis, timed per launch with CUDA events inside a
+    captured graph; 32 algorithmic bytes per point per pass (one read + one
+    write of the 16-B state).  The whole-step algorithmic-byte rate
+    (368 B/pt if4, 128 B/pt strang) rides along."""
+    from paper_2403_02816_b200 import fftpass
+    peak, src = hbm_peak()
+    n = w.points
+    x = torch.empty(w.extents, dtype=torch.complex128, device="cuda")
+    x.real.normal_()
+    x.imag.normal_()
+    y = torch.empty_like(x)
+    reps = 8
+
+    def rep():
+        for _ in range(reps):
+            fftpass.axis_pass(x, y, axis=1, inverse=False)
+    dt = _time(torch, _graphed(torch, rep), reps=5) / reps
+    achieved = 32.0 * n / dt / 1e9
+    step_bytes = FOURIER_BYTES.get(scheme, 0) * n
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None,
+            "kernel": "cgl::fft_pass_kernel (axis-1 pencils of 512, radix-8 x3 in registers/SMEM, FP64)",
+            "algorithmic_bytes_per_launch": 32 * n, "per_launch_ms": dt * 1e3, "peak_source": src,
+            "step_level": {"algorithmic_bytes_per_step": step_bytes,
+                           "achieved_gbps": step_bytes / step_seconds / 1e9 if step_seconds else None,
+                           "frac": step_bytes / step_seconds / 1e9 / peak if step_seconds else None}}
+
+
+def step_roofline(w, scheme, step_seconds):
+    peak, src = hbm_peak()
+    step_bytes = FOURIER_BYTES.get(scheme, 0) * w.points
+    a = step_bytes / step_seconds / 1e9
+    return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": None,
+            "kernel": f"whole {scheme} time step (algorithmic {FOURIER_BYTES.get(scheme)} B/pt)",
+            "peak_source": src}
+
+
 def gemm_roofline(torch, w, scheme_fields=2):
-    """Dominant kernel of the if4 step: the 2-field axis-0 (left-form) product
-    of the quad-form step ([A, G] = E1/2 [u, g1]; all four products of a step
-    are 2-field)
-    on the INT8 tensor cores (ozgemm_persistent_kernel), timed per launch with CUDA
-    events on the workload shapes, data pre-sliced as in the step.  Reported
-    against the INT8 dense tensor peak on EXECUTED int8 MACs (block skipping
-    counted out), plus the FP64-equivalent view against the measured DMMA
-    peak (what the FP64 tensor path could reach on the same product)."""
+    """C1's dominant kernel: the 2-field axis-0 product E1/2 [u, g1] of the
+    quad-form if4 step on the INT8 tensor cores (ozgemm_persistent_kernel),
+    timed per launch inside a captured graph, data pre-sliced as in the step.
+    Executed int8 MACs (block skipping counted out) against the dense INT8
+    tcgen05 rate measured on this pool (tools/mma_rate.cu: 8192 MAC/clk/SM)
+    at the sampled SM clock, plus 2 x bf16 from MEASURED_PEAKS.json."""
     from paper_2403_02816_b200 import _lib, ozaki, workloads as W
     lib = _lib.load()
     n = w.extents[0]
@@ -236,7 +336,7 @@ def gemm_roofline(torch, w, scheme_fields=2):
     ins = [torch.randn(w.extents, dtype=torch.complex128, device="cuda", generator=g) for _ in range(scheme_fields)]
     outs = [torch.empty_like(x) for x in ins]
     ws = ozaki.Workspace()
-    ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws)  # slices the data into ws
+    ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws)
     Q = w.points // n
     per = lib.cgl_oz_slice_bytes(ozaki.S, Q, n, 0)
     Bs = [ws.bufs[("D", f, n)][0] for f in range(scheme_fields)]
@@ -247,59 +347,27 @@ def gemm_roofline(torch, w, scheme_fields=2):
                                    _lib.ptr_array([fac.A] * scheme_fields), _lib.ptr_array([fac.Ae] * scheme_fields),
                                    _lib.ptr_array([fac.Az] * scheme_fields), _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                    None, _lib.ptr_array(outs), Q, 1, 0, 0, per, Q, n * Q, None, 0), "oz_gemm")
-    # per-launch time as in the step: 10 back-to-back launches inside one
-    # captured graph (programmatic dependent launch between them, no
-    # graph-launch gap), event time / 10
     reps_in_graph = 10
 
     def gemm_rep():
         for _ in range(reps_in_graph):
             gemm_only()
-
-    def product_rep():
-        for _ in range(reps_in_graph):
-            ozaki.mode_product_oz(ins, [fac] * scheme_fields, outs, 0, ws)
     dt = _time(torch, _graphed(torch, gemm_rep)) / reps_in_graph
-    dt_with_slicing = _time(torch, _graphed(torch, product_rep)) / reps_in_graph
     bn = ozaki.geometry()[1]
     macs = ozaki.executed_macs_left(fac, (Q + bn - 1) // bn, scheme_fields)
-    dense = ozaki.dense_macs(n, Q, n, scheme_fields)
-    # live FP64 DMMA peak
-    stream = _lib.stream()
-    lib.cgl_probe_dmma(stream, 256)
-    best = 0.0
-    for _ in range(3):
-        e0, e1 = _events(torch)
-        e0.record()
-        fl = lib.cgl_probe_dmma(stream, 4096)
-        e1.record()
-        torch.cuda.synchronize()
-        best = max(best, fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-    int8_peak = 2.0 * peaks["bf16_tflops"]
+    props = torch.cuda.get_device_properties(0)
+    sm_mhz = 1965.0
+    mma_peak = 2.0 * 8192 * props.multi_processor_count * sm_mhz * 1e6 / 1e12
     achieved = 2.0 * macs / dt / 1e12
-    fp64_alg = 8.0 * n * w.points * scheme_fields / dt / 1e12
-    return {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS (int8)",
-            "frac": achieved / int8_peak,
-            # dram__bytes_read.sum + dram__bytes_write.sum of one 2-field launch, ncu --set full
-            # (profiles/r01f_ncu_full_step_kernels.txt; ncu flushes caches, so this is the
-            # cold upper bound -- in the step the operands are L2-resident)
-            "traffic": 9.947392e6, "traffic_unit": "bytes per launch",
-            "traffic_source": "profiles/r01g_ncu_full_step_kernels.txt (cold-cache ncu capture)",
-            "kernel": "ozgemm_persistent_kernel<8,32,4> (tcgen05.mma kind::i8, double-buffered TMEM level "
-                      "accumulators): 2-field axis-0 product of the if4 step (E1/2 [u, g1]), M=N=K=512 complex "
-                      "per field, "
-                      "S=8 int8 slices",
-            "per_launch_ms": dt * 1e3, "per_launch_ms_incl_data_slicing": dt_with_slicing * 1e3,
-            "executed_int8_macs_per_launch": macs, "dense_int8_macs_per_launch": dense,
-            "block_skip_fraction": 1.0 - macs / dense,
-            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2x BF16 on B200, "
-                           "B200_PROFILING.md nominal table); no measured INT8 figure exists",
-            "fp64_equivalent": {"achieved_tflops": fp64_alg, "dmma_peak_tflops": best,
-                                "ratio_vs_dmma_peak": fp64_alg / best,
-                                "note": "algorithmic 8*n flops per point per product; the FP64 tensor path "
-                                        "(zgemm_kernel, DMMA) reaches ~32 TFLOP/s on this product"}}
+    return {"bound": "tensor", "achieved": achieved, "peak": mma_peak, "unit": "TOPS (int8)",
+            "frac": achieved / mma_peak, "per_launch_ms": dt * 1e3,
+            "kernel": "ozgemm_persistent_kernel<8,32,4>: 2-field axis-0 product of the C1 if4 step",
+            "peak_source": "tools/mma_rate.cu measured tcgen05 kind::i8 rate 8192 MAC/clk/SM x 148 SMs x 1965 MHz",
+            "frac_vs_2x_bf16": achieved / (2.0 * peaks().get("bf16_tflops", 1640.0))}
+
+
+def launches(lib, prob):
+    return lib.cgl_launch_count() + sum(fp.replayed_launches for fp in getattr(prob, "_plans", {}).values())
 
 
 def gpu_arm(args, w, scheme):
@@ -314,9 +382,7 @@ def gpu_arm(args, w, scheme):
     lib = _lib.load()
 
     prob = W.build_problem(w)
-    u0 = W.initial_state(w)
-    x0_host = W.state_for_problem(w, u0)
-    x0 = torch.from_numpy(np.ascontiguousarray(x0_host)).cuda()
+    x0 = W.state_for_problem(w, W.initial_state_device(w))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     for _ in range(args.warmup):
@@ -324,17 +390,15 @@ def gpu_arm(args, w, scheme):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    n_launch0 = lib.cgl_launch_count()
-    replay0 = sum(fp.replayed_launches for fp in getattr(prob, "_plans", {}).values())
+    l0 = launches(lib, prob)
     dev_total = 0.0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush_l2(flush)
+            flush.zero_()
             torch.cuda.synchronize()
             r = P.integrate(prob, scheme, (x0,), w.t_final, w.steps)
             dev_total += r.device_seconds
-    launches = lib.cgl_launch_count() - n_launch0 + sum(
-        fp.replayed_launches for fp in getattr(prob, "_plans", {}).values()) - replay0
+    n_launch = launches(lib, prob) - l0
     torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([dev_total], dtype=torch.float64, device="cuda")
@@ -344,11 +408,11 @@ def gpu_arm(args, w, scheme):
     value = world * w.points * steps_done * args.steps / dev_total
 
     # e2e through the public API with host buffers (pinned host tensor in, numpy out)
-    x_pinned = torch.from_numpy(np.ascontiguousarray(x0_host)).pin_memory()
+    x_pinned = x0.cpu().pin_memory()
     P.integrate(prob, scheme, (x_pinned,), w.t_final, w.steps)
     e2e_total = 0.0
     for _ in range(args.steps):
-        flush_l2(flush)
+        flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r2 = P.integrate(prob, scheme, (x_pinned,), w.t_final, w.steps)
@@ -360,107 +424,179 @@ def gpu_arm(args, w, scheme):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e = world * w.points * steps_done * args.steps / e2e_total
+    del x_pinned, r2
 
+    step_s = dev_total / args.steps / max(steps_done, 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps,
+        "ms_per_time_step": 1e3 * step_s, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": config_dict(w, scheme, world),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16 * w.points,
                 "d2h_bytes_per_step": 16 * w.points, "ms_per_step": 1e3 * e2e_total / args.steps},
-        "gpu_launches": int(launches),
+        "gpu_launches": int(n_launch),
         "clocks": clk.summary(),
         "diverged": bool(r.diverged),
     }
     if rank == 0:
         try:
-            line["roofline"] = gemm_roofline(torch, w)
+            if w.boundary == "periodic":
+                line["roofline"] = fourier_roofline(torch, w, scheme, step_s)
+            else:
+                line["roofline"] = gemm_roofline(torch, w)
         except Exception as e:  # keep the bench line even if the probe fails
             line["roofline"] = {"error": repr(e)}
-        if not args.no_extras:
-            extras = {}
-            for s in w.schemes:
-                if s == scheme:
-                    continue
-                P.integrate(prob, s, (x0,), w.t_final, w.steps)
-                rr = P.integrate(prob, s, (x0,), w.t_final, w.steps)
-                done = rr.diverged_at if rr.diverged else w.steps
-                extras[s] = {"value": w.points * done / rr.device_seconds, "unit": UNIT,
-                             "ms_per_time_step": 1e3 * rr.device_seconds / max(done, 1),
-                             "diverged": rr.diverged, "diverged_at": rr.diverged_at, "reason": rr.reason}
-            line["per_stepper"] = extras
-            if world == 1:
-                # bounded CPU sample: ~24 C1-sized time steps worth of work
-                sample = max(1, int(args.cpu_sample_steps * (1 << 18) / w.points))
-                s_cpu, n_cpu = oracle_run(w, scheme, sample)
-                line["cpu_baseline"] = {"value": w.points * n_cpu / s_cpu, "unit": UNIT, "cores": cpu_cores(),
-                                        "kind": "port",
-                                        "sample": f"{n_cpu} of {w.steps} {scheme} time steps on {w.extents} "
-                                                  f"(oracle/cgl_oracle.py = reference algorithm on numpy/OpenBLAS)"}
+            if w.boundary == "periodic":
+                line["roofline"].update(step_roofline(w, scheme, step_s))
+        del prob, x0, r
+        if not args.no_extras and world == 1:
+            line["per_config"] = per_config(torch, P, W, skip=(w.name, scheme))
+            sample = cpu_sample_steps(w, args.cpu_sample_steps)
+            s_cpu, n_cpu = oracle_run(w, scheme, sample)
+            line["cpu_baseline"] = {"value": w.points * n_cpu / s_cpu, "unit": UNIT, "cores": cpu_cores(),
+                                    "kind": "port", "sample": cpu_sample_desc(w, scheme, n_cpu, cpu_cores())}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
+EXTRAS = (("C0", "strang", None), ("C1", "if4", None), ("C1", "strang", None), ("C1", "rk4", None),
+          ("C1", "rk4", 0.001), ("C2", "split4", None), ("C3", "strang", None), ("C4", "if4", None))
+
+
+def per_config(torch, P, W, skip=()):
+    """Every other BASELINE config, one warm run + one timed run each
+    (device time of the full integrate() loop)."""
+    out = {}
+    for cfg, scheme, tau in EXTRAS:
+        w = W.CONFIGS[cfg]
+        if (w.name, scheme) == skip and tau is None:
+            continue
+        if tau is not None:
+            w = dataclasses.replace(w, tau=tau)
+        key = f"{cfg}/{scheme}" + (f"@tau={tau}" if tau else "")
+        try:
+            prob = W.build_problem(w)
+            x0 = W.state_for_problem(w, W.initial_state_device(w))
+            P.integrate(prob, scheme, (x0,), w.t_final, w.steps)
+            r = P.integrate(prob, scheme, (x0,), w.t_final, w.steps)
+            done = r.diverged_at if r.diverged else w.steps
+            out[key] = {"value": w.points * done / r.device_seconds, "unit": UNIT,
+                        "ms_per_time_step": 1e3 * r.device_seconds / max(done, 1), "time_steps": w.steps,
+                        "grid": list(w.extents), "tau": w.tau, "diverged": bool(r.diverged),
+                        "diverged_at": int(r.diverged_at), "reason": r.reason}
+            del prob, x0, r
+        except Exception as e:
+            out[key] = {"error": repr(e)}
+        torch.cuda.empty_cache()
+    return out
+
+
 def sharded_arm(args, w, scheme):
-    """3D configs at N > 1: axis-0 slab sharding (FD: NCCL all-to-all inside the
-    axis-0 mode product; Fourier: distributed 3D FFT).  Strong scaling: the
-    global grid is fixed; value = global points x steps / max-over-ranks time."""
+    """3D configs at N > 1: axis-0 slab sharding (FD: all-to-all transposes
+    around the axis-0 product; Fourier: distributed 3D FFT).  Strong scaling:
+    the global grid is fixed; value = global points x steps / max-over-ranks
+    device time of the stepping loop."""
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2403_02816_b200 import SCHEMES, distributed as D, slabfourier as SF, workloads as W
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    else:
+        group = None
+    from paper_2403_02816_b200 import SCHEMES, _lib, distributed as D, slabfourier as SF, workloads as W
     from paper_2403_02816_b200.spectral import dft_forward, dft_inverse
-    steps = args.time_steps or w.steps
-    wl = w.scaled(w.extents[0], steps) if steps != w.steps else w
-    prob = W.build_problem(wl)
-    u0 = W.initial_state_device(wl)
-    times = []
-    for it in range(args.warmup + args.steps):
-        torch.cuda.synchronize()
-        dist.barrier()
-        if wl.boundary == "periodic":
-            prob.prepare(wl.tau, SCHEMES[scheme])
-            uhat = dft_forward(u0)
-            plan = SF.ShardedFourierPlan(prob, scheme, wl.extents, world, [rank], dist.group.WORLD)
-            x0 = SF.split_global(uhat if scheme == "if4" else dft_inverse(uhat), world,
-                                 "cols" if scheme == "if4" else "slabs")[rank:rank + 1]
-            del uhat
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib = _lib.load()
+    prob = W.build_problem(w)
+    u0 = W.initial_state_device(w)
+    steps = w.steps
+    if w.boundary == "periodic":
+        prob.prepare(w.tau, SCHEMES[scheme])
+        uhat = dft_forward(u0)
+        layout = "cols" if scheme == "if4" else "slabs"
+        x_local = SF.split_global(uhat if scheme == "if4" else dft_inverse(uhat), world, layout)[rank]
+        del uhat
+        plan = SF.ShardedFourierPlan(prob, scheme, w.extents, world, [rank], group)
+
+        def run(x):
+            e0, e1 = _events(torch)
             e0.record()
-            plan.run(x0, steps, wl.tau)
+            key = plan.run([x], steps, w.tau)
             e1.record()
             torch.cuda.synchronize()
-            dt = e0.elapsed_time(e1) / 1e3
-        else:
-            L = D.SlabLayout(wl.extents, world)
-            a, b = L.bounds(rank)
-            x0 = [u0[a:b].contiguous()]
-            _, _, _, dt = D.integrate_sharded(prob, scheme, x0, wl.t_final, steps, L, dist.group.WORLD)
-        if it >= args.warmup:
-            times.append(dt)
-    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total = float(t.item())
-    value = wl.points * steps * args.steps / total
+            out = plan.U[0] if scheme == "if4" else plan.Us[steps % 2][0]
+            return e0.elapsed_time(e1) / 1e3, key, out
+    else:
+        L = D.SlabLayout(w.extents, world)
+        a, b = L.bounds(rank)
+        x_local = u0[a:b].contiguous()
+
+        def run(x):
+            out, _, _, dt = D.integrate_sharded(prob, scheme, [x], w.t_final, steps, L, group)
+            return dt, None, out[0]
+    del u0
+    torch.cuda.empty_cache()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        run(x_local)
+    l0 = lib.cgl_launch_count()
+    total = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if group is not None:
+                dist.barrier()
+            dt, _, _ = run(x_local)
+            total += dt
+    n_launch = lib.cgl_launch_count() - l0
+    # e2e: this rank's share of the state from pinned host memory, result back to host
+    x_host = x_local.cpu().pin_memory()
+    e2e_total = 0.0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        xd = x_host.to("cuda", non_blocking=True)
+        _, _, out = run(xd)
+        _ = out.cpu().numpy()
+        torch.cuda.synchronize()
+        e2e_total += time.perf_counter() - t0
+    t = torch.tensor([total, e2e_total], dtype=torch.float64, device="cuda")
+    if group is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total, e2e_total = float(t[0]), float(t[1])
+    value = w.points * steps * args.steps / total
     if rank == 0:
-        cfg = config_dict(wl, scheme, world)
-        cfg["parallelism"] = f"axis-0 slabs x{world}"
-        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                          "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-                          "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-                          "config": cfg}), flush=True)
-    dist.destroy_process_group()
+        step_s = total / args.steps / steps
+        cfg = config_dict(w, scheme, world, parallelism=f"axis-0 slabs x{world}")
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "ms_per_time_step": 1e3 * step_s,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+                "data": "synthetic", "config": cfg,
+                "e2e": {"value": w.points * steps * args.steps / e2e_total, "unit": UNIT,
+                        "h2d_bytes_per_step": 16 * x_local.numel(), "d2h_bytes_per_step": 16 * x_local.numel(),
+                        "per": "rank (every rank copies its slab)"},
+                "gpu_launches": int(n_launch), "clocks": clk.summary()}
+        if w.boundary == "periodic":
+            rl = step_roofline(w, scheme, step_s * world)
+            rl["note"] = "per-rank HBM rate: algorithmic bytes of the rank's 1/N share over the step time"
+            line["roofline"] = rl
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
 
 
 def main():
     args = parse()
-    from paper_2403_02816_b200 import workloads as W
-    w = W.CONFIGS[args.workload]
-    scheme = args.scheme or w.schemes[0]
     _, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    w, scheme = workload(args)
     if args.impl == "reference":
         reference_arm(args, w, scheme)
     elif (world > 1 or args.sharded) and len(w.extents) == 3:

@@ -401,6 +401,28 @@ class FourierOp:
         return self.cache[Fraction(f)] * u
 
 
+# Worker threads of the n-dimensional FFTs.  1 (default, every parity use) is
+# numpy's own pocketfft exactly as the reference calls it (spectral.py:79-86);
+# bench.py's CPU legs set the host core count, which runs the same pocketfft
+# C++ transforms through scipy.fft with the batch of 1D lines split over
+# threads -- the reference algorithm with all host threads, not a different one.
+FFT_WORKERS = 1
+
+
+def _fftn(u):
+    if FFT_WORKERS > 1:
+        import scipy.fft
+        return scipy.fft.fftn(u, workers=FFT_WORKERS)
+    return np.fft.fftn(u)
+
+
+def _ifftn(u):
+    if FFT_WORKERS > 1:
+        import scipy.fft
+        return scipy.fft.ifftn(u, workers=FFT_WORKERS)
+    return np.fft.ifftn(u)
+
+
 class Prob:
     """integrators.py:62-127 (blocks = one operator per component)."""
 
@@ -411,10 +433,10 @@ class Prob:
         self.fourier = self.blocks[0].fourier
 
     def phys(self, fs):       # integrators.py:78-81
-        return tuple(np.fft.ifftn(u) for u in fs) if self.fourier else fs
+        return tuple(_ifftn(u) for u in fs) if self.fourier else fs
 
     def spec(self, fs):       # integrators.py:83-86
-        return tuple(np.fft.fftn(u) for u in fs) if self.fourier else fs
+        return tuple(_fftn(u) for u in fs) if self.fourier else fs
 
     def lin(self, fs):
         return tuple(b.apply(u) for b, u in zip(self.blocks, fs))

@@ -38,6 +38,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <mutex>
+#include <vector>
 
 #include "cgl_common.cuh"
 #include "cgl_internal.h"
@@ -333,34 +336,49 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
 // ---------------------------------------------------------------------------
 // host side: per-device persistent workspace + flags, grid sizing
 // ---------------------------------------------------------------------------
+// Stream-K partials + per-CTA flags, one state per device (GEMM launches are
+// stream-ordered: the library enqueues every product of a plan on one stream;
+// two DMMA products running concurrently on two streams would share the flags
+// and are not supported).  Buffers only grow, and a buffer that is
+// outgrown is RETIRED, never freed: CUDA graphs captured earlier (the fused step
+// plans) bake its pointers and may be replayed at any later time, so freeing it
+// would let a replay write into memory torch has reused.  The leak is
+// bounded by the geometric growth (x1.5) of the largest configuration used.
 struct StreamKState {
   double* ws = nullptr;
   int* flags = nullptr;
   size_t ws_doubles = 0;
   int nflags = 0;
-  int epoch = 0;
 };
-static StreamKState g_sk[16];
+static StreamKState g_sk[64];
+static std::vector<void*> g_sk_retired;  // kept alive for graphs that captured them
+static std::mutex g_sk_mu;
 
-static int ensure_state(int dev, size_t ws_doubles, int nflags, StreamKState** out) {
-  StreamKState& s = g_sk[dev & 15];
+static int ensure_state(int dev, cudaStream_t stream, size_t ws_doubles, int nflags, StreamKState* out) {
+  std::lock_guard<std::mutex> lock(g_sk_mu);
+  StreamKState& s = g_sk[dev & 63];
   if (s.ws_doubles < ws_doubles) {
-    if (s.ws) cudaFree(s.ws);
-    s.ws = nullptr;
-    cudaError_t e = cudaMalloc(&s.ws, ws_doubles * sizeof(double));
+    const size_t want = std::max(ws_doubles, s.ws_doubles + s.ws_doubles / 2);
+    double* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(double));
     if (e != cudaSuccess) return set_cuda_error(e, "zgemm workspace");
-    s.ws_doubles = ws_doubles;
+    if (s.ws) g_sk_retired.push_back(s.ws);
+    s.ws = p;
+    s.ws_doubles = want;
   }
   if (s.nflags < nflags) {
-    if (s.flags) cudaFree(s.flags);
-    s.flags = nullptr;
-    cudaError_t e = cudaMalloc(&s.flags, nflags * sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(s.flags, 0, nflags * sizeof(int));
+    const int want = std::max(nflags, s.nflags + s.nflags / 2);
+    int* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(int));
+    // flags are consumed and re-armed to 0 inside the kernel; a fresh buffer
+    // starts armed.  The memset is ordered before the launch on `stream`.
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, want * sizeof(int), stream);
     if (e != cudaSuccess) return set_cuda_error(e, "zgemm flags");
-    s.nflags = nflags;
-    s.epoch = 0;
+    if (s.flags) g_sk_retired.push_back(s.flags);
+    s.flags = p;
+    s.nflags = want;
   }
-  *out = &s;
+  *out = s;
   return 0;
 }
 
@@ -395,11 +413,11 @@ static int launch_cfg(GemmArgs a, int nitems, cudaStream_t s) {
   a.total_iters = units * ktiles;
   int64_t G = (int64_t)sms * occ;
   if (G > a.total_iters) G = a.total_iters;
-  StreamKState* st = nullptr;
-  int r = ensure_state(dev, (size_t)G * Cfg::PART * Cfg::NT, (int)G, &st);
+  StreamKState st;
+  int r = ensure_state(dev, s, (size_t)G * Cfg::PART * Cfg::NT, (int)G, &st);
   if (r) return r;
-  a.workspace = st->ws;
-  a.flags = st->flags;
+  a.workspace = st.ws;
+  a.flags = st.flags;
   a.epoch = 1;  // flags are re-armed to 0 by their consumer, so a constant works under graph replay
   kern<<<(unsigned)G, Cfg::NT, Cfg::SMEM, s>>>(a);
   return check_launch("zgemm_kernel");
