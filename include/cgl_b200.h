@@ -358,6 +358,44 @@ int cgl_fft_plan_many(int rank, const int64_t* n, int64_t batch, int64_t istride
                       int64_t idist, int64_t ostride, int64_t odist, void** plan);
 int cgl_fft_destroy(void* plan);
 
+/* ---- Pencil-FFT passes with fused step programs (csrc/fftpass.cu) -------- */
+/* One HBM pass of unnormalised length-shape[axis] transforms along `axis` of a
+ * C-order complex128 field (2D/3D, power-of-two extents 16..512), with the
+ * pointwise pieces of the Fourier steppers fused in (spectral.py:79-86 around
+ * integrators.py:99-120, 161-164, 205-215).  A 3D transform is three passes
+ * (axis 2 contiguous, axes 1 and 0 strided); the programs below fuse the
+ * Lawson stage combinations, g, the exact flows, the finiteness check and
+ * the separable exp(f tau symbol) multipliers into the first/last pass. */
+enum cgl_fft_program {
+  CGL_FFT_PLAIN = 0,      /* transform src -> dst (direction from `inverse`)         */
+  CGL_FFT_IF4_START = 1,  /* last axis, inverse: u (spectral state) -> dst             */
+  CGL_FFT_IF4_B1 = 2,     /* last axis: g1 = F src -> g_out; dst = F^-1 E1/2 (u + t/2 g1) */
+  CGL_FFT_IF4_B2 = 3,     /* g2 = F src -> g_out; dst = F^-1 (E1/2 u + t/2 g2)           */
+  CGL_FFT_IF4_B3 = 4,     /* g3 = F src -> g_out; dst = F^-1 (t E1/2 g3 + E1 u)          */
+  CGL_FFT_IF4_B4 = 5,     /* g4 = F src; u_out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3)
+                             + t/6 g4 (checked); dst = F^-1 u_out unless dst == NULL   */
+  CGL_FFT_G = 6,          /* dst = F g(scale * F^-1 src) along one axis                */
+  CGL_FFT_STR_START = 7,  /* strided: dst = F flow(scale * u, t/2)  [step, seq 0]      */
+  CGL_FFT_STR_A0 = 8,     /* strided: w = scale F^-1 src; u_out = flow(w, t/2) [seq 1],
+                             checked; dst = F flow(u_out, t/2) [step + 1] unless NULL  */
+  CGL_FFT_STR_MID = 9     /* last axis: dst = F^-1 (E1 .* F src)                       */
+};
+typedef struct {
+  const double* u;           /* state operand (spectral for if4, physical for strang) */
+  double* u_out;             /* state output                                        */
+  const double* g[3];        /* g1, g2, g3 (IF4_B4)                                  */
+  double* g_out;             /* g_i output (IF4_B1..B3)                              */
+  const double* tables[2][3];/* separable exp(f tau symbol): [1/2, 1][axis]           */
+  double tau, scale;
+  cgl_nonlinear_t nl;        /* scalar kinds only (cubic / cubic_quintic)            */
+  cgl_flag_t* flag;
+  uint64_t pos;
+} cgl_fft_ops_t;
+/* 1 when the pass kernels support this grid, else 0 (no error set). */
+int cgl_fft_pass_supported(int ndim, const int64_t* shape);
+int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse,
+                 const double* src, double* dst, const cgl_fft_ops_t* ops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,16 @@ class OzPrologue(ctypes.Structure):
 
 PRO_SLICE = -1
 
+
+class FftOps(ctypes.Structure):
+    """cgl_fft_ops_t (include/cgl_b200.h): operands of a fused pencil-FFT pass."""
+    _fields_ = [("u", c_ptr), ("u_out", c_ptr), ("g", c_ptr * 3), ("g_out", c_ptr), ("tables", (c_ptr * 3) * 2),
+                ("tau", c_dbl), ("scale", c_dbl), ("nl", Nonlinear), ("flag", c_ptr), ("pos", c_u64)]
+
+
+FFT_PROGRAMS = {"plain": 0, "if4_start": 1, "if4_b1": 2, "if4_b2": 3, "if4_b3": 4, "if4_b4": 5, "g": 6,
+                "str_start": 7, "str_a0": 8, "str_mid": 9}
+
 _SIGS = {
     "cgl_oz_gemm_fused": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                                   c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64, c_int,
@@ -131,6 +141,8 @@ _SIGS = {
     "cgl_fft_plan": (c_int, [c_int, c_ptr, ctypes.POINTER(c_ptr)]),
     "cgl_fft_exec": (c_int, [c_ptr, c_ptr, c_ptr, c_ptr, c_int]),
     "cgl_fft_destroy": (c_int, [c_ptr]),
+    "cgl_fft_pass_supported": (c_int, [c_int, c_ptr]),
+    "cgl_fft_pass": (c_int, [c_ptr, c_int, c_int, c_ptr, c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(FftOps)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -336,6 +336,16 @@ int cgl_stage_fourier_cols(void* stream, int program, int nfields, int ndim, con
                       ndim, shape, tables, cols, col_offset);
 }
 
+int cgl_fft_pass_supported(int ndim, const int64_t* shape) {
+  return shape && fft_pass_supported(ndim, shape) ? 1 : 0;
+}
+
+int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse, const double* src,
+                 double* dst, const cgl_fft_ops_t* ops) {
+  if (!shape) return set_error(CGL_EINVAL, "fft_pass: null shape");
+  return fft_pass_launch((cudaStream_t)stream, program, ndim, shape, axis, inverse, src, dst, ops);
+}
+
 int64_t cgl_oz_slice_bytes(int S, int64_t rows, int64_t cols, int a_mode) {
   return oz_slice_bytes(S, rows, cols, a_mode, a_mode ? kOzBM : kOzBN);
 }

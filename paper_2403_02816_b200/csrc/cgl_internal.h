@@ -51,6 +51,11 @@ int rows_slice_plain(cudaStream_t st, int nitems, const double* const* srcs, int
                      int64_t K, int64_t batch, int64_t src_bs, int8_t* const* outs, int64_t out_bs,
                      int* const* exps, int64_t exp_bs);
 
+// pencil-FFT passes (fftpass.cu)
+bool fft_pass_supported(int ndim, const int64_t* shape);
+int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, int axis, int inverse,
+                    const double* src, double* dst, const cgl_fft_ops_t* ops);
+
 // error plumbing (capi.cu)
 // Launch with the programmatic-dependent-launch attribute (CGL_PDL=0
 // disables) and an optional thread-block cluster shape.  Every kernel

@@ -1,0 +1,492 @@
+// Pencil-FFT passes for the periodic (Fourier pseudospectral) path, sm_100a.
+//
+// The reference transforms with numpy's pocketfft (spectral.py:79-86,
+// `np.fft.fftn` / `ifftn`) around every pointwise nonlinear evaluation
+// (integrators.py:99-120: Problem.g / Problem.flow on a Fourier operator
+// are F g F^-1).  A 3D transform of a 512^3 complex128 field cannot be done in
+// one HBM pass (a pencil plane is 4 MiB; an SM holds 227 KB), so it is three
+// passes, one per axis.  What this file adds over a library FFT is FUSION:
+// every pointwise piece of the time step rides inside the first or last pass
+// whose data is already in registers:
+//   * F g F^-1 of a stage input: the inverse pass along the slowest axis,
+//     the 1/N scale, g(.) and the forward pass along the same axis are ONE
+//     kernel (the inverse's last radix stage leaves each thread holding
+//     exactly the elements the forward's first stage reads);
+//   * the Lawson stage combinations (integrators.py:205-215) and the
+//     separable exp(f tau symbol) multipliers run between the forward pass of
+//     g_i and the inverse pass of the next stage input along the contiguous
+//     axis (one kernel: forward -> g_i -> stage -> inverse);
+//   * strang: the end-of-step flow, the finiteness check, the next step's
+//     first flow and the forward pass share one kernel along the slowest axis;
+//     E1 rides between the forward and inverse passes of the contiguous axis.
+// Per-pass layout:
+//   contiguous axis (stride 1): a CTA owns 4096/L whole rows; thread t of a
+//     row holds elements t + (L/8) r, r = 0..7; the exchange buffer uses the
+//     128-byte XOR swizzle (conflict-free for every radix-8 stage pattern);
+//   strided axis (stride I, I % 8 == 0): a CTA owns 512/L chunks of 8
+//     adjacent pencils (one 128-byte line per axis index); the 8 threads of a
+//     quarter-warp are the 8 pencils of a chunk, so global accesses are whole
+//     128-byte lines and the exchange buffer [i][8] is conflict-free.
+// Transform: Stockham autosort, radix-8 stages (+ one radix-2/4 stage last
+// for L = 2^(3a+1), 2^(3a+2)); every stage reads x[t + (L/8) r], so the
+// first stage loads straight from HBM and the last stores straight to HBM;
+// two shared-memory exchanges per 512-point pencil.  Twiddles come from one
+// correctly rounded 512-entry table (fft_twiddles.h).  Unnormalised both
+// ways (the 1/N of ifftn is applied by the program that consumes the inverse).
+#include <cuda_runtime.h>
+
+#include "cgl_common.cuh"
+#include "cgl_internal.h"
+#include "fft_twiddles.h"
+#include "stage_ops.cuh"
+
+namespace cgl {
+namespace fftp {
+
+constexpr int kThreads = 512;
+constexpr int kTileElems = 4096;  // elements per CTA tile (64 KB of complex128)
+
+enum Prog {
+  FP_PLAIN = 0,     // transform only
+  FP_IF4_START,     // contiguous, inverse: src = spectral state u
+  FP_IF4_B1,        // contiguous: g1 = F(src); u2 = E1/2 (u + t/2 g1); dst = F^-1 u2
+  FP_IF4_B2,        // g2 = F(src); u3 = E1/2 u + t/2 g2
+  FP_IF4_B3,        // g3 = F(src); u4 = t E1/2 g3 + E1 u
+  FP_IF4_B4,        // g4 = F(src); out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4 -> u; check;
+                    // dst = F^-1 out (the next step's first inverse pass) when dst != null
+  FP_G,             // inverse, x scale, g(.), forward (any axis)
+  FP_STR_START,     // strided, forward: src = physical u (x scale); v = flow(u, t/2) [seq 0]
+  FP_STR_A0,        // strided: w = F^-1(src) x scale; out = flow(w, t/2) [seq w]; check; u_out = out;
+                    // v = flow(out, t/2) [step + 1, seq 0]; dst = F(v) when dst != null
+  FP_STR_MID,       // contiguous: F, x E1, F^-1
+  FP_NPROG
+};
+
+struct Args {
+  const double2* src;
+  double2* dst;
+  int64_t O, I;  // outer count, inner stride of the transform axis (I = 1: contiguous)
+  const double2* u;
+  double2* u_out;
+  const double2* g[3];
+  double2* g_out;
+  const double2* tab[2][3];  // separable exp(f tau symbol): [fraction 1/2, 1][axis]
+  int nd;
+  int lg1;        // log2 n1 (3D row decode: i0 = row >> lg1, i1 = row & (n1 - 1))
+  double tau, scale;
+  StageNL nl;
+  cgl_flag_t* flag;
+  uint64_t pos;
+  int fw;
+};
+
+__device__ __forceinline__ double2 mul_mi(double2 a, bool inv) {  // a * (-i) forward, a * (+i) inverse
+  return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+__device__ __forceinline__ double2 mul_w8(double2 a, bool inv) {  // a * exp(-+ i pi / 4)
+  const double s = 0.70710678118654752440;
+  return inv ? make_double2(__dmul_rn(s, __dsub_rn(a.x, a.y)), __dmul_rn(s, __dadd_rn(a.x, a.y)))
+             : make_double2(__dmul_rn(s, __dadd_rn(a.x, a.y)), __dmul_rn(s, __dsub_rn(a.y, a.x)));
+}
+__device__ __forceinline__ double2 mul_w83(double2 a, bool inv) {  // a * exp(-+ 3 i pi / 4)
+  const double s = 0.70710678118654752440;
+  return inv ? make_double2(__dmul_rn(-s, __dadd_rn(a.x, a.y)), __dmul_rn(s, __dsub_rn(a.x, a.y)))
+             : make_double2(__dmul_rn(s, __dsub_rn(a.y, a.x)), __dmul_rn(-s, __dadd_rn(a.x, a.y)));
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(double2 (&a)[8]) {
+  const double2 b0 = cadd(a[0], a[4]), b4 = csub(a[0], a[4]);
+  const double2 b1 = cadd(a[1], a[5]), b5 = mul_w8(csub(a[1], a[5]), INV);
+  const double2 b2 = cadd(a[2], a[6]), b6 = mul_mi(csub(a[2], a[6]), INV);
+  const double2 b3 = cadd(a[3], a[7]), b7 = mul_w83(csub(a[3], a[7]), INV);
+  const double2 c0 = cadd(b0, b2), c2 = csub(b0, b2), c1 = cadd(b1, b3), c3 = mul_mi(csub(b1, b3), INV);
+  const double2 c4 = cadd(b4, b6), c6 = csub(b4, b6), c5 = cadd(b5, b7), c7 = mul_mi(csub(b5, b7), INV);
+  a[0] = cadd(c0, c1);
+  a[4] = csub(c0, c1);
+  a[2] = cadd(c2, c3);
+  a[6] = csub(c2, c3);
+  a[1] = cadd(c4, c5);
+  a[5] = csub(c4, c5);
+  a[3] = cadd(c6, c7);
+  a[7] = csub(c6, c7);
+}
+template <bool INV>
+__device__ __forceinline__ void dft4(double2 (&a)[4]) {
+  const double2 b0 = cadd(a[0], a[2]), b2 = csub(a[0], a[2]);
+  const double2 b1 = cadd(a[1], a[3]), b3 = mul_mi(csub(a[1], a[3]), INV);
+  a[0] = cadd(b0, b1);
+  a[2] = csub(b0, b1);
+  a[1] = cadd(b2, b3);
+  a[3] = csub(b2, b3);
+}
+
+__device__ __forceinline__ double2 twiddle(int idx512, bool inv) {
+  const double2 w = __ldg(&g_fft_tw512[idx512 & 511]);
+  return inv ? make_double2(w.x, -w.y) : w;
+}
+
+// log2 and radix plan of a power-of-two length 8 <= L <= 512
+template <int L>
+struct Plan {
+  static constexpr int p = L == 8 ? 3 : L == 16 ? 4 : L == 32 ? 5 : L == 64 ? 6 : L == 128 ? 7 : L == 256 ? 8 : 9;
+  static constexpr int n8 = p / 3;          // radix-8 stages
+  static constexpr int tail = p % 3;        // 0: none, 1: radix-2, 2: radix-4 (last stage)
+  static constexpr int nstages = n8 + (tail ? 1 : 0);
+  static constexpr int T = L / 8;           // threads per pencil
+};
+
+// shared-memory slot of element i of the calling thread's pencil
+template <int L, bool CONTIG>
+struct Lay {
+  int base;  // CONTIG: pencil * L; strided: group * L * 8 + pencil-in-chunk
+  __device__ __forceinline__ int at(int i) const {
+    if (CONTIG) return base + ((i & ~7) | ((i ^ (i >> 3)) & 7));
+    return base + i * 8;
+  }
+};
+
+// In-register transform of one pencil: on entry v[r] = x[t + T r]; on exit
+// v[r] = X[t + T r].  sm: the CTA's exchange buffer.
+template <int L, bool CONTIG, bool INV>
+__device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, const Lay<L, CONTIG>& lay) {
+  using PL = Plan<L>;
+  constexpr int T = PL::T;
+  int Ns = 1;
+#pragma unroll
+  for (int s = 0; s < PL::nstages; ++s) {
+    const int R = s < PL::n8 ? 8 : (PL::tail == 1 ? 2 : 4);
+    const bool last = s == PL::nstages - 1;
+    // twiddle W_{Ns R}^{m k} = W_512^{m k 512 / (Ns R)}
+    if (R == 8) {
+      const int j = t;
+      const int k = j & (Ns - 1);
+      double2 a[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = v[m];
+      if (Ns > 1) {
+#pragma unroll
+        for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], twiddle(m * k * (512 / (Ns * 8)), INV));
+      }
+      dft8<INV>(a);
+      if (last) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = a[q];
+      } else {
+        const int o = (j / Ns) * Ns * 8 + k;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sm[lay.at(o + q * Ns)] = a[q];
+      }
+    } else if (R == 4) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = t + h * T;
+        const int k = j & (Ns - 1);
+        double2 a[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) a[m] = v[h + 2 * m];
+        if (Ns > 1) {
+#pragma unroll
+          for (int m = 1; m < 4; ++m) a[m] = cmul(a[m], twiddle(m * k * (512 / (Ns * 4)), INV));
+        }
+        dft4<INV>(a);
+        // radix-4 only ever runs last (L = 2^(3a+2)): out[j + q Ns] = v[h + 2 q]
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[h + 2 * q] = a[q];
+      }
+    } else {
+      // radix 2, last stage
+      double2 a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[r] = v[r];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int j = t + h * T;
+        const int k = j & (Ns - 1);
+        double2 x0 = a[h], x1 = a[h + 4];
+        if (Ns > 1) x1 = cmul(x1, twiddle(k * (512 / (Ns * 2)), INV));
+        v[h] = cadd(x0, x1);
+        v[h + 4] = csub(x0, x1);
+      }
+    }
+    if (!last) {
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = sm[lay.at(t + T * r)];
+      __syncthreads();
+    }
+    Ns *= R;
+  }
+}
+
+// separable exp(f tau symbol) at (row, i) of a contiguous-axis pass
+__device__ __forceinline__ double2 efac(const Args& a, int fr, int64_t row, int i) {
+  double2 e = ld2(a.tab[fr][a.nd - 1] + i);  // 1 * t_last, as sep_factor's first product (exact)
+  if (a.nd == 3) {
+    e = cmul(e, ld2(a.tab[fr][1] + (row & ((1ll << a.lg1) - 1))));
+    e = cmul(e, ld2(a.tab[fr][0] + (row >> a.lg1)));
+  } else {
+    e = cmul(e, ld2(a.tab[fr][0] + row));
+  }
+  return e;
+}
+
+template <int L, bool CONTIG, int PROG, bool INV>
+__global__ void __launch_bounds__(kThreads) fft_pass_kernel(const Args a) {
+  using PL = Plan<L>;
+  constexpr int T = PL::T;
+  extern __shared__ double2 sm[];
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t step = resolve_pos(a.flag, a.pos) >> 24;
+  int first = 0;
+  if (PROG == FP_STR_A0) first = a.fw;
+  if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)first << 8))) return;
+
+  const int tid = threadIdx.x;
+  Lay<L, CONTIG> lay;
+  int t;
+  int64_t gbase, gstride;  // element (t + T r) at gbase + (t + T r) * gstride
+  int64_t row = 0;
+  if (CONTIG) {
+    constexpr int P = kTileElems / L;
+    const int p = tid / T;
+    t = tid % T;
+    row = (int64_t)blockIdx.x * P + p;
+    lay.base = p * L;
+    gbase = row * L;
+    gstride = 1;
+  } else {
+    constexpr int G = kTileElems / (8 * L);
+    const int pp = tid & 7;
+    const int g = (tid >> 3) / T;
+    t = (tid >> 3) % T;
+    const int64_t c = (int64_t)blockIdx.x * G + g;  // chunk of 8 adjacent pencils
+    const int64_t cpo = a.I / 8;                    // chunks per outer index
+    const int64_t o = c / cpo;
+    gbase = o * L * a.I + (c % cpo) * 8 + pp;
+    gstride = a.I;
+    lay.base = g * L * 8 + pp;
+  }
+  double2 v[8];
+  uint64_t key = ~0ull;
+  const double tau = a.tau;
+  const uint64_t check_pos = (step << 24) | (255ull << 8);
+
+  if (PROG == FP_IF4_START) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = ld2(a.u + gbase + (int64_t)(t + T * r) * gstride);
+  } else if (PROG == FP_STR_START) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, ld2(a.u + gbase + (int64_t)(t + T * r) * gstride));
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = ld2(a.src + gbase + (int64_t)(t + T * r) * gstride);
+  }
+
+  if (PROG == FP_PLAIN) {
+    fft_pencil<L, CONTIG, INV>(v, t, sm, lay);
+  } else if (PROG == FP_IF4_START) {
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+  } else if (PROG == FP_G) {
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      v[r] = gfun<1>(a.nl, x).c[0];
+    }
+    __syncthreads();
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+  } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay);  // v = g_i (spectral)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = t + T * r;
+      const int64_t gi = gbase + i;
+      const double2 gi_v = v[r];
+      const double2 u = ld2(a.u + gi);
+      if (PROG == FP_IF4_B1) {
+        a.g_out[gi] = gi_v;
+        v[r] = cmul(efac(a, 0, row, i), caxpy(0.5 * tau, gi_v, u));
+      } else if (PROG == FP_IF4_B2) {
+        a.g_out[gi] = gi_v;
+        v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, row, i), u));
+      } else if (PROG == FP_IF4_B3) {
+        a.g_out[gi] = gi_v;
+        v[r] = caxpy(tau, cmul(efac(a, 0, row, i), gi_v), cmul(efac(a, 1, row, i), u));
+      } else {
+        const double2 g1 = ld2(a.g[0] + gi), g2 = ld2(a.g[1] + gi), g3 = ld2(a.g[2] + gi);
+        const double2 out =
+            caxpy(tau / 6.0, gi_v,
+                  caxpy(tau / 3.0, cmul(efac(a, 0, row, i), caxpy(1.0, g2, g3)),
+                        cmul(efac(a, 1, row, i), caxpy(tau / 6.0, g1, u))));
+        if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        a.u_out[gi] = out;
+        v[r] = out;
+      }
+    }
+    if (PROG == FP_IF4_B4 && a.dst == nullptr) {
+      raise_min(a.flag, key);
+      return;
+    }
+    __syncthreads();
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+  } else if (PROG == FP_STR_START) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = v[r];
+      v[r] = flow<1>(a.nl, x, 0.5 * tau, step, 0, key).c[0];
+    }
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+  } else if (PROG == FP_STR_A0) {
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      const double2 out = flow<1>(a.nl, x, 0.5 * tau, step, a.fw, key).c[0];
+      if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      a.u_out[gbase + (int64_t)(t + T * r) * gstride] = out;
+      x.c[0] = out;
+      v[r] = flow<1>(a.nl, x, 0.5 * tau, step + 1, 0, key).c[0];
+    }
+    if (a.dst == nullptr) {
+      raise_min(a.flag, key);
+      return;
+    }
+    __syncthreads();
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+  } else if (PROG == FP_STR_MID) {
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, row, t + T * r), v[r]);
+    __syncthreads();
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+  }
+
+#pragma unroll
+  for (int r = 0; r < 8; ++r) a.dst[gbase + (int64_t)(t + T * r) * gstride] = v[r];
+  if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, key);
+}
+
+template <int L, bool CONTIG, int PROG, bool INV>
+static int launch_one(const Args& a, cudaStream_t st) {
+  auto kern = fft_pass_kernel<L, CONTIG, PROG, INV>;
+  static bool attr = false;
+  const int smem = kTileElems * (int)sizeof(double2);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fft_pass)");
+    attr = true;
+  }
+  const int64_t tiles = CONTIG ? a.O / (kTileElems / L) : (a.O * a.I / 8) / (kTileElems / (8 * L));
+  if (tiles <= 0) return 0;
+  cudaError_t e = launch_k(kern, dim3((unsigned)tiles), dim3(kThreads), (size_t)smem, st, dim3(1), a);
+  if (e != cudaSuccess) return set_cuda_error(e, "fft_pass launch");
+  return check_launch("fft_pass_kernel");
+}
+
+template <int L>
+static int launch_L(int prog, bool contig, bool inv, const Args& a, cudaStream_t st) {
+  if (contig) {
+    switch (prog) {
+      case FP_PLAIN: return inv ? launch_one<L, true, FP_PLAIN, true>(a, st) : launch_one<L, true, FP_PLAIN, false>(a, st);
+      case FP_IF4_START: return launch_one<L, true, FP_IF4_START, true>(a, st);
+      case FP_IF4_B1: return launch_one<L, true, FP_IF4_B1, false>(a, st);
+      case FP_IF4_B2: return launch_one<L, true, FP_IF4_B2, false>(a, st);
+      case FP_IF4_B3: return launch_one<L, true, FP_IF4_B3, false>(a, st);
+      case FP_IF4_B4: return launch_one<L, true, FP_IF4_B4, false>(a, st);
+      case FP_G: return launch_one<L, true, FP_G, false>(a, st);
+      case FP_STR_MID: return launch_one<L, true, FP_STR_MID, false>(a, st);
+      default: return set_error(CGL_EINVAL, "fft_pass: program needs a strided axis");
+    }
+  }
+  switch (prog) {
+    case FP_PLAIN: return inv ? launch_one<L, false, FP_PLAIN, true>(a, st) : launch_one<L, false, FP_PLAIN, false>(a, st);
+    case FP_G: return launch_one<L, false, FP_G, false>(a, st);
+    case FP_STR_START: return launch_one<L, false, FP_STR_START, false>(a, st);
+    case FP_STR_A0: return launch_one<L, false, FP_STR_A0, false>(a, st);
+    default: return set_error(CGL_EINVAL, "fft_pass: program needs the contiguous axis");
+  }
+}
+
+}  // namespace fftp
+
+bool fft_pass_supported(int ndim, const int64_t* shape) {
+  if (ndim < 2 || ndim > 3) return false;
+  for (int d = 0; d < ndim; ++d) {
+    const int64_t n = shape[d];
+    if (n < 16 || n > 512 || (n & (n - 1))) return false;
+  }
+  return true;
+}
+
+int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, int axis, int inverse,
+                    const double* src, double* dst, const cgl_fft_ops_t* ops) {
+  using namespace fftp;
+  if (program < 0 || program >= FP_NPROG) return set_error(CGL_EINVAL, "fft_pass: unknown program");
+  if (!fft_pass_supported(ndim, shape)) return set_error(CGL_ESHAPE, "fft_pass: 2D/3D, power-of-two extents 16..512");
+  if (axis < 0 || axis >= ndim) return set_error(CGL_EINVAL, "fft_pass: bad axis");
+  Args a{};
+  a.src = reinterpret_cast<const double2*>(src);
+  a.dst = reinterpret_cast<double2*>(dst);
+  a.O = 1;
+  a.I = 1;
+  for (int d = 0; d < axis; ++d) a.O *= shape[d];
+  for (int d = axis + 1; d < ndim; ++d) a.I *= shape[d];
+  const bool contig = axis == ndim - 1;
+  const int L = (int)shape[axis];
+  a.nd = ndim;
+  a.lg1 = 0;
+  if (ndim == 3)
+    while ((1ll << a.lg1) < shape[1]) ++a.lg1;
+  if (ops) {
+    a.u = reinterpret_cast<const double2*>(ops->u);
+    a.u_out = reinterpret_cast<double2*>(ops->u_out);
+    for (int q = 0; q < 3; ++q) a.g[q] = reinterpret_cast<const double2*>(ops->g[q]);
+    a.g_out = reinterpret_cast<double2*>(ops->g_out);
+    for (int fr = 0; fr < 2; ++fr)
+      for (int d = 0; d < ndim; ++d) a.tab[fr][d] = reinterpret_cast<const double2*>(ops->tables[fr][d]);
+    a.tau = ops->tau;
+    a.scale = ops->scale;
+    const cgl_nonlinear_t& nl = ops->nl;
+    a.nl = StageNL{nl.alpha3, nl.beta3, nl.alpha4, nl.beta4, nl.alpha5, nl.kind};
+    if (nl.kind == 2) return set_error(CGL_EINVAL, "fft_pass: scalar fields only");
+    a.fw = 1;
+    a.flag = ops->flag;
+    a.pos = ops->pos;
+  } else if (program != FP_PLAIN) {
+    return set_error(CGL_EINVAL, "fft_pass: program needs its operands");
+  }
+  // operand checks per program
+  const bool need_src = !(program == FP_IF4_START || program == FP_STR_START);
+  if (need_src && !src) return set_error(CGL_EINVAL, "fft_pass: null src");
+  const bool dst_optional = program == FP_IF4_B4 || program == FP_STR_A0;
+  if (!dst && !dst_optional) return set_error(CGL_EINVAL, "fft_pass: null dst");
+  if ((program >= FP_IF4_START && program <= FP_IF4_B4 || program == FP_STR_START) && !a.u)
+    return set_error(CGL_EINVAL, "fft_pass: program needs u");
+  if ((program >= FP_IF4_B1 && program <= FP_IF4_B3) && !a.g_out) return set_error(CGL_EINVAL, "fft_pass: needs g_out");
+  if (program == FP_IF4_B4 && (!a.g[0] || !a.g[1] || !a.g[2] || !a.u_out))
+    return set_error(CGL_EINVAL, "fft_pass: B4 needs g1..g3 and u_out");
+  if (program == FP_STR_A0 && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: needs u_out");
+  if ((program >= FP_IF4_B1 && program <= FP_IF4_B4) || program == FP_STR_MID)
+    for (int fr = 0; fr < 2; ++fr)
+      for (int d = 0; d < ndim; ++d)
+        if (!a.tab[fr][d]) return set_error(CGL_EINVAL, "fft_pass: program needs the exp tables");
+  if (!contig && a.I % 8) return set_error(CGL_ESHAPE, "fft_pass: strided axis needs inner extent % 8 == 0");
+  switch (L) {
+    case 16: return launch_L<16>(program, contig, inverse != 0, a, st);
+    case 32: return launch_L<32>(program, contig, inverse != 0, a, st);
+    case 64: return launch_L<64>(program, contig, inverse != 0, a, st);
+    case 128: return launch_L<128>(program, contig, inverse != 0, a, st);
+    case 256: return launch_L<256>(program, contig, inverse != 0, a, st);
+    case 512: return launch_L<512>(program, contig, inverse != 0, a, st);
+    default: return set_error(CGL_ESHAPE, "fft_pass: extent");
+  }
+}
+
+CGL_PROF_TU(fftpass)
+
+}  // namespace cgl

@@ -47,7 +47,11 @@ def supports(problem, scheme_name):
 
 
 def make_plan(problem, scheme_name, like):
-    return (FourierPlan if problem.fourier else FusedPlan)(problem, scheme_name, like)
+    if problem.fourier:
+        if PencilFourierPlan.applies(problem, scheme_name, like):
+            return PencilFourierPlan(problem, scheme_name, like)
+        return FourierPlan(problem, scheme_name, like)
+    return FusedPlan(problem, scheme_name, like)
 
 
 class FusedPlan:
@@ -590,3 +594,121 @@ class FourierPlan(FusedPlan):
         out = [torch.empty_like(x) for x in self.U[0]]
         self._fft(self.state_after(k), out, inverse=False)
         return out
+
+
+class PencilFourierPlan(FourierPlan):
+    """if4 / strang on power-of-two periodic grids (2D/3D, extents 16..512)
+    with the fused pencil-FFT passes (csrc/fftpass.cu) instead of cuFFT plus
+    separate pointwise kernels.  One pass per axis per transform; every
+    pointwise piece rides in a pass (3D, axes 0/1/2, axis 2 contiguous):
+
+    if4 (state u in coefficient space, scratch T, g1..g3):
+      prologue  IF4_START  T = F2^-1 u
+      eval i    G1^-1, G0 (F0^-1, /N, g, F0), G1      (2D: G0 only)
+                B_i: g_i = F2 T; next stage input q -> T = F2^-1 q
+                (B4: u = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4, checked;
+                T = F2^-1 u starts the next step)
+      16 passes per 3D step: 688 B/pt of HBM traffic (cuFFT + stage kernels: ~1.1 KB/pt).
+    strang (state in physical space, ping-pong U; the reference's F^-1 F at
+    each step boundary elided exactly as FourierPlan):
+      prologue  STR_START  T = F0 flow(u0 / N, t/2)
+      step k    F1, STR_MID (F2, E1, F2^-1), F1^-1,
+                STR_A0: w = F0^-1 T / N; u_k = flow(w, t/2) (checked, stored);
+                T = F0 flow(u_k, t/2) of step k + 1
+      4 passes per 3D step: 144 B/pt.
+    Divergence keys and positions are those of the stage kernels (same
+    programs, same flag record), so diverged_at / reason are unchanged.
+    """
+
+    def __init__(self, problem, scheme_name, like):
+        from fractions import Fraction
+        self.p = problem
+        self.scheme = scheme_name
+        self.nf = len(like)
+        self.shape = tuple(like[0].shape)
+        self.n = like[0].numel()
+        self.nl = problem._nl
+        self.blocks = problem._blocks
+        self.half, self.one = Fraction(1, 2), Fraction(1)
+        mk = lambda: torch.empty_like(like[0])  # noqa: E731
+        self.T = mk()
+        if scheme_name == "if4":
+            self.U = [[mk()]]
+            self.G = [mk() for _ in range(3)]
+        else:
+            self.U = [[mk()], [mk()]]
+        self.graphs = {}
+        self.flag = _lib.new_flag(0)
+        self._pos = _lib.rel_pos(1)
+        self._k_base = 0
+        self._flag0 = self.flag.clone()
+        self.graph_launches = {}
+        self.replayed_launches = 0
+        self.W = []
+
+    @staticmethod
+    def applies(problem, scheme_name, like):
+        from . import fftpass
+        return (scheme_name in ("if4", "strang") and len(like) == 1 and problem._nl.kind != 2
+                and fftpass.supported(like[0].shape))
+
+    def _ops(self, tau, **kw):
+        from .fftpass import make_ops
+        return make_ops(tables=self._tabs, tau=tau, nl=self.nl, flag=self.flag, pos=self._pos, **kw)
+
+    def _pass(self, prog, axis, src, dst, tau, inverse=False, **kw):
+        from .fftpass import axis_pass
+        axis_pass(src, dst, axis, inverse=inverse, program=prog, ops=self._ops(tau, **kw), shape=self.shape)
+
+    def load_state(self, u0, tau):
+        from .fftpass import fftn
+        tabs = self._tables()   # [fraction (1/2, 1)][axis] for the single component
+        d = len(self.shape)
+        self._tab_keep = tabs
+        self._tabs = [tabs[0:d], tabs[d:2 * d]]
+        if self.scheme == "if4":
+            self.U[0][0].copy_(u0[0])
+        else:
+            fftn(u0[0], out=self.U[0][0], inverse=True)   # physical p0 * N (1/N folded into STR_START)
+
+    def prologue(self, flag, tau):
+        last = len(self.shape) - 1
+        if self.scheme == "if4":
+            self._pass("if4_start", last, None, self.T, tau, u=self.U[0][0])
+        else:
+            self._pass("str_start", 0, None, self.T, tau, u=self.U[0][0], scale=1.0 / self.n)
+
+    def step(self, k, flag, tau):
+        self._pos = _lib.rel_pos(k - self._k_base)
+        d = len(self.shape)
+        last = d - 1
+        T = self.T
+        inv_n = 1.0 / self.n
+        if self.scheme == "if4":
+            u = self.U[0][0]
+            g1, g2, g3 = self.G
+            for prog, gout in (("if4_b1", g1), ("if4_b2", g2), ("if4_b3", g3), ("if4_b4", None)):
+                if d == 3:
+                    self._pass("plain", 1, T, T, tau, inverse=True)
+                self._pass("g", 0, T, T, tau, scale=inv_n)
+                if d == 3:
+                    self._pass("plain", 1, T, T, tau)
+                if gout is not None:
+                    self._pass(prog, last, T, T, tau, u=u, g_out=gout)
+                else:
+                    self._pass(prog, last, T, T, tau, u=u, u_out=u, g=(g1, g2, g3))
+        else:
+            out = self.U[k % 2][0]
+            if d == 3:
+                self._pass("plain", 1, T, T, tau)
+            self._pass("str_mid", last, T, T, tau)
+            if d == 3:
+                self._pass("plain", 1, T, T, tau, inverse=True)
+            self._before_end(flag)
+            self._pass("str_a0", 0, T, T, tau, u_out=out, scale=inv_n)
+
+    def result(self, k):
+        from .fftpass import fftn
+        if self.scheme == "if4":
+            return self.U[0]
+        return [fftn(self.U[k % 2][0])]

@@ -1,0 +1,132 @@
+"""Pencil-FFT passes (csrc/fftpass.cu) and the fused Fourier plans built on
+them (plan.PencilFourierPlan), against cuFFT (torch.fft) for the bare
+transforms and against the REAL reference (tests/golden/pencil.*, made by
+make_golden_pencil.py) for whole integrations: smooth runs, every divergence
+reason of if4/strang, and the snapshot list around a divergence.
+
+Tolerances: a transform <= 1e-14 relative max vs cuFFT (both FP64 radix
+FFTs); integrations <= 1e-10 relative L2 (BASELINE north_star) with exact
+diverged / diverged_at / reason and the same snapshot steps.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from cases import gpu_problem
+from conftest import GOLDEN, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(16, 16, 16), (16, 32, 64), (64, 16, 128), (512, 16, 16), (32, 512, 8 * 2), (16, 16), (64, 256),
+          (512, 32), (128, 128, 128)]
+
+
+def _rand(shape, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.empty(shape, dtype=torch.complex128, device="cuda")
+    x.real.normal_(generator=g)
+    x.imag.normal_(generator=g)
+    return x
+
+
+def _relmax(a, b):
+    return float((a - b).abs().max() / b.abs().max())
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fftn_matches_cufft(shape):
+    from paper_2403_02816_b200 import fftpass
+    x = _rand(shape)
+    assert fftpass.supported(shape)
+    fwd = fftpass.fftn(x)
+    assert _relmax(fwd, torch.fft.fftn(x)) <= 1e-14
+    inv = fftpass.fftn(x, inverse=True)
+    assert _relmax(inv, torch.fft.ifftn(x) * x.numel()) <= 1e-14
+    # round trip and in-place passes
+    y = x.clone()
+    fftpass.fftn(y, out=y)
+    fftpass.fftn(y, out=y, inverse=True)
+    assert _relmax(y / x.numel(), x) <= 1e-14
+
+
+@pytest.mark.parametrize("shape", [(16, 32, 64), (64, 256)])
+def test_single_axis_passes(shape):
+    from paper_2403_02816_b200 import fftpass
+    x = _rand(shape, 1)
+    for axis in range(len(shape)):
+        for inv in (False, True):
+            y = torch.empty_like(x)
+            fftpass.axis_pass(x, y, axis, inverse=inv)
+            ref = torch.fft.ifft(x, dim=axis) * shape[axis] if inv else torch.fft.fft(x, dim=axis)
+            assert _relmax(y, ref) <= 1e-14
+
+
+def test_unsupported_shapes_are_rejected():
+    from paper_2403_02816_b200 import _lib, fftpass
+    for shape in [(12, 16, 16), (16, 16, 1024), (8, 16, 16), (32,), (16, 16, 16, 16)]:
+        assert not fftpass.supported(shape)
+    x = _rand((16, 16, 16))
+    with pytest.raises(ValueError):
+        fftpass.axis_pass(x, x, 3)
+    with pytest.raises(ValueError):
+        fftpass.axis_pass(x, x, 0, program="if4_b1")   # program needs its operands
+    assert _lib.load().cgl_fft_pass(None, 99, 3, _lib.i64_array((16, 16, 16)), 0, 0, _lib.ptr(x), _lib.ptr(x),
+                                    None) != 0
+
+
+@pytest.fixture(scope="module")
+def pencil_golden():
+    with open(os.path.join(GOLDEN, "pencil.json")) as f:
+        meta = json.load(f)
+    return meta, np.load(os.path.join(GOLDEN, "pencil.npz"))
+
+
+def _cases():
+    with open(os.path.join(GOLDEN, "pencil.json")) as f:
+        return [c["name"] for c in json.load(f)]
+
+
+@pytest.mark.parametrize("name", _cases())
+def test_pencil_plan_against_reference(pencil_golden, name):
+    import paper_2403_02816_b200 as P
+    from paper_2403_02816_b200.plan import PencilFourierPlan
+    meta, arrays = pencil_golden
+    case = next(c for c in meta if c["name"] == name)
+    i = case["index"]
+    prob = gpu_problem(case)
+    snaps = []
+    res = P.integrate(prob, case["scheme"], (arrays[f"s{i}_ic0"],), case["t_final"], case["steps"],
+                      snapshot_steps=case["snapshot_steps"], on_snapshot=lambda k, t, f: snaps.append((k, f[0])))
+    assert any(isinstance(p, PencilFourierPlan) for p in prob._plans.values()), "pencil plan not used"
+    assert (res.diverged, res.diverged_at, res.reason) == (case["diverged"], case["diverged_at"], case["reason"])
+    ref = arrays[f"s{i}_out0"]
+    if np.all(np.isfinite(ref)):
+        assert rel_l2(res.fields[0], ref) <= 1e-10
+    else:
+        assert np.array_equal(np.isfinite(res.fields[0]), np.isfinite(ref))
+    assert [k for k, _ in snaps] == case["snapshots_taken"]
+    for k, f in snaps:
+        assert rel_l2(f, arrays[f"s{i}_snap{k}"]) <= 1e-10
+
+
+@pytest.mark.parametrize("scheme", ["if4", "strang"])
+def test_pencil_plan_matches_cufft_plan(scheme):
+    """The fused pencil plan and the cuFFT + stage-kernel plan (FourierPlan)
+    on the same C3-physics problem at 64^3 agree to rounding level."""
+    from paper_2403_02816_b200 import SCHEMES, _lib, workloads as W
+    from paper_2403_02816_b200.plan import FourierPlan, PencilFourierPlan
+    w = W.CONFIGS["C3"].scaled(64, 20)
+    prob = W.build_problem(w)
+    x0 = W.state_for_problem(w, W.initial_state_device(w))
+    prob.prepare(w.tau, SCHEMES[scheme])
+    outs = []
+    for cls in (PencilFourierPlan, FourierPlan):
+        plan = cls(prob, scheme, [x0])
+        key = plan.run([x0], w.steps, w.tau)
+        assert key == _lib.NO_DIVERGENCE
+        outs.append(plan.result(w.steps)[0].clone())
+    assert rel_l2(outs[0].cpu().numpy(), outs[1].cpu().numpy()) <= 1e-12
