@@ -33,6 +33,8 @@
 // two shared-memory exchanges per 512-point pencil.  Twiddles come from one
 // correctly rounded 512-entry table (fft_twiddles.h).  Unnormalised both
 // ways (the 1/N of ifftn is applied by the program that consumes the inverse).
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "cgl_common.cuh"
@@ -43,8 +45,6 @@
 namespace cgl {
 namespace fftp {
 
-constexpr int kThreads = 512;
-constexpr int kTileElems = 4096;  // elements per CTA tile (64 KB of complex128)
 
 enum Prog {
   FP_PLAIN = 0,     // transform only
@@ -139,10 +139,11 @@ struct Plan {
 // shared-memory slot of element i of the calling thread's pencil
 template <int L, bool CONTIG>
 struct Lay {
-  int base;  // CONTIG: pencil * L; strided: group * L * 8 + pencil-in-chunk
+  int base;  // CONTIG: pencil * L; strided: chunk * L * CW + pencil-in-chunk
+  int cw;    // strided: pencils per chunk
   __device__ __forceinline__ int at(int i) const {
     if (CONTIG) return base + ((i & ~7) | ((i ^ (i >> 3)) & 7));
-    return base + i * 8;
+    return base + i * cw;
   }
 };
 
@@ -219,22 +220,42 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
   }
 }
 
-// separable exp(f tau symbol) at (row, i) of a contiguous-axis pass
-__device__ __forceinline__ double2 efac(const Args& a, int fr, int64_t row, int i) {
-  double2 e = ld2(a.tab[fr][a.nd - 1] + i);  // 1 * t_last, as sep_factor's first product (exact)
-  if (a.nd == 3) {
-    e = cmul(e, ld2(a.tab[fr][1] + (row & ((1ll << a.lg1) - 1))));
-    e = cmul(e, ld2(a.tab[fr][0] + (row >> a.lg1)));
-  } else {
-    e = cmul(e, ld2(a.tab[fr][0] + row));
-  }
-  return e;
+// separable exp(f tau symbol) of a contiguous-axis row: every element of a
+// thread lies in one row, so the product of the row's slower-axis factors is
+// formed once (rf[fr]) and each element costs one table load and one cmul.
+__device__ __forceinline__ double2 row_factor(const Args& a, int fr, int64_t row) {
+  if (a.nd == 3) return cmul(ld2(a.tab[fr][1] + (row & ((1ll << a.lg1) - 1))), ld2(a.tab[fr][0] + (row >> a.lg1)));
+  return ld2(a.tab[fr][0] + row);
+}
+__device__ __forceinline__ double2 efac(const Args& a, int fr, const double2 (&rf)[2], int i) {
+  return cmul(ld2(a.tab[fr][a.nd - 1] + i), rf[fr]);
 }
 
-template <int L, bool CONTIG, int PROG, bool INV>
-__global__ void __launch_bounds__(kThreads) fft_pass_kernel(const Args a) {
-  using PL = Plan<L>;
-  constexpr int T = PL::T;
+// streaming global accesses: every pass touches each element once
+__device__ __forceinline__ double2 ldg_s(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void stg_s(double2* p, double2 v) { __stcs(p, v); }
+
+// CTA geometry for threads NT and pencil length L
+template <int L, bool CONTIG, int NT>
+struct Geo {
+  static constexpr int T = L / 8;                                  // threads per pencil
+  static constexpr int TILE = NT * 8;                              // elements per CTA
+  static constexpr int ROWS = CONTIG ? TILE / L : 0;               // contiguous: rows per CTA
+  static constexpr int CW = CONTIG ? 0 : (NT / T < 8 ? NT / T : 8);  // strided: pencils per chunk
+  static constexpr int G = CONTIG ? 0 : NT / (T * CW);             // strided: chunks per CTA
+};
+
+// registers per thread the program needs to co-reside MINB CTAs per SM
+template <int PROG, int NT>
+struct Occ {
+  static constexpr int MINB = NT >= 512 ? 1 : (PROG == FP_PLAIN || PROG == FP_IF4_START) ? 4
+                              : (PROG == FP_STR_A0 || PROG == FP_STR_START || PROG == FP_IF4_B4) ? 2 : 3;
+};
+
+template <int L, bool CONTIG, int PROG, bool INV, int NT>
+__global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const Args a) {
+  using GE = Geo<L, CONTIG, NT>;
+  constexpr int T = GE::T;
   extern __shared__ double2 sm[];
   pdl_wait();
   pdl_trigger();
@@ -246,42 +267,46 @@ __global__ void __launch_bounds__(kThreads) fft_pass_kernel(const Args a) {
   const int tid = threadIdx.x;
   Lay<L, CONTIG> lay;
   int t;
+  bool valid;
   int64_t gbase, gstride;  // element (t + T r) at gbase + (t + T r) * gstride
   int64_t row = 0;
   if (CONTIG) {
-    constexpr int P = kTileElems / L;
     const int p = tid / T;
     t = tid % T;
-    row = (int64_t)blockIdx.x * P + p;
+    row = (int64_t)blockIdx.x * GE::ROWS + p;
+    valid = row < a.O;
     lay.base = p * L;
     gbase = row * L;
     gstride = 1;
   } else {
-    constexpr int G = kTileElems / (8 * L);
-    const int pp = tid & 7;
-    const int g = (tid >> 3) / T;
-    t = (tid >> 3) % T;
-    const int64_t c = (int64_t)blockIdx.x * G + g;  // chunk of 8 adjacent pencils
-    const int64_t cpo = a.I / 8;                    // chunks per outer index
+    constexpr int CW = GE::CW;
+    const int pp = tid % CW;
+    const int g = (tid / CW) / T;
+    t = (tid / CW) % T;
+    const int64_t cpo = a.I / CW;                   // chunks per outer index
+    const int64_t c = (int64_t)blockIdx.x * GE::G + g;  // chunk of CW adjacent pencils
+    valid = c < a.O * cpo;
     const int64_t o = c / cpo;
-    gbase = o * L * a.I + (c % cpo) * 8 + pp;
+    gbase = o * L * a.I + (c % cpo) * CW + pp;
     gstride = a.I;
-    lay.base = g * L * 8 + pp;
+    lay.base = g * L * CW + pp;
+    lay.cw = CW;
   }
   double2 v[8];
   uint64_t key = ~0ull;
   const double tau = a.tau;
   const uint64_t check_pos = (step << 24) | (255ull << 8);
-
-  if (PROG == FP_IF4_START) {
+  const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
+  if (valid) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = ld2(a.u + gbase + (int64_t)(t + T * r) * gstride);
-  } else if (PROG == FP_STR_START) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, ld2(a.u + gbase + (int64_t)(t + T * r) * gstride));
+    for (int r = 0; r < 8; ++r) v[r] = ldg_s(src + gbase + (int64_t)(t + T * r) * gstride);
   } else {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = ld2(a.src + gbase + (int64_t)(t + T * r) * gstride);
+    for (int r = 0; r < 8; ++r) v[r] = make_double2(0.0, 0.0);
+  }
+  if (PROG == FP_STR_START) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, v[r]);
   }
 
   if (PROG == FP_PLAIN) {
@@ -300,30 +325,35 @@ __global__ void __launch_bounds__(kThreads) fft_pass_kernel(const Args a) {
     fft_pencil<L, CONTIG, false>(v, t, sm, lay);
   } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
     fft_pencil<L, CONTIG, false>(v, t, sm, lay);  // v = g_i (spectral)
+    double2 rf[2];
+    rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
+    rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
+    if (valid) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int i = t + T * r;
-      const int64_t gi = gbase + i;
-      const double2 gi_v = v[r];
-      const double2 u = ld2(a.u + gi);
-      if (PROG == FP_IF4_B1) {
-        a.g_out[gi] = gi_v;
-        v[r] = cmul(efac(a, 0, row, i), caxpy(0.5 * tau, gi_v, u));
-      } else if (PROG == FP_IF4_B2) {
-        a.g_out[gi] = gi_v;
-        v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, row, i), u));
-      } else if (PROG == FP_IF4_B3) {
-        a.g_out[gi] = gi_v;
-        v[r] = caxpy(tau, cmul(efac(a, 0, row, i), gi_v), cmul(efac(a, 1, row, i), u));
-      } else {
-        const double2 g1 = ld2(a.g[0] + gi), g2 = ld2(a.g[1] + gi), g3 = ld2(a.g[2] + gi);
-        const double2 out =
-            caxpy(tau / 6.0, gi_v,
-                  caxpy(tau / 3.0, cmul(efac(a, 0, row, i), caxpy(1.0, g2, g3)),
-                        cmul(efac(a, 1, row, i), caxpy(tau / 6.0, g1, u))));
-        if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
-        a.u_out[gi] = out;
-        v[r] = out;
+      for (int r = 0; r < 8; ++r) {
+        const int i = t + T * r;
+        const int64_t gi = gbase + i;
+        const double2 gi_v = v[r];
+        const double2 u = ldg_s(a.u + gi);
+        if (PROG == FP_IF4_B1) {
+          stg_s(a.g_out + gi, gi_v);
+          v[r] = cmul(efac(a, 0, rf, i), caxpy(0.5 * tau, gi_v, u));
+        } else if (PROG == FP_IF4_B2) {
+          stg_s(a.g_out + gi, gi_v);
+          v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, rf, i), u));
+        } else if (PROG == FP_IF4_B3) {
+          stg_s(a.g_out + gi, gi_v);
+          v[r] = caxpy(tau, cmul(efac(a, 0, rf, i), gi_v), cmul(efac(a, 1, rf, i), u));
+        } else {
+          const double2 g1 = ldg_s(a.g[0] + gi), g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
+          const double2 out =
+              caxpy(tau / 6.0, gi_v,
+                    caxpy(tau / 3.0, cmul(efac(a, 0, rf, i), caxpy(1.0, g2, g3)),
+                          cmul(efac(a, 1, rf, i), caxpy(tau / 6.0, g1, u))));
+          if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+          stg_s(a.u_out + gi, out);
+          v[r] = out;
+        }
       }
     }
     if (PROG == FP_IF4_B4 && a.dst == nullptr) {
@@ -348,44 +378,67 @@ __global__ void __launch_bounds__(kThreads) fft_pass_kernel(const Args a) {
       x.c[0] = cscale(a.scale, v[r]);
       const double2 out = flow<1>(a.nl, x, 0.5 * tau, step, a.fw, key).c[0];
       if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
-      a.u_out[gbase + (int64_t)(t + T * r) * gstride] = out;
+      if (valid) stg_s(a.u_out + gbase + (int64_t)(t + T * r) * gstride, out);
       x.c[0] = out;
       v[r] = flow<1>(a.nl, x, 0.5 * tau, step + 1, 0, key).c[0];
     }
     if (a.dst == nullptr) {
-      raise_min(a.flag, key);
+      raise_min(a.flag, valid ? key : ~0ull);
       return;
     }
     __syncthreads();
     fft_pencil<L, CONTIG, false>(v, t, sm, lay);
   } else if (PROG == FP_STR_MID) {
     fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+    double2 rf[2];
+    rf[1] = valid ? row_factor(a, 1, row) : make_double2(0.0, 0.0);
+    rf[0] = rf[1];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, row, t + T * r), v[r]);
+    for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, rf, t + T * r), v[r]);
     __syncthreads();
     fft_pencil<L, CONTIG, true>(v, t, sm, lay);
   }
 
+  if (valid) {
 #pragma unroll
-  for (int r = 0; r < 8; ++r) a.dst[gbase + (int64_t)(t + T * r) * gstride] = v[r];
-  if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, key);
+    for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (int64_t)(t + T * r) * gstride, v[r]);
+  }
+  if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, valid ? key : ~0ull);
 }
 
-template <int L, bool CONTIG, int PROG, bool INV>
-static int launch_one(const Args& a, cudaStream_t st) {
-  auto kern = fft_pass_kernel<L, CONTIG, PROG, INV>;
+static int threads_for(int L) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("CGL_FFT_NT");
+    forced = e ? atoi(e) : 0;
+  }
+  return (forced == 512 && L == 512) ? 512 : 256;
+}
+
+template <int L, bool CONTIG, int PROG, bool INV, int NT>
+static int launch_nt(const Args& a, cudaStream_t st) {
+  using GE = Geo<L, CONTIG, NT>;
+  auto kern = fft_pass_kernel<L, CONTIG, PROG, INV, NT>;
   static bool attr = false;
-  const int smem = kTileElems * (int)sizeof(double2);
+  const int smem = GE::TILE * (int)sizeof(double2);
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fft_pass)");
     attr = true;
   }
-  const int64_t tiles = CONTIG ? a.O / (kTileElems / L) : (a.O * a.I / 8) / (kTileElems / (8 * L));
+  const int64_t tiles = CONTIG ? (a.O + GE::ROWS - 1) / GE::ROWS : ((a.O * (a.I / GE::CW)) + GE::G - 1) / GE::G;
   if (tiles <= 0) return 0;
-  cudaError_t e = launch_k(kern, dim3((unsigned)tiles), dim3(kThreads), (size_t)smem, st, dim3(1), a);
+  cudaError_t e = launch_k(kern, dim3((unsigned)tiles), dim3(NT), (size_t)smem, st, dim3(1), a);
   if (e != cudaSuccess) return set_cuda_error(e, "fft_pass launch");
   return check_launch("fft_pass_kernel");
+}
+
+template <int L, bool CONTIG, int PROG, bool INV>
+static int launch_one(const Args& a, cudaStream_t st) {
+  if constexpr (L == 512) {
+    if (threads_for(L) == 512) return launch_nt<L, CONTIG, PROG, INV, 512>(a, st);
+  }
+  return launch_nt<L, CONTIG, PROG, INV, 256>(a, st);
 }
 
 template <int L>
