@@ -121,8 +121,9 @@ __device__ __forceinline__ void dft4(double2 (&a)[4]) {
   a[3] = csub(b2, b3);
 }
 
-__device__ __forceinline__ double2 twiddle(int idx512, bool inv) {
-  const double2 w = __ldg(&g_fft_tw512[idx512 & 511]);
+// twiddles: the 512-entry table is staged once per CTA in shared memory
+__device__ __forceinline__ double2 twiddle(const double2* tw, int idx512, bool inv) {
+  const double2 w = tw[idx512 & 511];
   return inv ? make_double2(w.x, -w.y) : w;
 }
 
@@ -150,7 +151,8 @@ struct Lay {
 // In-register transform of one pencil: on entry v[r] = x[t + T r]; on exit
 // v[r] = X[t + T r].  sm: the CTA's exchange buffer.
 template <int L, bool CONTIG, bool INV>
-__device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, const Lay<L, CONTIG>& lay) {
+__device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, const Lay<L, CONTIG>& lay,
+                                           const double2* tw) {
   using PL = Plan<L>;
   constexpr int T = PL::T;
   int Ns = 1;
@@ -167,7 +169,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
       for (int m = 0; m < 8; ++m) a[m] = v[m];
       if (Ns > 1) {
 #pragma unroll
-        for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], twiddle(m * k * (512 / (Ns * 8)), INV));
+        for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], twiddle(tw, m * k * (512 / (Ns * 8)), INV));
       }
       dft8<INV>(a);
       if (last) {
@@ -188,7 +190,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
         for (int m = 0; m < 4; ++m) a[m] = v[h + 2 * m];
         if (Ns > 1) {
 #pragma unroll
-          for (int m = 1; m < 4; ++m) a[m] = cmul(a[m], twiddle(m * k * (512 / (Ns * 4)), INV));
+          for (int m = 1; m < 4; ++m) a[m] = cmul(a[m], twiddle(tw, m * k * (512 / (Ns * 4)), INV));
         }
         dft4<INV>(a);
         // radix-4 only ever runs last (L = 2^(3a+2)): out[j + q Ns] = v[h + 2 q]
@@ -205,7 +207,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
         const int j = t + h * T;
         const int k = j & (Ns - 1);
         double2 x0 = a[h], x1 = a[h + 4];
-        if (Ns > 1) x1 = cmul(x1, twiddle(k * (512 / (Ns * 2)), INV));
+        if (Ns > 1) x1 = cmul(x1, twiddle(tw, k * (512 / (Ns * 2)), INV));
         v[h] = cadd(x0, x1);
         v[h + 4] = csub(x0, x1);
       }
@@ -231,6 +233,19 @@ __device__ __forceinline__ double2 efac(const Args& a, int fr, const double2 (&r
   return cmul(ld2(a.tab[fr][a.nd - 1] + i), rf[fr]);
 }
 
+// operands prefetched into shared memory by the stage programs
+template <int PROG>
+struct Aux {
+  static constexpr int N = (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3) ? 1 : PROG == FP_IF4_B4 ? 2 : 0;
+};
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // streaming global accesses: every pass touches each element once
 __device__ __forceinline__ double2 ldg_s(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void stg_s(double2* p, double2 v) { __stcs(p, v); }
@@ -249,7 +264,7 @@ struct Geo {
 template <int PROG, int NT>
 struct Occ {
   static constexpr int MINB = NT >= 512 ? 1 : (PROG == FP_PLAIN || PROG == FP_IF4_START) ? 4
-                              : (PROG == FP_STR_A0 || PROG == FP_STR_START || PROG == FP_IF4_B4) ? 2 : 3;
+                              : (PROG == FP_IF4_B4) ? 2 : 3;
 };
 
 template <int L, bool CONTIG, int PROG, bool INV, int NT>
@@ -297,24 +312,40 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   const double tau = a.tau;
   const uint64_t check_pos = (step << 24) | (255ull << 8);
   const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
+  double2* tw = sm + GE::TILE;                 // 512 twiddles
+  double2* aux = tw + 512;                     // prefetched operands: [k][r][NT]
+  constexpr int NAUX = Aux<PROG>::N;
   if (valid) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = ldg_s(src + gbase + (int64_t)(t + T * r) * gstride);
+    // the pointwise operands of the stage programs are needed only after the
+    // first transform: start their copies now (cp.async, L2-only) so their
+    // latency hides behind it
+    if (NAUX > 0) {
+      const double2* ops[2] = {a.u, PROG == FP_IF4_B4 ? a.g[0] : nullptr};
+#pragma unroll
+      for (int k = 0; k < NAUX; ++k)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) cp_async16(aux + (k * 8 + r) * NT + tid, ops[k] + gbase + (t + T * r));
+      cp_async_commit();
+    }
   } else {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = make_double2(0.0, 0.0);
   }
+  for (int q = tid; q < 512; q += NT) tw[q] = __ldg(&g_fft_tw512[q]);
+  __syncthreads();
   if (PROG == FP_STR_START) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, v[r]);
   }
 
   if (PROG == FP_PLAIN) {
-    fft_pencil<L, CONTIG, INV>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, INV>(v, t, sm, lay, tw);
   } else if (PROG == FP_IF4_START) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
   } else if (PROG == FP_G) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       V<1> x;
@@ -322,9 +353,9 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       v[r] = gfun<1>(a.nl, x).c[0];
     }
     __syncthreads();
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
   } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay);  // v = g_i (spectral)
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);  // v = g_i (spectral)
     double2 rf[2];
     rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
     rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
@@ -334,7 +365,8 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
         const int i = t + T * r;
         const int64_t gi = gbase + i;
         const double2 gi_v = v[r];
-        const double2 u = ldg_s(a.u + gi);
+        if (r == 0) cp_async_wait_all();
+        const double2 u = aux[r * NT + tid];
         if (PROG == FP_IF4_B1) {
           stg_s(a.g_out + gi, gi_v);
           v[r] = cmul(efac(a, 0, rf, i), caxpy(0.5 * tau, gi_v, u));
@@ -345,7 +377,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
           stg_s(a.g_out + gi, gi_v);
           v[r] = caxpy(tau, cmul(efac(a, 0, rf, i), gi_v), cmul(efac(a, 1, rf, i), u));
         } else {
-          const double2 g1 = ldg_s(a.g[0] + gi), g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
+          const double2 g1 = aux[(8 + r) * NT + tid], g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
           const double2 out =
               caxpy(tau / 6.0, gi_v,
                     caxpy(tau / 3.0, cmul(efac(a, 0, rf, i), caxpy(1.0, g2, g3)),
@@ -361,7 +393,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       return;
     }
     __syncthreads();
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
   } else if (PROG == FP_STR_START) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -369,9 +401,9 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       x.c[0] = v[r];
       v[r] = flow<1>(a.nl, x, 0.5 * tau, step, 0, key).c[0];
     }
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
   } else if (PROG == FP_STR_A0) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       V<1> x;
@@ -387,16 +419,16 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       return;
     }
     __syncthreads();
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
   } else if (PROG == FP_STR_MID) {
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
     double2 rf[2];
     rf[1] = valid ? row_factor(a, 1, row) : make_double2(0.0, 0.0);
     rf[0] = rf[1];
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, rf, t + T * r), v[r]);
     __syncthreads();
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay);
+    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
   }
 
   if (valid) {
@@ -420,7 +452,7 @@ static int launch_nt(const Args& a, cudaStream_t st) {
   using GE = Geo<L, CONTIG, NT>;
   auto kern = fft_pass_kernel<L, CONTIG, PROG, INV, NT>;
   static bool attr = false;
-  const int smem = GE::TILE * (int)sizeof(double2);
+  const int smem = (GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fft_pass)");
