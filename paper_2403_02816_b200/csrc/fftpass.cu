@@ -121,9 +121,13 @@ __device__ __forceinline__ void dft4(double2 (&a)[4]) {
   a[3] = csub(b2, b3);
 }
 
-// twiddles: the 512-entry table is staged once per CTA in shared memory
-__device__ __forceinline__ double2 twiddle(const double2* tw, int idx512, bool inv) {
-  const double2 w = tw[idx512 & 511];
+// twiddles: staged once per CTA in shared memory as per-stage tables
+// tw[base(s) + (m - 1) Ns + k] = W_{Ns R}^{m k}, so the threads of a
+// quarter-warp (consecutive k) read consecutive 16-byte words: no bank
+// conflicts (a 512-entry table indexed by m k 512/(Ns R) puts them 8 words
+// apart).
+__device__ __forceinline__ double2 twiddle(const double2* tw, int idx, bool inv) {
+  const double2 w = tw[idx];
   return inv ? make_double2(w.x, -w.y) : w;
 }
 
@@ -135,7 +139,28 @@ struct Plan {
   static constexpr int tail = p % 3;        // 0: none, 1: radix-2, 2: radix-4 (last stage)
   static constexpr int nstages = n8 + (tail ? 1 : 0);
   static constexpr int T = L / 8;           // threads per pencil
+  static constexpr int radix(int s) { return s < n8 ? 8 : (tail == 1 ? 2 : 4); }
+  static constexpr int ns(int s) { return s == 0 ? 1 : ns(s - 1) * radix(s - 1); }
+  // first twiddle of stage s (stage 0 has Ns = 1: no twiddles)
+  static constexpr int twbase(int s) { return s <= 1 ? 0 : twbase(s - 1) + (radix(s - 1) - 1) * ns(s - 1); }
+  static constexpr int twsize() { return twbase(nstages); }
 };
+
+// per-stage twiddle tables of a length-L transform (see twiddle())
+template <int L>
+__device__ __forceinline__ void stage_twiddles(double2* tw, int tid, int nt) {
+  using PL = Plan<L>;
+  for (int e = tid; e < PL::twsize(); e += nt) {
+    int s = 1;
+#pragma unroll
+    for (int q = 2; q < PL::nstages; ++q)
+      if (e >= PL::twbase(q)) s = q;
+    const int off = e - PL::twbase(s);
+    const int Ns = PL::ns(s), R = PL::radix(s);
+    const int m = off / Ns + 1, k = off % Ns;
+    tw[e] = __ldg(&g_fft_tw512[(m * k * (512 / (Ns * R))) & 511]);
+  }
+}
 
 // shared-memory slot of element i of the calling thread's pencil
 template <int L, bool CONTIG>
@@ -144,6 +169,10 @@ struct Lay {
   int cw;    // strided: pencils per chunk
   __device__ __forceinline__ int at(int i) const {
     if (CONTIG) return base + ((i & ~7) | ((i ^ (i >> 3)) & 7));
+    // 4-pencil chunks: a quarter-warp covers rows of two threads t, t + 1;
+    // swapping rows 2q, 2q + 1 when bit 3 of i is set puts those two rows in
+    // different halves of a 128-byte line for every stage pattern
+    if (cw == 4) return base + ((i ^ ((i >> 3) & 1)) << 2);
     return base + i * cw;
   }
 };
@@ -169,7 +198,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
       for (int m = 0; m < 8; ++m) a[m] = v[m];
       if (Ns > 1) {
 #pragma unroll
-        for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], twiddle(tw, m * k * (512 / (Ns * 8)), INV));
+        for (int m = 1; m < 8; ++m) a[m] = cmul(a[m], twiddle(tw, PL::twbase(s) + (m - 1) * Ns + k, INV));
       }
       dft8<INV>(a);
       if (last) {
@@ -190,7 +219,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
         for (int m = 0; m < 4; ++m) a[m] = v[h + 2 * m];
         if (Ns > 1) {
 #pragma unroll
-          for (int m = 1; m < 4; ++m) a[m] = cmul(a[m], twiddle(tw, m * k * (512 / (Ns * 4)), INV));
+          for (int m = 1; m < 4; ++m) a[m] = cmul(a[m], twiddle(tw, PL::twbase(s) + (m - 1) * Ns + k, INV));
         }
         dft4<INV>(a);
         // radix-4 only ever runs last (L = 2^(3a+2)): out[j + q Ns] = v[h + 2 q]
@@ -207,7 +236,7 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
         const int j = t + h * T;
         const int k = j & (Ns - 1);
         double2 x0 = a[h], x1 = a[h + 4];
-        if (Ns > 1) x1 = cmul(x1, twiddle(tw, k * (512 / (Ns * 2)), INV));
+        if (Ns > 1) x1 = cmul(x1, twiddle(tw, PL::twbase(s) + k, INV));
         v[h] = cadd(x0, x1);
         v[h + 4] = csub(x0, x1);
       }
@@ -333,7 +362,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = make_double2(0.0, 0.0);
   }
-  for (int q = tid; q < 512; q += NT) tw[q] = __ldg(&g_fft_tw512[q]);
+  stage_twiddles<L>(tw, tid, NT);
   __syncthreads();
   if (PROG == FP_STR_START) {
 #pragma unroll
