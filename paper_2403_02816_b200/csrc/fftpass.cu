@@ -254,8 +254,8 @@ __device__ __forceinline__ void fft_pencil(double2 (&v)[8], int t, double2* sm, 
 // separable exp(f tau symbol) of a contiguous-axis row: every element of a
 // thread lies in one row, so the product of the row's slower-axis factors is
 // formed once (rf[fr]) and each element costs one table load and one cmul.
-__device__ __forceinline__ double2 row_factor(const Args& a, int fr, int64_t row) {
-  if (a.nd == 3) return cmul(ld2(a.tab[fr][1] + (row & ((1ll << a.lg1) - 1))), ld2(a.tab[fr][0] + (row >> a.lg1)));
+__device__ __forceinline__ double2 row_factor(const Args& a, int fr, int row) {
+  if (a.nd == 3) return cmul(ld2(a.tab[fr][1] + (row & ((1 << a.lg1) - 1))), ld2(a.tab[fr][0] + (row >> a.lg1)));
   return ld2(a.tab[fr][0] + row);
 }
 __device__ __forceinline__ double2 efac(const Args& a, int fr, const double2 (&rf)[2], int i) {
@@ -265,7 +265,7 @@ __device__ __forceinline__ double2 efac(const Args& a, int fr, const double2 (&r
 // operands prefetched into shared memory by the stage programs
 template <int PROG>
 struct Aux {
-  static constexpr int N = (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3) ? 1 : PROG == FP_IF4_B4 ? 2 : 0;
+  static constexpr int N = (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4) ? 1 : 0;
 };
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
@@ -273,7 +273,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // streaming global accesses: every pass touches each element once
 __device__ __forceinline__ double2 ldg_s(const double2* p) { return __ldcs(p); }
@@ -292,14 +293,60 @@ struct Geo {
 // registers per thread the program needs to co-reside MINB CTAs per SM
 template <int PROG, int NT>
 struct Occ {
-  static constexpr int MINB = NT >= 512 ? 1 : (PROG == FP_PLAIN || PROG == FP_IF4_START) ? 4
-                              : (PROG == FP_IF4_B4) ? 2 : 3;
+  // shared memory: 2 tiles of 32 KB + 8 KB twiddles (+ 32 KB stage operands for B1..B4)
+  static constexpr int MINB = NT >= 512 ? 1 : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4) ? 2 : 3;
+};
+
+// Persistent pass kernel: each CTA walks tiles blockIdx.x, +gridDim.x, ...
+// The main operand of tile i+1 is copied (cp.async, L2 -> shared, no
+// registers) into the other half of a two-tile ring while tile i is
+// transformed, so HBM reads stay in flight through the compute phase; each
+// thread copies exactly the elements it will read (its own slots of the
+// exchange layout), so the copy needs no barrier, and the tile buffer doubles
+// as the exchange buffer of the transform.
+template <int L, bool CONTIG, int NT>
+struct TileMap {
+  using GE = Geo<L, CONTIG, NT>;
+  static constexpr int T = GE::T;
+  int t, p_or_g, pp;
+  __device__ __forceinline__ explicit TileMap(int tid) {
+    if constexpr (CONTIG) {
+      p_or_g = tid / T;
+      t = tid % T;
+      pp = 0;
+    } else {
+      pp = tid % GE::CW;
+      p_or_g = (tid / GE::CW) / T;
+      t = (tid / GE::CW) % T;
+    }
+  }
+  // element (t + T r) of this thread's pencil in tile `tile` sits at gbase + (t + T r) * gstride
+  __device__ __forceinline__ bool geo(const Args& a, int64_t tile, int& gbase, int& gstride, int& row) const {
+    if (CONTIG) {
+      row = tile * GE::ROWS + p_or_g;
+      gbase = row * L;
+      gstride = 1;
+      return row < (int)a.O;
+    } else {
+    const int cpo = (int)a.I / GE::CW;
+    const int c = tile * GE::G + p_or_g;
+    const int o = c / cpo;
+    gbase = o * L * (int)a.I + (c % cpo) * GE::CW + pp;
+    gstride = (int)a.I;
+    row = 0;
+    return c < (int)a.O * cpo;
+    }
+  }
+  __device__ __forceinline__ int lay_base() const {
+    return CONTIG ? p_or_g * L : p_or_g * L * GE::CW + pp;
+  }
 };
 
 template <int L, bool CONTIG, int PROG, bool INV, int NT>
-__global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const Args a) {
+__global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const Args a, const int ntiles) {
   using GE = Geo<L, CONTIG, NT>;
   constexpr int T = GE::T;
+  constexpr int NAUX = Aux<PROG>::N;
   extern __shared__ double2 sm[];
   pdl_wait();
   pdl_trigger();
@@ -309,162 +356,152 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)first << 8))) return;
 
   const int tid = threadIdx.x;
+  const TileMap<L, CONTIG, NT> map(tid);
+  const int t = map.t;
   Lay<L, CONTIG> lay;
-  int t;
-  bool valid;
-  int64_t gbase, gstride;  // element (t + T r) at gbase + (t + T r) * gstride
-  int64_t row = 0;
-  if (CONTIG) {
-    const int p = tid / T;
-    t = tid % T;
-    row = (int64_t)blockIdx.x * GE::ROWS + p;
-    valid = row < a.O;
-    lay.base = p * L;
-    gbase = row * L;
-    gstride = 1;
-  } else {
-    constexpr int CW = GE::CW;
-    const int pp = tid % CW;
-    const int g = (tid / CW) / T;
-    t = (tid / CW) % T;
-    const int64_t cpo = a.I / CW;                   // chunks per outer index
-    const int64_t c = (int64_t)blockIdx.x * GE::G + g;  // chunk of CW adjacent pencils
-    valid = c < a.O * cpo;
-    const int64_t o = c / cpo;
-    gbase = o * L * a.I + (c % cpo) * CW + pp;
-    gstride = a.I;
-    lay.base = g * L * CW + pp;
-    lay.cw = CW;
-  }
-  double2 v[8];
+  lay.base = map.lay_base();
+  lay.cw = CONTIG ? 0 : GE::CW;
+  double2* ring[2] = {sm, sm + GE::TILE};
+  double2* tw = sm + 2 * GE::TILE;             // per-stage twiddle tables (< 512 entries)
+  double2* aux = tw + 512;                     // stage operands of the current tile: [k][r][NT]
+  const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
   uint64_t key = ~0ull;
   const double tau = a.tau;
   const uint64_t check_pos = (step << 24) | (255ull << 8);
-  const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
-  double2* tw = sm + GE::TILE;                 // 512 twiddles
-  double2* aux = tw + 512;                     // prefetched operands: [k][r][NT]
-  constexpr int NAUX = Aux<PROG>::N;
-  if (valid) {
+
+  auto issue = [&](int tile, double2* buf) {
+    int gb, gs, rw;
+    if (tile < ntiles && map.geo(a, tile, gb, gs, rw)) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = ldg_s(src + gbase + (int64_t)(t + T * r) * gstride);
-    // the pointwise operands of the stage programs are needed only after the
-    // first transform: start their copies now (cp.async, L2-only) so their
-    // latency hides behind it
-    if (NAUX > 0) {
-      const double2* ops[2] = {a.u, PROG == FP_IF4_B4 ? a.g[0] : nullptr};
-#pragma unroll
-      for (int k = 0; k < NAUX; ++k)
-#pragma unroll
-        for (int r = 0; r < 8; ++r) cp_async16(aux + (k * 8 + r) * NT + tid, ops[k] + gbase + (t + T * r));
-      cp_async_commit();
+      for (int r = 0; r < 8; ++r) cp_async16(buf + lay.at(t + T * r), src + gb + (t + T * r) * gs);
     }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_double2(0.0, 0.0);
-  }
+    cp_async_commit();
+  };
+  issue(blockIdx.x, ring[0]);
   stage_twiddles<L>(tw, tid, NT);
   __syncthreads();
-  if (PROG == FP_STR_START) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, v[r]);
-  }
 
-  if (PROG == FP_PLAIN) {
-    fft_pencil<L, CONTIG, INV>(v, t, sm, lay, tw);
-  } else if (PROG == FP_IF4_START) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
-  } else if (PROG == FP_G) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    double2* sbuf = ring[it & 1];
+    issue(tile + (int)gridDim.x, ring[(it + 1) & 1]);
+    int gbase, gstride, row;
+    const bool valid = map.geo(a, tile, gbase, gstride, row);
+    if (NAUX > 0 && valid) {
+      // pointwise operands, needed after the first transform
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      V<1> x;
-      x.c[0] = cscale(a.scale, v[r]);
-      v[r] = gfun<1>(a.nl, x).c[0];
+      for (int r = 0; r < 8; ++r) cp_async16(aux + r * NT + tid, a.u + gbase + (t + T * r));
     }
-    __syncthreads();
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
-  } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);  // v = g_i (spectral)
-    double2 rf[2];
-    rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
-    rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
-    if (valid) {
+    cp_async_commit();
+    cp_async_wait<2>();  // this tile's main operand (the two newer groups may still fly)
+    double2 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = valid ? sbuf[lay.at(t + T * r)] : make_double2(0.0, 0.0);
+    __syncthreads();  // every thread holds its inputs: the tile buffer becomes the exchange buffer
+    if (PROG == FP_STR_START) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, v[r]);
+    }
+    bool store = true;
+    if (PROG == FP_PLAIN) {
+      fft_pencil<L, CONTIG, INV>(v, t, sbuf, lay, tw);
+    } else if (PROG == FP_IF4_START) {
+      fft_pencil<L, CONTIG, true>(v, t, sbuf, lay, tw);
+    } else if (PROG == FP_G) {
+      fft_pencil<L, CONTIG, true>(v, t, sbuf, lay, tw);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const int i = t + T * r;
-        const int64_t gi = gbase + i;
-        const double2 gi_v = v[r];
-        if (r == 0) cp_async_wait_all();
-        const double2 u = aux[r * NT + tid];
-        if (PROG == FP_IF4_B1) {
-          stg_s(a.g_out + gi, gi_v);
-          v[r] = cmul(efac(a, 0, rf, i), caxpy(0.5 * tau, gi_v, u));
-        } else if (PROG == FP_IF4_B2) {
-          stg_s(a.g_out + gi, gi_v);
-          v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, rf, i), u));
-        } else if (PROG == FP_IF4_B3) {
-          stg_s(a.g_out + gi, gi_v);
-          v[r] = caxpy(tau, cmul(efac(a, 0, rf, i), gi_v), cmul(efac(a, 1, rf, i), u));
-        } else {
-          const double2 g1 = aux[(8 + r) * NT + tid], g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
-          const double2 out =
-              caxpy(tau / 6.0, gi_v,
-                    caxpy(tau / 3.0, cmul(efac(a, 0, rf, i), caxpy(1.0, g2, g3)),
-                          cmul(efac(a, 1, rf, i), caxpy(tau / 6.0, g1, u))));
-          if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
-          stg_s(a.u_out + gi, out);
-          v[r] = out;
+        V<1> x;
+        x.c[0] = cscale(a.scale, v[r]);
+        v[r] = gfun<1>(a.nl, x).c[0];
+      }
+      __syncthreads();
+      fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);
+    } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
+      fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);  // v = g_i (spectral)
+      cp_async_wait<1>();                                 // the stage operands (the prefetch may fly)
+      double2 rf[2];
+      rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
+      rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = t + T * r;
+          const int gi = gbase + i;
+          const double2 gi_v = v[r];
+          const double2 u = aux[r * NT + tid];
+          if (PROG == FP_IF4_B1) {
+            stg_s(a.g_out + gi, gi_v);
+            v[r] = cmul(efac(a, 0, rf, i), caxpy(0.5 * tau, gi_v, u));
+          } else if (PROG == FP_IF4_B2) {
+            stg_s(a.g_out + gi, gi_v);
+            v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, rf, i), u));
+          } else if (PROG == FP_IF4_B3) {
+            stg_s(a.g_out + gi, gi_v);
+            v[r] = caxpy(tau, cmul(efac(a, 0, rf, i), gi_v), cmul(efac(a, 1, rf, i), u));
+          } else {
+            const double2 g1 = ldg_s(a.g[0] + gi), g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
+            const double2 out =
+                caxpy(tau / 6.0, gi_v,
+                      caxpy(tau / 3.0, cmul(efac(a, 0, rf, i), caxpy(1.0, g2, g3)),
+                            cmul(efac(a, 1, rf, i), caxpy(tau / 6.0, g1, u))));
+            if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+            stg_s(a.u_out + gi, out);
+            v[r] = out;
+          }
         }
       }
-    }
-    if (PROG == FP_IF4_B4 && a.dst == nullptr) {
-      raise_min(a.flag, key);
-      return;
-    }
-    __syncthreads();
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
-  } else if (PROG == FP_STR_START) {
+      if (PROG == FP_IF4_B4 && a.dst == nullptr) {
+        store = false;
+      } else {
+        __syncthreads();
+        fft_pencil<L, CONTIG, true>(v, t, sbuf, lay, tw);
+      }
+    } else if (PROG == FP_STR_START) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      V<1> x;
-      x.c[0] = v[r];
-      v[r] = flow<1>(a.nl, x, 0.5 * tau, step, 0, key).c[0];
-    }
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
-  } else if (PROG == FP_STR_A0) {
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
+      for (int r = 0; r < 8; ++r) {
+        V<1> x;
+        x.c[0] = v[r];
+        v[r] = flow<1>(a.nl, x, 0.5 * tau, step, 0, key).c[0];
+      }
+      fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);
+    } else if (PROG == FP_STR_A0) {
+      fft_pencil<L, CONTIG, true>(v, t, sbuf, lay, tw);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      V<1> x;
-      x.c[0] = cscale(a.scale, v[r]);
-      const double2 out = flow<1>(a.nl, x, 0.5 * tau, step, a.fw, key).c[0];
-      if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
-      if (valid) stg_s(a.u_out + gbase + (int64_t)(t + T * r) * gstride, out);
-      x.c[0] = out;
-      v[r] = flow<1>(a.nl, x, 0.5 * tau, step + 1, 0, key).c[0];
-    }
-    if (a.dst == nullptr) {
-      raise_min(a.flag, valid ? key : ~0ull);
-      return;
-    }
-    __syncthreads();
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
-  } else if (PROG == FP_STR_MID) {
-    fft_pencil<L, CONTIG, false>(v, t, sm, lay, tw);
-    double2 rf[2];
-    rf[1] = valid ? row_factor(a, 1, row) : make_double2(0.0, 0.0);
-    rf[0] = rf[1];
+      for (int r = 0; r < 8; ++r) {
+        V<1> x;
+        x.c[0] = cscale(a.scale, v[r]);
+        const double2 out = flow<1>(a.nl, x, 0.5 * tau, step, a.fw, key).c[0];
+        if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+        if (valid) stg_s(a.u_out + gbase + (t + T * r) * gstride, out);
+        x.c[0] = out;
+        v[r] = flow<1>(a.nl, x, 0.5 * tau, step + 1, 0, key).c[0];
+      }
+      if (a.dst == nullptr) {
+        store = false;
+      } else {
+        __syncthreads();
+        fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);
+      }
+    } else if (PROG == FP_STR_MID) {
+      fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);
+      double2 rf[2];
+      rf[1] = valid ? row_factor(a, 1, row) : make_double2(0.0, 0.0);
+      rf[0] = rf[1];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, rf, t + T * r), v[r]);
-    __syncthreads();
-    fft_pencil<L, CONTIG, true>(v, t, sm, lay, tw);
+      for (int r = 0; r < 8; ++r) v[r] = cmul(efac(a, 1, rf, t + T * r), v[r]);
+      __syncthreads();
+      fft_pencil<L, CONTIG, true>(v, t, sbuf, lay, tw);
+    }
+    if (valid && store) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (t + T * r) * gstride, v[r]);
+    }
+    if (!valid) key = ~0ull;
+    __syncthreads();  // the exchange reads of this tile are done before its buffer is refilled
   }
-
-  if (valid) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (int64_t)(t + T * r) * gstride, v[r]);
-  }
-  if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, valid ? key : ~0ull);
+  cp_async_wait<0>();
+  if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, key);
 }
 
 static int threads_for(int L) {
@@ -480,16 +517,21 @@ template <int L, bool CONTIG, int PROG, bool INV, int NT>
 static int launch_nt(const Args& a, cudaStream_t st) {
   using GE = Geo<L, CONTIG, NT>;
   auto kern = fft_pass_kernel<L, CONTIG, PROG, INV, NT>;
-  static bool attr = false;
-  const int smem = (GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
-  if (!attr) {
+  static int blocks_per_sm = 0, sms = 0;
+  const int smem = (2 * GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
+  if (blocks_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(fft_pass)");
-    attr = true;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, NT, smem);
+    if (e != cudaSuccess || blocks_per_sm < 1) return set_cuda_error(e, "fft_pass occupancy");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t tiles = CONTIG ? (a.O + GE::ROWS - 1) / GE::ROWS : ((a.O * (a.I / GE::CW)) + GE::G - 1) / GE::G;
   if (tiles <= 0) return 0;
-  cudaError_t e = launch_k(kern, dim3((unsigned)tiles), dim3(NT), (size_t)smem, st, dim3(1), a);
+  int64_t grid = (int64_t)sms * blocks_per_sm;
+  if (grid > tiles) grid = tiles;
+  cudaError_t e = launch_k(kern, dim3((unsigned)grid), dim3(NT), (size_t)smem, st, dim3(1), a, tiles);
   if (e != cudaSuccess) return set_cuda_error(e, "fft_pass launch");
   return check_launch("fft_pass_kernel");
 }
@@ -590,6 +632,7 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
       for (int d = 0; d < ndim; ++d)
         if (!a.tab[fr][d]) return set_error(CGL_EINVAL, "fft_pass: program needs the exp tables");
   if (!contig && a.I % 8) return set_error(CGL_ESHAPE, "fft_pass: strided axis needs inner extent % 8 == 0");
+  // 32-bit element offsets in the kernels: extents <= 512 in <= 3D keep N <= 2^27
   switch (L) {
     case 16: return launch_L<16>(program, contig, inverse != 0, a, st);
     case 32: return launch_L<32>(program, contig, inverse != 0, a, st);
