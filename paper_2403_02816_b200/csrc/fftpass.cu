@@ -361,8 +361,9 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   Lay<L, CONTIG> lay;
   lay.base = map.lay_base();
   lay.cw = CONTIG ? 0 : GE::CW;
+  constexpr bool RING = CONTIG;                // strided passes: one tile per CTA, loads straight to registers
   double2* ring[2] = {sm, sm + GE::TILE};
-  double2* tw = sm + 2 * GE::TILE;             // per-stage twiddle tables (< 512 entries)
+  double2* tw = sm + (RING ? 2 : 1) * GE::TILE;  // per-stage twiddle tables (< 512 entries)
   double2* aux = tw + 512;                     // stage operands of the current tile: [k][r][NT]
   const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
   uint64_t key = ~0ull;
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   const uint64_t check_pos = (step << 24) | (255ull << 8);
 
   auto issue = [&](int tile, double2* buf) {
+    if (!RING) return;
     int gb, gs, rw;
     if (tile < ntiles && map.geo(a, tile, gb, gs, rw)) {
 #pragma unroll
@@ -393,11 +395,16 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       for (int r = 0; r < 8; ++r) cp_async16(aux + r * NT + tid, a.u + gbase + (t + T * r));
     }
     cp_async_commit();
-    cp_async_wait<2>();  // this tile's main operand (the two newer groups may still fly)
     double2 v[8];
+    if (RING) {
+      cp_async_wait<2>();  // this tile's main operand (the two newer groups may still fly)
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = valid ? sbuf[lay.at(t + T * r)] : make_double2(0.0, 0.0);
-    __syncthreads();  // every thread holds its inputs: the tile buffer becomes the exchange buffer
+      for (int r = 0; r < 8; ++r) v[r] = valid ? sbuf[lay.at(t + T * r)] : make_double2(0.0, 0.0);
+      __syncthreads();  // every thread holds its inputs: the tile buffer becomes the exchange buffer
+    } else {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = valid ? ldg_s(src + gbase + (t + T * r) * gstride) : make_double2(0.0, 0.0);
+    }
     if (PROG == FP_STR_START) {
 #pragma unroll
       for (int r = 0; r < 8; ++r) v[r] = cscale(a.scale, v[r]);
@@ -518,7 +525,7 @@ static int launch_nt(const Args& a, cudaStream_t st) {
   using GE = Geo<L, CONTIG, NT>;
   auto kern = fft_pass_kernel<L, CONTIG, PROG, INV, NT>;
   static int blocks_per_sm = 0, sms = 0;
-  const int smem = (2 * GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
+  const int smem = ((CONTIG ? 2 : 1) * GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, NT, smem);
@@ -529,7 +536,8 @@ static int launch_nt(const Args& a, cudaStream_t st) {
   }
   const int64_t tiles = CONTIG ? (a.O + GE::ROWS - 1) / GE::ROWS : ((a.O * (a.I / GE::CW)) + GE::G - 1) / GE::G;
   if (tiles <= 0) return 0;
-  int64_t grid = (int64_t)sms * blocks_per_sm;
+  // contiguous passes: persistent CTAs over the tile ring; strided passes: one tile per CTA
+  int64_t grid = CONTIG ? (int64_t)sms * blocks_per_sm : tiles;
   if (grid > tiles) grid = tiles;
   cudaError_t e = launch_k(kern, dim3((unsigned)grid), dim3(NT), (size_t)smem, st, dim3(1), a, tiles);
   if (e != cudaSuccess) return set_cuda_error(e, "fft_pass launch");
