@@ -379,6 +379,15 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
     }
     cp_async_commit();
   };
+  // strided passes (one tile per CTA): the tile's loads go out before the
+  // twiddle tables are staged, so their latency overlaps the staging
+  double2 v[8];
+  if (!RING) {
+    int gb, gs, rw;
+    const bool ok = map.geo(a, blockIdx.x, gb, gs, rw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = ok ? ldg_s(src + gb + (t + T * r) * gs) : make_double2(0.0, 0.0);
+  }
   issue(blockIdx.x, ring[0]);
   stage_twiddles<L>(tw, tid, NT);
   __syncthreads();
@@ -386,24 +395,21 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     double2* sbuf = ring[it & 1];
-    issue(tile + (int)gridDim.x, ring[(it + 1) & 1]);
     int gbase, gstride, row;
     const bool valid = map.geo(a, tile, gbase, gstride, row);
     if (NAUX > 0 && valid) {
-      // pointwise operands, needed after the first transform
+      // pointwise operands, needed after the first transform (committed before
+      // the next tile's prefetch so that wait_group 1 covers them)
 #pragma unroll
       for (int r = 0; r < 8; ++r) cp_async16(aux + r * NT + tid, a.u + gbase + (t + T * r));
     }
     cp_async_commit();
-    double2 v[8];
+    issue(tile + (int)gridDim.x, ring[(it + 1) & 1]);
     if (RING) {
       cp_async_wait<2>();  // this tile's main operand (the two newer groups may still fly)
 #pragma unroll
       for (int r = 0; r < 8; ++r) v[r] = valid ? sbuf[lay.at(t + T * r)] : make_double2(0.0, 0.0);
       __syncthreads();  // every thread holds its inputs: the tile buffer becomes the exchange buffer
-    } else {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = valid ? ldg_s(src + gbase + (t + T * r) * gstride) : make_double2(0.0, 0.0);
     }
     if (PROG == FP_STR_START) {
 #pragma unroll
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
       fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);
     } else if (PROG == FP_IF4_B1 || PROG == FP_IF4_B2 || PROG == FP_IF4_B3 || PROG == FP_IF4_B4) {
       fft_pencil<L, CONTIG, false>(v, t, sbuf, lay, tw);  // v = g_i (spectral)
-      cp_async_wait<1>();                                 // the stage operands (the prefetch may fly)
+      cp_async_wait<RING ? 1 : 0>();                      // the stage operands (the prefetch may fly)
       double2 rf[2];
       rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
       rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
