@@ -127,7 +127,7 @@ __device__ __forceinline__ void dft4(double2 (&a)[4]) {
 // conflicts (a 512-entry table indexed by m k 512/(Ns R) puts them 8 words
 // apart).
 __device__ __forceinline__ double2 twiddle(const double2* tw, int idx, bool inv) {
-  const double2 w = tw[idx];
+  const double2 w = tw[idx];  // shared (persistent CTAs) or the global table through L1
   return inv ? make_double2(w.x, -w.y) : w;
 }
 
@@ -146,20 +146,11 @@ struct Plan {
   static constexpr int twsize() { return twbase(nstages); }
 };
 
-// per-stage twiddle tables of a length-L transform (see twiddle())
+// per-stage twiddle tables of a length-L transform (see twiddle()), copied
+// from the generated global table into shared memory by persistent CTAs
 template <int L>
 __device__ __forceinline__ void stage_twiddles(double2* tw, int tid, int nt) {
-  using PL = Plan<L>;
-  for (int e = tid; e < PL::twsize(); e += nt) {
-    int s = 1;
-#pragma unroll
-    for (int q = 2; q < PL::nstages; ++q)
-      if (e >= PL::twbase(q)) s = q;
-    const int off = e - PL::twbase(s);
-    const int Ns = PL::ns(s), R = PL::radix(s);
-    const int m = off / Ns + 1, k = off % Ns;
-    tw[e] = __ldg(&g_fft_tw512[(m * k * (512 / (Ns * R))) & 511]);
-  }
+  for (int e = tid; e < Plan<L>::twsize(); e += nt) tw[e] = __ldg(&g_fft_stage_tw[fft_stage_tw_offset(L) + e]);
 }
 
 // shared-memory slot of element i of the calling thread's pencil
@@ -291,10 +282,13 @@ struct Geo {
 };
 
 // registers per thread the program needs to co-reside MINB CTAs per SM
-template <int PROG, int NT>
+template <int PROG, int NT, bool CONTIG>
 struct Occ {
   // shared memory: 2 tiles of 32 KB + 8 KB twiddles (+ 32 KB stage operands for B1..B4)
-  static constexpr int MINB = NT >= 512 ? 1 : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4) ? 2 : 3;
+  static constexpr int MINB = NT >= 512                                   ? 1
+                              : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4)   ? 2
+                              : (PROG == FP_PLAIN && !CONTIG)              ? 4
+                                                                           : 3;
 };
 
 // Persistent pass kernel: each CTA walks tiles blockIdx.x, +gridDim.x, ...
@@ -343,7 +337,7 @@ struct TileMap {
 };
 
 template <int L, bool CONTIG, int PROG, bool INV, int NT>
-__global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const Args a, const int ntiles) {
+__global__ void __launch_bounds__(NT, Occ<PROG, NT, CONTIG>::MINB) fft_pass_kernel(const Args a, const int ntiles) {
   using GE = Geo<L, CONTIG, NT>;
   constexpr int T = GE::T;
   constexpr int NAUX = Aux<PROG>::N;
@@ -363,8 +357,11 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   lay.cw = CONTIG ? 0 : GE::CW;
   constexpr bool RING = CONTIG;                // strided passes: one tile per CTA, loads straight to registers
   double2* ring[2] = {sm, sm + GE::TILE};
-  double2* tw = sm + (RING ? 2 : 1) * GE::TILE;  // per-stage twiddle tables (< 512 entries)
-  double2* aux = tw + 512;                     // stage operands of the current tile: [k][r][NT]
+  // per-stage twiddles: staged in shared memory by the persistent (contiguous)
+  // CTAs; one-tile strided CTAs read the global table through L1
+  double2* tws = sm + (RING ? 2 : 1) * GE::TILE;
+  const double2* tw = RING ? tws : g_fft_stage_tw + fft_stage_tw_offset(L);
+  double2* aux = tws + (RING ? 512 : 0);       // stage operands of the current tile: [k][r][NT]
   const double2* src = (PROG == FP_IF4_START || PROG == FP_STR_START) ? a.u : a.src;
   uint64_t key = ~0ull;
   const double tau = a.tau;
@@ -389,8 +386,10 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
     for (int r = 0; r < 8; ++r) v[r] = ok ? ldg_s(src + gb + (t + T * r) * gs) : make_double2(0.0, 0.0);
   }
   issue(blockIdx.x, ring[0]);
-  stage_twiddles<L>(tw, tid, NT);
-  __syncthreads();
+  if (RING) {
+    stage_twiddles<L>(tws, tid, NT);
+    __syncthreads();
+  }
 
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -517,6 +516,82 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT>::MINB) fft_pass_kernel(const
   if (PROG == FP_IF4_B4 || PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, key);
 }
 
+// Strided-axis pass: one tile (G chunks of CW adjacent pencils) per CTA,
+// straight-line -- loads go to registers first, the per-stage twiddles come
+// from the global table through L1, the tile buffer is the exchange buffer.
+// (A persistent ring does not pay here: the 64-byte chunks at an 8 KB / 4 MB
+// stride are DRAM-activation-bound, and the ring's registers cost occupancy.)
+template <int L, int PROG, bool INV, int NT>
+__global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_kernel(const Args a, const int ntiles) {
+  using GE = Geo<L, false, NT>;
+  constexpr int T = GE::T;
+  extern __shared__ double2 sm[];
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t step = resolve_pos(a.flag, a.pos) >> 24;
+  if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)(PROG == FP_STR_A0 ? a.fw : 0) << 8))) return;
+  const int tid = threadIdx.x;
+  const TileMap<L, false, NT> map(tid);
+  const int t = map.t;
+  Lay<L, false> lay;
+  lay.base = map.lay_base();
+  lay.cw = GE::CW;
+  const double2* tw = g_fft_stage_tw + fft_stage_tw_offset(L);
+  int gbase, gstride, row;
+  const bool valid = map.geo(a, blockIdx.x, gbase, gstride, row);
+  const double2* src = PROG == FP_STR_START ? a.u : a.src;
+  double2 v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = valid ? ldg_s(src + gbase + (t + T * r) * gstride) : make_double2(0.0, 0.0);
+  uint64_t key = ~0ull;
+  const double tau = a.tau;
+  if (PROG == FP_PLAIN) {
+    fft_pencil<L, false, INV>(v, t, sm, lay, tw);
+  } else if (PROG == FP_G) {
+    fft_pencil<L, false, true>(v, t, sm, lay, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      v[r] = gfun<1>(a.nl, x).c[0];
+    }
+    __syncthreads();
+    fft_pencil<L, false, false>(v, t, sm, lay, tw);
+  } else if (PROG == FP_STR_START) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      v[r] = flow<1>(a.nl, x, 0.5 * tau, step, 0, key).c[0];
+    }
+    fft_pencil<L, false, false>(v, t, sm, lay, tw);
+  } else if (PROG == FP_STR_A0) {
+    const uint64_t check_pos = (step << 24) | (255ull << 8);
+    fft_pencil<L, false, true>(v, t, sm, lay, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      const double2 out = flow<1>(a.nl, x, 0.5 * tau, step, a.fw, key).c[0];
+      if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
+      if (valid) stg_s(a.u_out + gbase + (t + T * r) * gstride, out);
+      x.c[0] = out;
+      v[r] = flow<1>(a.nl, x, 0.5 * tau, step + 1, 0, key).c[0];
+    }
+    if (a.dst == nullptr) {
+      raise_min(a.flag, valid ? key : ~0ull);
+      return;
+    }
+    __syncthreads();
+    fft_pencil<L, false, false>(v, t, sm, lay, tw);
+  }
+  if (valid) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (t + T * r) * gstride, v[r]);
+  }
+  if (PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, valid ? key : ~0ull);
+}
+
 static int threads_for(int L) {
   static int forced = -1;
   if (forced < 0) {
@@ -529,9 +604,12 @@ static int threads_for(int L) {
 template <int L, bool CONTIG, int PROG, bool INV, int NT>
 static int launch_nt(const Args& a, cudaStream_t st) {
   using GE = Geo<L, CONTIG, NT>;
-  auto kern = fft_pass_kernel<L, CONTIG, PROG, INV, NT>;
+  void (*kern)(const Args, const int);
+  if constexpr (CONTIG) kern = fft_pass_kernel<L, true, PROG, INV, NT>;
+  else kern = fft_strided_kernel<L, PROG, INV, NT>;
   static int blocks_per_sm = 0, sms = 0;
-  const int smem = ((CONTIG ? 2 : 1) * GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2);
+  const int smem = CONTIG ? (2 * GE::TILE + 512 + Aux<PROG>::N * 8 * NT) * (int)sizeof(double2)
+                          : GE::TILE * (int)sizeof(double2);
   if (blocks_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, NT, smem);
