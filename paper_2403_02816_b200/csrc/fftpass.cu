@@ -285,7 +285,7 @@ struct Geo {
 template <int PROG, int NT, bool CONTIG>
 struct Occ {
   // shared memory: 2 tiles of 32 KB + 8 KB twiddles (+ 32 KB stage operands for B1..B4)
-  static constexpr int MINB = NT >= 512                                   ? 1
+  static constexpr int MINB = NT >= 512                                   ? ((PROG == FP_PLAIN && !CONTIG) ? 2 : 1)
                               : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4)   ? 2
                               : (PROG == FP_PLAIN && !CONTIG)              ? 4
                                                                            : 3;
