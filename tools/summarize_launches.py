@@ -15,7 +15,7 @@ for r in rows[hdr + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
-    name = r[ki].split("(")[0][:60]
+    name = r[ki].split("(")[0][:90]
     tot[name] += v
     cnt[name] += 1
 T = sum(tot.values())
