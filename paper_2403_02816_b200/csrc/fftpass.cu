@@ -42,6 +42,10 @@
 #include "fft_twiddles.h"
 #include "stage_ops.cuh"
 
+#ifndef CGL_FFT_GV
+#define CGL_FFT_GV 0  // A/B (tools/fft_probe.py): G pass at 256 threads (0), 512 x 1 CTA (1), 512 x 2 CTAs (2)
+#endif
+
 namespace cgl {
 namespace fftp {
 
@@ -285,7 +289,7 @@ struct Geo {
 template <int PROG, int NT, bool CONTIG>
 struct Occ {
   // shared memory: 2 tiles of 32 KB + 8 KB twiddles (+ 32 KB stage operands for B1..B4)
-  static constexpr int MINB = NT >= 512                                   ? ((PROG == FP_PLAIN && !CONTIG) ? 2 : 1)
+  static constexpr int MINB = NT >= 512                                   ? ((PROG == FP_PLAIN || (PROG == FP_G && CGL_FFT_GV == 2)) ? 2 : 1)
                               : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4)   ? 2
                               : (PROG == FP_PLAIN && !CONTIG)              ? 4
                                                                            : 3;
@@ -526,8 +530,10 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
   using GE = Geo<L, false, NT>;
   constexpr int T = GE::T;
   extern __shared__ double2 sm[];
+  // dependents are released only when this CTA is done: with tens of
+  // thousands of CTAs an early trigger would let the next grid's waiting CTAs
+  // take the slots this grid's remaining CTAs need
   pdl_wait();
-  pdl_trigger();
   const uint64_t step = resolve_pos(a.flag, a.pos) >> 24;
   if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)(PROG == FP_STR_A0 ? a.fw : 0) << 8))) return;
   const int tid = threadIdx.x;
@@ -580,6 +586,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
     }
     if (a.dst == nullptr) {
       raise_min(a.flag, valid ? key : ~0ull);
+      pdl_trigger();
       return;
     }
     __syncthreads();
@@ -590,15 +597,16 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
     for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (t + T * r) * gstride, v[r]);
   }
   if (PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, valid ? key : ~0ull);
+  pdl_trigger();
 }
 
-static int threads_for(int L) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("CGL_FFT_NT");
-    forced = e ? atoi(e) : 0;
-  }
-  return (forced == 512 && L == 512) ? 512 : 256;
+// threads per CTA: 256 for the contiguous ring (measured: 92% of HBM vs 77%
+// at 512); 512 for strided 512-point passes, so a chunk is 8 pencils = one
+// 128-byte line per axis index (81% / 73% on axes 1 / 0 vs 72% / 46% with
+// 64-byte chunks at 256 threads)
+static int threads_for(int L, bool contig, int prog) {
+  if (prog == FP_G && CGL_FFT_GV == 0) return 256;
+  return (!contig && L == 512) ? 512 : 256;
 }
 
 template <int L, bool CONTIG, int PROG, bool INV, int NT>
@@ -630,8 +638,8 @@ static int launch_nt(const Args& a, cudaStream_t st) {
 
 template <int L, bool CONTIG, int PROG, bool INV>
 static int launch_one(const Args& a, cudaStream_t st) {
-  if constexpr (L == 512) {
-    if (threads_for(L) == 512) return launch_nt<L, CONTIG, PROG, INV, 512>(a, st);
+  if constexpr (L == 512 && !CONTIG) {
+    if (threads_for(L, CONTIG, PROG) == 512) return launch_nt<L, CONTIG, PROG, INV, 512>(a, st);
   }
   return launch_nt<L, CONTIG, PROG, INV, 256>(a, st);
 }
