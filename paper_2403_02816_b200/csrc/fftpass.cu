@@ -42,9 +42,6 @@
 #include "fft_twiddles.h"
 #include "stage_ops.cuh"
 
-#ifndef CGL_FFT_GV
-#define CGL_FFT_GV 0  // A/B (tools/fft_probe.py): G pass at 256 threads (0), 512 x 1 CTA (1), 512 x 2 CTAs (2)
-#endif
 
 namespace cgl {
 namespace fftp {
@@ -289,7 +286,7 @@ struct Geo {
 template <int PROG, int NT, bool CONTIG>
 struct Occ {
   // shared memory: 2 tiles of 32 KB + 8 KB twiddles (+ 32 KB stage operands for B1..B4)
-  static constexpr int MINB = NT >= 512                                   ? ((PROG == FP_PLAIN || (PROG == FP_G && CGL_FFT_GV == 2)) ? 2 : 1)
+  static constexpr int MINB = NT >= 512                                   ? ((PROG == FP_PLAIN || PROG == FP_G) ? 2 : 1)
                               : (PROG >= FP_IF4_B1 && PROG <= FP_IF4_B4)   ? 2
                               : (PROG == FP_PLAIN && !CONTIG)              ? 4
                                                                            : 3;
@@ -600,12 +597,18 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
   pdl_trigger();
 }
 
-// threads per CTA: 256 for the contiguous ring (measured: 92% of HBM vs 77%
-// at 512); 512 for strided 512-point passes, so a chunk is 8 pencils = one
-// 128-byte line per axis index (81% / 73% on axes 1 / 0 vs 72% / 46% with
-// 64-byte chunks at 256 threads)
+// Threads per CTA, chosen by same-box A/B at 512^3 (tools/fft_probe.py,
+// profiles/r02_fft_passes.txt):
+//  * contiguous ring: 256 (92% of HBM; 77% at 512);
+//  * strided 512-point passes: 512, so a chunk is 8 pencils = one 128-byte
+//    line per axis index (plain 81% / 76% on axes 1 / 0 vs 72% / 46% with
+//    64-byte chunks at 256); the fused g pass at 2 CTAs x 64 registers
+//    (1.50 ms, vs 1.63 at 1 CTA and 1.67 at 256 threads);
+//  * strided strang flow passes: 256 x 3 CTAs (3.67 ms vs 4.64 at 512): the
+//    two exact flows per point are FP64-latency-bound and want warps more
+//    than 128-byte chunks.
 static int threads_for(int L, bool contig, int prog) {
-  if (prog == FP_G && CGL_FFT_GV == 0) return 256;
+  if (prog == FP_STR_A0 || prog == FP_STR_START) return 256;
   return (!contig && L == 512) ? 512 : 256;
 }
 
