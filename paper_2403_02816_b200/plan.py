@@ -437,6 +437,11 @@ class FusedPlan:
                 torch.cuda.current_stream().synchronize()
                 key = diverged(flag[0].item())
                 if key is not None:
+                    # the end-of-step pass of step k-1 also runs step k's first
+                    # flow: a divergence there (key step k) leaves step k-1
+                    # complete, and the reference snapshots it before failing
+                    if (key >> 24) > k - 1 and (k - 1) in stops and on_stop is not None:
+                        on_stop(k - 1, self.result(k - 1))
                     return key
                 if (k - 1) in stops and on_stop is not None:
                     on_stop(k - 1, self.result(k - 1))

@@ -30,14 +30,16 @@ def spectral_ic(seed, shape, amp):
     return np.fft.fftn(amp * rc(np.random.default_rng(seed), shape))
 
 
-def bump_ic(shape, intervals, amp):
-    """Centred Gaussian bump (coefficient space): grows smoothly under an
-    explosive nonlinearity, so a divergence lands after a few good steps."""
+def bump_ic(shape, intervals, amp, spectral=True):
+    """Centred Gaussian bump (coefficient space for Fourier cases): grows
+    smoothly under an explosive nonlinearity, so a divergence lands after a
+    few good steps."""
     ax = [a + (b - a) * np.arange(n) / n for n, (a, b) in zip(shape, intervals)]
     d = len(shape)
     r2 = sum(((x - (a + b) / 2) ** 2).reshape([-1 if j == i else 1 for j in range(d)])
              for i, (x, (a, b)) in enumerate(zip(ax, intervals)))
-    return np.fft.fftn(amp * np.exp(-r2) * (1 + 0.1j))
+    u = amp * np.exp(-r2) * (1 + 0.1j)
+    return np.fft.fftn(u) if spectral else u
 
 
 def cases():
@@ -72,13 +74,20 @@ def divergence_cases():
         dict(name="div_p3_cq_rk4flow_strang", extents=(16, 16, 16), intervals=((-3.0, 3.0),) * 3,
              params=dict(CQ, alpha4=3.0), kind="cubic_quintic", scheme="strang", t_final=1.0, steps=10,
              lo=0.6, hi=1.1, want="RK4"),
+        # FD (Kronecker) strang: the fused end-of-step kernel also runs the next
+        # step's first flow, so a blow-up there must still leave the last
+        # snapshot the reference takes
+        dict(name="div_fd_blow_strang", op="fd", bc="dirichlet", extents=(16, 16), lengths=(8.0, 8.0),
+             intervals=((-4.0, 4.0),) * 2, params=P_BLOW, kind="cubic", scheme="strang", t_final=0.5, steps=10,
+             lo=1.2, hi=2.6, want="blow-up"),
     ]
     out = []
     for sp in specs:
         hit = None
         for amp in np.geomspace(sp["lo"], sp["hi"], 81):
-            ic = bump_ic(sp["extents"], sp["intervals"], amp)
-            case = dict(sp, op="fourier", ic=[ic])
+            op = sp.get("op", "fourier")
+            ic = bump_ic(sp["extents"], sp["intervals"], amp, spectral=op == "fourier")
+            case = dict(sp, op=op, ic=[ic])
             res = rint.integrate(_ref_problem(case), case["scheme"], (ic,), case["t_final"], case["steps"])
             if res.diverged and 3 <= res.diverged_at <= 8 and sp["want"] in res.reason:
                 hit = dict(case, amp=float(amp))

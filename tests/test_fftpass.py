@@ -101,7 +101,8 @@ def test_pencil_plan_against_reference(pencil_golden, name):
     snaps = []
     res = P.integrate(prob, case["scheme"], (arrays[f"s{i}_ic0"],), case["t_final"], case["steps"],
                       snapshot_steps=case["snapshot_steps"], on_snapshot=lambda k, t, f: snaps.append((k, f[0])))
-    assert any(isinstance(p, PencilFourierPlan) for p in prob._plans.values()), "pencil plan not used"
+    if case["op"] == "fourier":
+        assert any(isinstance(p, PencilFourierPlan) for p in prob._plans.values()), "pencil plan not used"
     assert (res.diverged, res.diverged_at, res.reason) == (case["diverged"], case["diverged_at"], case["reason"])
     ref = arrays[f"s{i}_out0"]
     if np.all(np.isfinite(ref)):

@@ -696,3 +696,24 @@ def test_snapshot_from_device_streamed(P, unit_golden, tmp_path):
     cio.write_snapshot(path, (torch.from_numpy(g["snap_u"]).cuda(), torch.from_numpy(g["snap_v"]).cuda()), 0.75,
                        grids, chunk_bytes=16 * 3 * 4 * 2)
     assert path.read_bytes() == g["snap_bytes"].tobytes()
+
+
+def test_cached_dmma_plan_replays_after_workspace_growth(P):
+    """ADVICE r1 (zgemm.cu stream-K state): a graph-captured DMMA plan (C0,
+    128^2) must replay correctly after a larger DMMA product grew the shared
+    stream-K workspace, and must not write into memory handed out since
+    (the outgrown buffer is retired, never freed)."""
+    from paper_2403_02816_b200 import tensors, workloads as W
+    w = W.CONFIGS["C0"]
+    prob = W.build_problem(w)
+    x0 = W.state_for_problem(w, W.initial_state_device(w))
+    first = P.integrate(prob, "strang", (x0,), w.t_final, w.steps).fields[0].clone()
+    rng = np.random.default_rng(5)
+    big = torch.from_numpy(rng.standard_normal((1024, 1024)) + 1j * rng.standard_normal((1024, 1024))).cuda()
+    m = torch.from_numpy(rng.standard_normal((1024, 1024)) + 0j).cuda()
+    tensors.mu_mode_product(big, m, 0)          # DMMA product with many more stream-K CTAs
+    canaries = [torch.full((1 << 20,), 7.0, dtype=torch.float64, device="cuda") for _ in range(64)]
+    again = P.integrate(prob, "strang", (x0,), w.t_final, w.steps).fields[0]
+    assert torch.equal(first, again)
+    torch.cuda.synchronize()
+    assert all(bool((c == 7.0).all()) for c in canaries)
