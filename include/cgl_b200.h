@@ -32,6 +32,8 @@ extern "C" {
 #define CGL_EINVAL (-1)
 #define CGL_ESHAPE (-2)
 #define CGL_ECUFFT (-3)
+#define CGL_ENCCL (-4)       /* an NCCL call failed                                 */
+#define CGL_EUNAVAILABLE (-5) /* NCCL is not loaded in this process                  */
 
 /* Sticky divergence record + device step base (24 bytes, device memory).
  * key = (step << 24) | (seq << 8) | reason, atomically min-reduced, so it
@@ -395,6 +397,23 @@ typedef struct {
 int cgl_fft_pass_supported(int ndim, const int64_t* shape);
 int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse,
                  const double* src, double* dst, const cgl_fft_ops_t* ops);
+
+/* ---- Slab-sharded axis-0 transposes (csrc/slab.cu) ------------------------
+ * A rank's slab of a global (world*planes, world*cols) field (axis 0 split,
+ * C order) <-> its (world*planes, cols) column block, so the mu-mode product
+ * along the sharded axis 0 (tensors.py:38-59, mu = 0) runs on whole fibres.
+ * pack:   slab (planes, world, cols) -> blocks [world][planes][cols]
+ * unpack: blocks [world][planes][cols] -> slab (planes, world, cols) */
+int cgl_slab_pack(void* stream, int64_t world, int64_t planes, int64_t cols, const double* slab, double* blocks);
+int cgl_slab_unpack(void* stream, int64_t world, int64_t planes, int64_t cols, const double* blocks,
+                    double* slab);
+/* dir 0: slab -> column block (pack into work, all-to-all into out);
+ * dir 1: column block -> slab (all-to-all into work, unpack into out).
+ * comm: the caller's ncclComm_t (world ranks); NCCL is resolved at run time
+ * from the process (CGL_EUNAVAILABLE if none is loaded).  work: scratch of
+ * planes*world*cols complex values.  in/out/work must not overlap. */
+int cgl_slab_transpose(void* stream, void* comm, int world, int dir, int64_t planes, int64_t cols,
+                       const double* in, double* out, double* work);
 
 #ifdef __cplusplus
 }

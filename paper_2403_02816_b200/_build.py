@@ -78,7 +78,7 @@ def build(force=False, verbose=False, csrc=CSRC, out=LIB, extra_flags=()):
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = out + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcufft", "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcufft", "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)

@@ -142,6 +142,9 @@ _SIGS = {
     "cgl_fft_exec": (c_int, [c_ptr, c_ptr, c_ptr, c_ptr, c_int]),
     "cgl_fft_destroy": (c_int, [c_ptr]),
     "cgl_fft_pass_supported": (c_int, [c_int, c_ptr]),
+    "cgl_slab_pack": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
+    "cgl_slab_unpack": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
+    "cgl_slab_transpose": (c_int, [c_ptr, c_ptr, c_int, c_int, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
     "cgl_fft_pass": (c_int, [c_ptr, c_int, c_int, c_ptr, c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(FftOps)]),
 }
 

@@ -336,6 +336,30 @@ int cgl_stage_fourier_cols(void* stream, int program, int nfields, int ndim, con
                       ndim, shape, tables, cols, col_offset);
 }
 
+int cgl_slab_pack(void* stream, int64_t world, int64_t planes, int64_t cols, const double* slab, double* blocks) {
+  return slab_rows((cudaStream_t)stream, slab, blocks, world, planes, cols, 0);
+}
+
+int cgl_slab_unpack(void* stream, int64_t world, int64_t planes, int64_t cols, const double* blocks, double* slab) {
+  return slab_rows((cudaStream_t)stream, blocks, slab, world, planes, cols, 1);
+}
+
+int cgl_slab_transpose(void* stream, void* comm, int world, int dir, int64_t planes, int64_t cols, const double* in,
+                       double* out, double* work) {
+  if (world < 1 || (dir != 0 && dir != 1)) return set_error(CGL_EINVAL, "slab_transpose: world >= 1, dir 0/1");
+  if (!comm) return set_error(CGL_EINVAL, "slab_transpose: null communicator");
+  if (!in || !out || !work || in == out || in == work || out == work)
+    return set_error(CGL_EINVAL, "slab_transpose: in/out/work must be distinct buffers");
+  const size_t count = (size_t)planes * (size_t)cols * 2;  // doubles per block
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dir == 0) {
+    int r = slab_rows(st, in, work, world, planes, cols, 0);
+    return r ? r : nccl_all_to_all(st, comm, world, work, out, count);
+  }
+  int r = nccl_all_to_all(st, comm, world, in, work, count);
+  return r ? r : slab_rows(st, work, out, world, planes, cols, 1);
+}
+
 int cgl_fft_pass_supported(int ndim, const int64_t* shape) {
   return shape && fft_pass_supported(ndim, shape) ? 1 : 0;
 }

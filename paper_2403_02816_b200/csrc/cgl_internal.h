@@ -56,6 +56,10 @@ bool fft_pass_supported(int ndim, const int64_t* shape);
 int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, int axis, int inverse,
                     const double* src, double* dst, const cgl_fft_ops_t* ops);
 
+// slab transposes (slab.cu)
+int slab_rows(cudaStream_t st, const double* src, double* dst, int64_t P, int64_t p0, int64_t m, int unpack);
+int nccl_all_to_all(cudaStream_t st, void* comm, int world, const double* send, double* recv, size_t count);
+
 // error plumbing (capi.cu)
 // Launch with the programmatic-dependent-launch attribute (CGL_PDL=0
 // disables) and an optional thread-block cluster shape.  Every kernel

@@ -58,45 +58,74 @@ class SlabLayout:
 
 
 class Transposer:
-    """Owns the send/receive buffers of the axis-0 transposes."""
+    """Send/receive buffers and the pack -> all-to-all -> unpack sequence of
+    the axis-0 transposes.  CUDA tensors use the library's row-permutation
+    kernels (cgl_slab_pack / cgl_slab_unpack, csrc/slab.cu) and NCCL through
+    torch.distributed; `cgl_slab_transpose` is the same sequence behind the C
+    ABI for a caller that owns an ncclComm_t.  CPU tensors (the gloo
+    world-size-2 tests of this layout code) move with torch copies."""
 
-    def __init__(self, layout, group=None, device=None, dtype=torch.complex128):
+    def __init__(self, layout, group=None, device=None, dtype=torch.complex128, nbuf=1):
         self.L = layout
         self.group = group
         P, p0, m = layout.world, layout.p0, layout.m
-        self.send = torch.empty((P, p0, m), dtype=dtype, device=device)
-        self.recv = torch.empty((P, p0, m), dtype=dtype, device=device)
-        self.cols_out = torch.empty((layout.n0, m), dtype=dtype, device=device)
+        self.send = [torch.empty((P, p0, m), dtype=dtype, device=device) for _ in range(nbuf)]
+        self.recv = [torch.empty((P, p0, m), dtype=dtype, device=device) for _ in range(nbuf)]
+        self.cols_out = [torch.empty((layout.n0, m), dtype=dtype, device=device) for _ in range(nbuf)]
 
-    def _a2a(self, out, inp):
+    def _a2a(self, out, inp, async_op=False):
         if self.L.world == 1:
             out.copy_(inp)
+            return None
+        return dist.all_to_all_single(out.view(-1), inp.reshape(-1), group=self.group, async_op=async_op)
+
+    def _pack(self, local, send):
+        P, p0, m = self.L.world, self.L.p0, self.L.m
+        if local.is_cuda:
+            _lib.check(_lib.load().cgl_slab_pack(_lib.stream(), P, p0, m, _lib.ptr(local), _lib.ptr(send)),
+                       "cgl_slab_pack")
         else:
-            dist.all_to_all_single(out.view(-1), inp.reshape(-1), group=self.group)
+            send.copy_(local.reshape(p0, P, m).transpose(0, 1))
 
-    def to_columns(self, local):
-        """(p0, ...) slab -> (n0, m) column block of this rank."""
+    def _unpack(self, recv, local_out):
         P, p0, m = self.L.world, self.L.p0, self.L.m
-        self.send.copy_(local.reshape(p0, P, m).transpose(0, 1))
-        self._a2a(self.recv, self.send)
-        return self.recv.view(self.L.n0, m)
+        if recv.is_cuda:
+            _lib.check(_lib.load().cgl_slab_unpack(_lib.stream(), P, p0, m, _lib.ptr(recv), _lib.ptr(local_out)),
+                       "cgl_slab_unpack")
+        else:
+            local_out.reshape(p0, P, m).copy_(recv.transpose(0, 1))
 
-    def from_columns(self, cols, local_out):
+    def to_columns(self, local, k=0, async_op=False):
+        """(p0, ...) slab -> (n0, m) column block of this rank (buffer set k);
+        with async_op the all-to-all's work handle is returned alongside."""
+        self._pack(local, self.send[k])
+        w = self._a2a(self.recv[k], self.send[k], async_op)
+        cols = self.recv[k].view(self.L.n0, self.L.m)
+        return (cols, w) if async_op else cols
+
+    def from_columns(self, cols, local_out, k=0):
         """(n0, m) column block -> (p0, ...) slab (written into local_out)."""
-        P, p0, m = self.L.world, self.L.p0, self.L.m
-        self._a2a(self.recv, cols)
-        local_out.reshape(p0, P, m).copy_(self.recv.transpose(0, 1))
+        self._a2a(self.recv[k], cols)
+        self._unpack(self.recv[k], local_out)
+        return local_out
+
+    def from_columns_start(self, cols, k=0):
+        return self._a2a(self.send[k], cols, async_op=True)
+
+    def from_columns_finish(self, local_out, k=0):
+        self._unpack(self.send[k], local_out)
         return local_out
 
 
 def mode0_sharded(local_in, mat, mat_t, local_out, tr, gemm=None, flag=None, pos=0):
-    """Axis-0 mu-mode product of a slab-sharded field."""
+    """Axis-0 mu-mode product of a slab-sharded field (DMMA / host callback;
+    the step plans use ShardedPlan's INT8-emulated products)."""
     cols = tr.to_columns(local_in)
     if gemm is None:
-        mode_product_dev(cols, mat, mat_t, 0, out=tr.cols_out, flag=flag, pos=pos)
+        mode_product_dev(cols, mat, mat_t, 0, out=tr.cols_out[0], flag=flag, pos=pos)
     else:
-        tr.cols_out.copy_(gemm(mat, cols))
-    return tr.from_columns(tr.cols_out, local_out)
+        tr.cols_out[0].copy_(gemm(mat, cols))
+    return tr.from_columns(tr.cols_out[0], local_out)
 
 
 def tucker_sharded(local_in, mats, mats_t, out, work, tr, gemm=None, local=None, flag=None, pos=0):
@@ -117,6 +146,36 @@ def tucker_sharded(local_in, mats, mats_t, out, work, tr, gemm=None, local=None,
     return out
 
 
+def tucker_sharded_oz(items, tr, ws, flag=None, pos=0):
+    """Tucker chains of several fields of a slab-sharded grid on the INT8
+    tensor cores (ozaki.py), the transposes overlapped with the products:
+    every field's slab -> column all-to-all is started first; field j's
+    axis-0 product runs while field j+1's columns are still in flight, and its
+    return all-to-all while field j+1's product runs; the local axes of field
+    j follow once its slab is back.  items: [(in, factors, out, work)]
+    (factors = sliced E_0 (global n0 x n0), E_1, ...); buffer set j of `tr`
+    belongs to item j."""
+    from .ozaki import mode_product_oz
+    started = [tr.to_columns(x, k=j, async_op=True) for j, (x, _, _, _) in enumerate(items)]
+    back = []
+    for j, ((x, facs, out, work), (cols, w)) in enumerate(zip(items, started)):
+        if w is not None:
+            w.wait()
+        mode_product_oz([cols], [facs[0]], [tr.cols_out[j]], 0, ws, flag=flag, pos=pos)
+        back.append(tr.from_columns_start(tr.cols_out[j], k=j))
+    for j, ((x, facs, out, work), w) in enumerate(zip(items, back)):
+        if w is not None:
+            w.wait()
+        d = x.ndim
+        tr.from_columns_finish(out if d % 2 == 1 else work, k=j)
+        cur = out if d % 2 == 1 else work
+        for axis in range(1, d):
+            dst = out if (d - axis) % 2 == 1 else work
+            mode_product_oz([cur], [facs[axis]], [dst], axis, ws, flag=flag, pos=pos)
+            cur = dst
+    return [it[2] for it in items]
+
+
 def global_min_key(flag, group=None):
     """Min-reduce the sticky divergence key over ranks (unsigned order)."""
     k = flag[0:1]
@@ -127,22 +186,37 @@ def global_min_key(flag, group=None):
 
 
 class ShardedPlan(FusedPlan):
-    """FusedPlan on the local slab: Tuckers through the axis-0 transposes, a
-    cross-rank key reduction before every end-of-step kernel, eager launches
-    (NCCL collectives are not captured)."""
+    """FusedPlan on the local slab: Tuckers through the axis-0 transposes on
+    the INT8 tensor cores (tucker_sharded_oz: all-to-alls overlapped with the
+    products), a cross-rank key reduction before every end-of-step kernel,
+    eager launches (NCCL collectives are not graph-captured).  Grids below the
+    emulated engine's size threshold use the DMMA products."""
 
     CHUNK = 1 << 30  # never graph-capture
-    FUSE_STAGE_SLICE = False  # products run through the transposes on DMMA
+    FUSE_STAGE_SLICE = False  # stage outputs stay FP64: the slabs travel before they are sliced
 
     def __init__(self, problem, scheme_name, like, layout, group=None):
         super().__init__(problem, scheme_name, like)
+        from . import ozaki
         self.layout = layout
         self.group = group
-        self.tr = Transposer(layout, group, device=like[0].device)
+        self.use_oz = ozaki.enabled() and ozaki.fits(layout.shape, 1)
+        # buffer sets: one per field of the widest Tucker job list (if4: 2, split4: 2)
+        self.tr = Transposer(layout, group, device=like[0].device, nbuf=2 * self.nf)
         if not self.W:
-            self.W = [torch.empty_like(like[0]) for _ in range(self.nf)]
+            self.W = [torch.empty_like(like[0]) for _ in range(2 * self.nf)]
+        while len(self.W) < 2 * self.nf:
+            self.W.append(torch.empty_like(like[0]))
 
-    def _tucker(self, jobs, flag):
+    def _tucker(self, jobs, flag, pre0=None, pro0=None):
+        if self.use_oz:
+            items = []
+            for f, fin, fout in jobs:
+                for c in range(self.nf):
+                    items.append((fin[c], self.blocks[c].sliced_factors(f), fout[c], self.W[len(items)]))
+            for i in range(0, len(items), len(self.tr.send)):
+                tucker_sharded_oz(items[i:i + len(self.tr.send)], self.tr, self.oz_ws, flag=flag, pos=self._pos)
+            return
         for f, fin, fout in jobs:
             for c in range(self.nf):
                 m, mt = self.blocks[c].exp_factors(f)
@@ -169,6 +243,8 @@ class ShardedPlan(FusedPlan):
                 global_min_key(flag, self.group)
                 key = int(flag[0].item()) & ((1 << 64) - 1)
                 if key != _lib.NO_DIVERGENCE and (key >> 24) <= steps:
+                    if (key >> 24) > k and k in stop_at and on_stop is not None:
+                        on_stop(k, self.result(k))
                     return key
                 if k in stop_at and on_stop is not None:
                     on_stop(k, self.result(k))
@@ -214,5 +290,30 @@ def tucker_slabs(slabs, mats, mats_t, ex, flag=None, pos=0):
     for t in tmp:
         for axis in range(1, t.ndim):
             t = mode_product_dev(t, mats[axis], mats_t[axis], axis, flag=flag, pos=pos)
+        out.append(t)
+    return out
+
+
+def tucker_slabs_oz(slabs, factors, ex, ws, flag=None, pos=0):
+    """tucker_slabs on the INT8 tensor cores (ozaki.py): the axis-0 product
+    of each column block is the unsharded first-axis product restricted to
+    those columns -- the data slices carry one exponent per column and the
+    K = n0 sum runs in the same order -- so the result is bit-identical to the
+    unsharded chain for any rank count."""
+    from .ozaki import mode_product_oz
+    n0 = ex.shape[0]
+    cols = [torch.empty((n0, ex.m), dtype=torch.complex128, device=s.device) for s in slabs]
+    ex.to_cols(slabs, cols)
+    outc = [torch.empty_like(c) for c in cols]
+    for c, o in zip(cols, outc):
+        mode_product_oz([c], [factors[0]], [o], 0, ws, flag=flag, pos=pos)
+    tmp = [torch.empty_like(s) for s in slabs]
+    ex.to_slabs(outc, tmp)
+    out = []
+    for t in tmp:
+        for axis in range(1, t.ndim):
+            o = torch.empty_like(t)
+            mode_product_oz([t], [factors[axis]], [o], axis, ws, flag=flag, pos=pos)
+            t = o
         out.append(t)
     return out

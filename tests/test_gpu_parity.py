@@ -666,6 +666,43 @@ def test_slab_sharded_fourier_virtual_ranks(P, config_golden, nranks, scheme, ta
     assert rel_l2(got, arrays[f"{tag}_out"]) <= 1e-10
 
 
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_fd_slab_tucker_oz_virtual_ranks_bit_identical(P, nranks):
+    """Slab-sharded Tucker chain on the INT8 tensor cores (column-block
+    axis-0 products) with P virtual ranks is BIT-IDENTICAL to the unsharded
+    chain of the step plans (tucker_oz), on C2 physics at 64^3."""
+    from paper_2403_02816_b200 import ozaki, workloads as W
+    from paper_2403_02816_b200.distributed import tucker_slabs_oz
+    from paper_2403_02816_b200.slabfourier import SlabExchange, split_global
+    w = W.CONFIGS["C2"].scaled(64)
+    op = W.build_problem(w).operator
+    op.prepare(w.tau, (1,))
+    facs = op.sliced_factors(1)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    u = torch.randn(w.extents, dtype=torch.complex128, device="cuda", generator=g)
+    want, work = torch.empty_like(u), torch.empty_like(u)
+    ozaki.tucker_oz([u], [facs], [want], [work], ozaki.Workspace())
+    ex = SlabExchange(w.extents, nranks, list(range(nranks)))
+    got = torch.cat(tucker_slabs_oz(split_global(u, nranks, "slabs"), facs, ex, ozaki.Workspace()), dim=0)
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("scheme", ["if4", "split4"])
+def test_sharded_plan_world1_matches_unsharded(P, scheme):
+    """integrate_sharded at one rank (transposes = pack/copy/unpack kernels,
+    axis-0 products on the column block, INT8 tensor cores) reproduces the
+    single-GPU fused plan on C2 physics at 64^3."""
+    from paper_2403_02816_b200 import distributed as D, workloads as W
+    w = W.CONFIGS["C2"].scaled(64, 10)
+    prob = W.build_problem(w)
+    x0 = W.initial_state_device(w)
+    ref = P.integrate(prob, scheme, (x0,), w.t_final, w.steps).fields[0]
+    out, k_div, reason, _ = D.integrate_sharded(W.build_problem(w), scheme, [x0.clone()], w.t_final, w.steps,
+                                                D.SlabLayout(w.extents, 1))
+    assert k_div == 0 and reason == ""
+    assert (torch.linalg.vector_norm(out[0] - ref) / torch.linalg.vector_norm(ref)).item() <= 1e-13
+
+
 @pytest.mark.parametrize("nranks", [2, 4])
 def test_fd_slab_tucker_virtual_ranks(P, nranks):
     """Axis-0 slab-sharded Tucker chain (all-to-all transposes + DMMA GEMMs on
@@ -684,6 +721,24 @@ def test_fd_slab_tucker_virtual_ranks(P, nranks):
     ex = SlabExchange(w.extents, nranks, list(range(nranks)))
     got = torch.cat(tucker_slabs(split_global(u, nranks, "slabs"), mats, mts, ex), dim=0)
     assert (torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)).item() <= 1e-14
+
+
+def test_slab_pack_unpack_kernels(P):
+    """cgl_slab_pack / cgl_slab_unpack against torch permutes, and the C-ABI
+    transpose's argument validation (no NCCL communicator needed)."""
+    from paper_2403_02816_b200 import _lib
+    lib = _lib.load()
+    for world, p0, m in [(1, 4, 16), (2, 3, 40), (8, 16, 1000)]:
+        slab = torch.randn((p0, world * m), dtype=torch.complex128, device="cuda")
+        blocks = torch.empty((world, p0, m), dtype=torch.complex128, device="cuda")
+        _lib.check(lib.cgl_slab_pack(_lib.stream(), world, p0, m, _lib.ptr(slab), _lib.ptr(blocks)), "pack")
+        assert torch.equal(blocks, slab.reshape(p0, world, m).transpose(0, 1))
+        back = torch.empty_like(slab)
+        _lib.check(lib.cgl_slab_unpack(_lib.stream(), world, p0, m, _lib.ptr(blocks), _lib.ptr(back)), "unpack")
+        assert torch.equal(back, slab)
+    x = torch.zeros(8, dtype=torch.complex128, device="cuda")
+    assert lib.cgl_slab_transpose(_lib.stream(), None, 1, 0, 2, 4, _lib.ptr(x), _lib.ptr(x), _lib.ptr(x)) != 0
+    assert lib.cgl_slab_pack(_lib.stream(), 2, 2, 2, _lib.ptr(x), _lib.ptr(x)) != 0   # in place
 
 
 def test_snapshot_from_device_streamed(P, unit_golden, tmp_path):
