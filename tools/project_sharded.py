@@ -35,6 +35,24 @@ def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 4
     ranks = [int(a) for a in args if a.isdigit() and a != str(steps)] or [1, 2, 4, 8]
+    if len(ranks) > 1:
+        # one process per rank count: every case gets the whole HBM
+        import subprocess
+        recs = []
+        for P in ranks:
+            res = subprocess.run([sys.executable, __file__, str(P), "--steps", str(steps)], capture_output=True,
+                                 text=True)
+            print(res.stdout, end="", flush=True)
+            if res.returncode:
+                print(json.dumps(dict(P=P, error=res.stderr.strip().splitlines()[-1:])), flush=True)
+                continue
+            recs.append(json.loads(res.stdout.strip().splitlines()[-1]))
+        base = next((r["local_ms_per_step"] for r in recs if r["P"] == 1), None)
+        if base:
+            print(json.dumps({"summary": [dict(P=r["P"], speedup_serial=base / r["projected_ms_serial"],
+                                               speedup_overlapped=base / r["projected_ms_overlapped"],
+                                               projected_ms=r["projected_ms_serial"]) for r in recs]}))
+        return
     w = W.CONFIGS["C4"]
     n0, n1, n2 = w.extents
     out = []
@@ -77,13 +95,6 @@ def main():
         out.append(rec)
         del plan, prob, u0
         torch.cuda.empty_cache()
-    base = next((r["local_ms_per_step"] for r in out if r["P"] == 1), None)
-    if base:
-        for r in out:
-            r["speedup_serial"] = base / r["projected_ms_serial"]
-            r["speedup_overlapped"] = base / r["projected_ms_overlapped"]
-        print(json.dumps({"summary": [(r["P"], round(r["speedup_serial"], 2), round(r["speedup_overlapped"], 2))
-                                      for r in out]}))
 
 
 if __name__ == "__main__":
