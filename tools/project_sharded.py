@@ -50,8 +50,10 @@ def main():
         base = next((r["local_ms_per_step"] for r in recs if r["P"] == 1), None)
         if base:
             print(json.dumps({"summary": [dict(P=r["P"], speedup_serial=base / r["projected_ms_serial"],
+                                               speedup_pipelined=base / r["projected_ms_pipelined"],
                                                speedup_overlapped=base / r["projected_ms_overlapped"],
-                                               projected_ms=r["projected_ms_serial"]) for r in recs]}))
+                                               projected_ms_pipelined=r["projected_ms_pipelined"])
+                                          for r in recs]}))
         return
     w = W.CONFIGS["C4"]
     n0, n1, n2 = w.extents
@@ -65,6 +67,7 @@ def main():
             r = PK.integrate(prob, "if4", (u0,), w.tau * steps, steps)
             rec = dict(P=1, local_ms_per_step=r.device_seconds / steps * 1e3, comm_ms_per_step=0.0)
             rec["projected_ms_serial"] = rec["projected_ms_overlapped"] = rec["local_ms_per_step"]
+            rec["projected_ms_pipelined"] = rec["local_ms_per_step"]
             print(json.dumps(rec), flush=True)
             out.append(rec)
             del prob, u0, r
@@ -84,12 +87,17 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         local_ms = e0.elapsed_time(e1) / steps
-        # quad if4: 4 Tuckers x 2 fields per step, 2 transposes each
-        transposes = 4 * 2 * 2
+        # quad if4: 2 Tucker groups x 2 fields per step, 2 transposes per field chain
+        transposes = 2 * 2 * 2
         bytes_per = 16 * n0 * n1 * n2 * (P - 1) / P ** 2
-        comm_ms = transposes * bytes_per / (NVLINK_GBS * 1e9) * 1e3
+        t_one = bytes_per / (NVLINK_GBS * 1e9) * 1e3
+        comm_ms = transposes * t_one
+        # tucker_sharded_oz: per group only the first field's slab->column
+        # exchange has nothing to overlap with (the others run under products)
+        exposed_ms = 2 * t_one
         rec = dict(P=P, local_ms_per_step=local_ms, comm_ms_per_step=comm_ms,
-                   projected_ms_serial=local_ms + comm_ms, projected_ms_overlapped=max(local_ms, comm_ms),
+                   projected_ms_serial=local_ms + comm_ms, projected_ms_pipelined=local_ms + exposed_ms,
+                   projected_ms_overlapped=max(local_ms, comm_ms),
                    slab=list(L.local_shape()), bytes_per_transpose=bytes_per)
         print(json.dumps(rec), flush=True)
         out.append(rec)
