@@ -415,6 +415,19 @@ int cgl_slab_unpack(void* stream, int64_t world, int64_t planes, int64_t cols, c
 int cgl_slab_transpose(void* stream, void* comm, int world, int dir, int64_t planes, int64_t cols,
                        const double* in, double* out, double* work);
 
+/* ---- Cross-mode fused 2D Tucker (csrc/tucker2d.cu) ------------------------
+ * out_q = E0_q in_q E1_q^T for (n0 x n1) fields (n1 <= 1024), mode 0 then
+ * mode 1 (tensors.py:62-69) in ONE launch, the intermediate row in shared
+ * memory.  e1t = E1^T.  band0/band1: int pairs [lo, hi] per row of E0 / E1,
+ * the significant band (entries >= 2^-60 of the row max).
+ * program 0: plain (1..8 items); 1: strang end-of-step (one scalar field):
+ * out[0] = flow(E0 in E1^T, t/2) checked, out[1] = flow(out[0], t/2) of the
+ * next step (integrators.py:161-164), positions as CGL_STAGE_STRANG_END. */
+int cgl_tucker2d(void* stream, int program, int nitems, int64_t n0, int64_t n1, const double* const* in,
+                 double* const* out, const double* const* e0, const double* const* e1t,
+                 const int* const* band0, const int* const* band1, const cgl_nonlinear_t* nl, double tau,
+                 cgl_flag_t* flag, uint64_t pos);
+
 #ifdef __cplusplus
 }
 #endif

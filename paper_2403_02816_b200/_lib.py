@@ -142,6 +142,8 @@ _SIGS = {
     "cgl_fft_exec": (c_int, [c_ptr, c_ptr, c_ptr, c_ptr, c_int]),
     "cgl_fft_destroy": (c_int, [c_ptr]),
     "cgl_fft_pass_supported": (c_int, [c_int, c_ptr]),
+    "cgl_tucker2d": (c_int, [c_ptr, c_int, c_int, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                             c_dbl, c_ptr, c_u64]),
     "cgl_slab_pack": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
     "cgl_slab_unpack": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
     "cgl_slab_transpose": (c_int, [c_ptr, c_ptr, c_int, c_int, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),

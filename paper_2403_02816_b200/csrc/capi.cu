@@ -336,6 +336,14 @@ int cgl_stage_fourier_cols(void* stream, int program, int nfields, int ndim, con
                       ndim, shape, tables, cols, col_offset);
 }
 
+int cgl_tucker2d(void* stream, int program, int nitems, int64_t n0, int64_t n1, const double* const* in,
+                 double* const* out, const double* const* e0, const double* const* e1t, const int* const* band0,
+                 const int* const* band1, const cgl_nonlinear_t* nl, double tau, cgl_flag_t* flag, uint64_t pos) {
+  if (!in || !out || !e0 || !e1t || !band0 || !band1) return set_error(CGL_EINVAL, "tucker2d: null array");
+  return tucker2d_launch((cudaStream_t)stream, program, nitems, n0, n1, in, out, e0, e1t, band0, band1, nl, tau,
+                         flag, pos);
+}
+
 int cgl_slab_pack(void* stream, int64_t world, int64_t planes, int64_t cols, const double* slab, double* blocks) {
   return slab_rows((cudaStream_t)stream, slab, blocks, world, planes, cols, 0);
 }

@@ -60,6 +60,11 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
 int slab_rows(cudaStream_t st, const double* src, double* dst, int64_t P, int64_t p0, int64_t m, int unpack);
 int nccl_all_to_all(cudaStream_t st, void* comm, int world, const double* send, double* recv, size_t count);
 
+// cross-mode fused 2D Tucker (tucker2d.cu)
+int tucker2d_launch(cudaStream_t st, int program, int nitems, int64_t n0, int64_t n1, const double* const* in,
+                    double* const* out, const double* const* e0, const double* const* e1t, const int* const* band0,
+                    const int* const* band1, const cgl_nonlinear_t* nl, double tau, cgl_flag_t* flag, uint64_t pos);
+
 // error plumbing (capi.cu)
 // Launch with the programmatic-dependent-launch attribute (CGL_PDL=0
 // disables) and an optional thread-block cluster shape.  Every kernel

@@ -159,6 +159,7 @@ class KroneckerOperator:
         self._tau = tau
         self._cache = {}
         self.__dict__.pop("_oz", None)
+        self.__dict__.pop("_bands", None)
         _lib.require_cuda()
         for f in fr:
             step = float(f) * self._tau
@@ -192,6 +193,25 @@ class KroneckerOperator:
                 if id(m) not in seen:
                     seen[id(m)] = SlicedFactor(m)
                 out.append(seen[id(m)])
+            cache[f] = out
+        return cache[f]
+
+    def tucker2d_bands(self, fraction):
+        """Per-row significant bands [lo, hi] (int32 pairs, device) of each
+        exp(f tau A_mu): entries >= 2^-60 of their row's largest magnitude, the
+        support the cross-mode fused 2D Tucker (cgl_tucker2d) contracts."""
+        f = Fraction(fraction)
+        mats, _ = self.exp_factors(f)
+        cache = self.__dict__.setdefault("_bands", {})
+        if f not in cache:
+            out = []
+            for m in mats:
+                a = m.abs()
+                keep = a >= a.amax(dim=1, keepdim=True) * 2.0 ** -60
+                n = m.shape[1]
+                lo = keep.int().argmax(dim=1)
+                hi = n - 1 - keep.flip(1).int().argmax(dim=1)
+                out.append(torch.stack([lo, hi], dim=1).to(torch.int32).contiguous())
             cache[f] = out
         return cache[f]
 

@@ -150,6 +150,12 @@ class FusedPlan:
             raise ValueError(f"CGL_IF4_FORM must be quad, half or ref, not {f!r}")
         return f
 
+    def _ensure_oz(self):
+        from . import ozaki
+        if self.use_oz is None:
+            self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
+        return self.use_oz
+
     def _fuse_pro(self):
         from . import ozaki
         return ozaki.fuse_enabled() and type(self) is FusedPlan and self._fused_slices() is not None
@@ -187,6 +193,9 @@ class FusedPlan:
                                 pro0=pro0 if i == 0 else None)
             return
         assert pre0 is None and pro0 is None, "pre-sliced operands need the INT8-emulated products"
+        if self._tucker2d_ok():
+            self._tucker2d(jobs, flag)
+            return
         ins, outs, mats, mts = [], [], [], []
         for f, fin, fout in jobs:
             for c in range(self.nf):
@@ -197,6 +206,33 @@ class FusedPlan:
                 mts.append(mt)
         work = self.W[:len(ins)] if self.W else None
         tucker_dev(ins, mats, mts, outs=outs, flag=flag, pos=self._pos, work=work)
+
+    def _tucker2d_ok(self):
+        """Cross-mode fused 2D Tucker (cgl_tucker2d, one launch per Tucker
+        group) for the small 2D grids the DMMA products serve."""
+        if getattr(self, "_t2d", None) is None:
+            self._t2d = (len(self.shape) == 2 and self.shape[1] <= 1024 and self.shape[0] <= 65535
+                         and not self.use_oz and all(isinstance(b, KroneckerOperator) for b in self.blocks)
+                         and type(self) is FusedPlan and os.environ.get("CGL_TUCKER2D", "1") != "0")
+        return self._t2d
+
+    def _tucker2d(self, jobs, flag, program=0, tau=0.0, out2=None):
+        lib = _lib.load()
+        items = []
+        for f, fin, fout in jobs:
+            for c in range(self.nf):
+                (m0, m1), (_, m1t) = self.blocks[c].exp_factors(f)
+                b0, b1 = self.blocks[c].tucker2d_bands(f)
+                items.append((fin[c], fout[c], m0, m1t, b0, b1))
+        for i in range(0, len(items), 8):
+            it = items[i:i + 8]
+            outs = [x[1] for x in it] + ([out2] if out2 is not None else [])
+            _lib.check(lib.cgl_tucker2d(_lib.stream(), program, len(it), self.shape[0], self.shape[1],
+                                        _lib.ptr_array([x[0] for x in it]), _lib.ptr_array(outs),
+                                        _lib.ptr_array([x[2] for x in it]), _lib.ptr_array([x[3] for x in it]),
+                                        _lib.ptr_array([x[4] for x in it]), _lib.ptr_array([x[5] for x in it]),
+                                        _lib.ctypes.byref(self.nl), tau, _lib.flag_ptr(flag), self._pos),
+                       "cgl_tucker2d")
 
     def _stage(self, name, ins, outs, flag, tau):
         lib = _lib.load()
@@ -339,6 +375,12 @@ class FusedPlan:
                 self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
             self._before_end(flag)
             self._end_stage("split4_end", [v, v2], self.state_after(k)[0], [F[0], F[1]], flag, tau)
+        elif self.scheme == "strang" and self.nf == 1 and self.nl.kind != 2 and self._ensure_oz() is False \
+                and self._tucker2d_ok():
+            # one launch per step: Tucker + flow, check, next step's flow (cgl_tucker2d);
+            # v ping-pongs between B[0] and B[1] (every output row reads a band of input rows)
+            v_in, v_out = B[(k - 1) % 2], B[k % 2]
+            self._tucker2d([(O, v_in, [self.state_after(k)[0]])], flag, program=1, tau=tau, out2=v_out[0])
         elif self.scheme == "strang":
             v, w = B
             self._tucker([(O, v, w)], flag)
