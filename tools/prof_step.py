@@ -15,6 +15,7 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 w = W.CONFIGS[key]
 prob = W.build_problem(w)
 x0 = torch.from_numpy(W.state_for_problem(w, W.initial_state(w))).cuda()
+P.integrate(prob, scheme, (x0,), w.tau * steps, steps)  # warm: plans, graphs, workspaces
 r = P.integrate(prob, scheme, (x0,), w.tau * steps, steps)
 torch.cuda.synchronize()
 print("ok", r.diverged, r.device_seconds / steps * 1e3, "ms/step")
