@@ -7,6 +7,17 @@ axis), with its block-sparsity map (the factors are numerically banded, so
 whole slice blocks are exactly zero and skipped).  The data operand is
 sliced per product into a reusable workspace.  Accuracy: ~1e-15 relative
 per product (tools/oz_check.py; parity tests at 1e-10 after full runs).
+
+Error model.  A product element is exact up to the truncation of its
+operands at 2^-56 of their scale: the ROW maximum of E (A side) and the
+COLUMN (fibre) maximum of the data (B side) -- not per element as in an FP64
+GEMM.  The global relative error is unaffected (full runs against the
+reference: C4 50 steps 1.3e-13 at 256^3, tests/test_full_runs.py), but an
+element far below its fibre's maximum keeps fewer significant bits: on C4 at
+64^3, over the points below 1e-6 of the peak, the error after 50 steps is
+1.5e-8 of that band's scale (1.5e-14 of the peak) against 4e-14 for the DMMA
+engine (profiles/r02_parity_full_runs.jsonl).  CGL_GEMM=dmma selects the
+per-element engine where that matters.
 """
 
 import math
