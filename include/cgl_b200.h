@@ -21,6 +21,7 @@
 #ifndef CGL_B200_H
 #define CGL_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -397,6 +398,20 @@ typedef struct {
 int cgl_fft_pass_supported(int ndim, const int64_t* shape);
 int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse,
                  const double* src, double* dst, const cgl_fft_ops_t* ops);
+
+/* Plane-chunked passes (csrc/fftplane.cu): for a 3D field with shape[1] ==
+ * shape[2] in 64..512, ONE persistent launch runs, for every axis-0 plane,
+ *   F_1 (axis 1, forward)  ->  `program` (IF4_B1..B4 or STR_MID, whole rows)  ->  F_1^-1
+ * in place in `field`, plane by plane, so that the two intermediate states of a
+ * plane stay in L2 (spectral.py:79-86 around integrators.py:161-164, 205-215;
+ * same arithmetic, bit-identical to the three cgl_fft_pass calls it replaces).
+ * `workspace`: cgl_fft_plane_workspace_bytes() bytes of device memory, 16-byte
+ * aligned, zeroed once by the caller; every launch leaves it zeroed.  One
+ * workspace serves one stream. */
+size_t cgl_fft_plane_workspace_bytes(void);
+int cgl_fft_plane_supported(int ndim, const int64_t* shape);
+int cgl_fft_plane(void* stream, int program, int ndim, const int64_t* shape, double* field,
+                  const cgl_fft_ops_t* ops, void* workspace);
 
 /* ---- Slab-sharded axis-0 transposes (csrc/slab.cu) ------------------------
  * A rank's slab of a global (world*planes, world*cols) field (axis 0 split,

@@ -372,6 +372,16 @@ int cgl_fft_pass_supported(int ndim, const int64_t* shape) {
   return shape && fft_pass_supported(ndim, shape) ? 1 : 0;
 }
 
+size_t cgl_fft_plane_workspace_bytes(void) { return fft_plane_workspace_bytes(); }
+int cgl_fft_plane_supported(int ndim, const int64_t* shape) {
+  return shape && fft_plane_supported(ndim, shape) ? 1 : 0;
+}
+int cgl_fft_plane(void* stream, int program, int ndim, const int64_t* shape, double* field, const cgl_fft_ops_t* ops,
+                  void* workspace) {
+  if (!shape) return set_error(CGL_EINVAL, "fft_plane: null shape");
+  return fft_plane_launch((cudaStream_t)stream, program, ndim, shape, field, ops, workspace);
+}
+
 int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse, const double* src,
                  double* dst, const cgl_fft_ops_t* ops) {
   if (!shape) return set_error(CGL_EINVAL, "fft_pass: null shape");

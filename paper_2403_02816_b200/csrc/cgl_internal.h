@@ -56,6 +56,12 @@ bool fft_pass_supported(int ndim, const int64_t* shape);
 int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, int axis, int inverse,
                     const double* src, double* dst, const cgl_fft_ops_t* ops);
 
+// plane-chunked passes (fftplane.cu)
+size_t fft_plane_workspace_bytes();
+bool fft_plane_supported(int ndim, const int64_t* shape);
+int fft_plane_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, double* field,
+                     const cgl_fft_ops_t* ops, void* workspace);
+
 // slab transposes (slab.cu)
 int slab_rows(cudaStream_t st, const double* src, double* dst, int64_t P, int64_t p0, int64_t m, int unpack);
 int nccl_all_to_all(cudaStream_t st, void* comm, int world, const double* send, double* recv, size_t count);

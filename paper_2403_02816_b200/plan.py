@@ -663,6 +663,12 @@ class PencilFourierPlan(FourierPlan):
                 STR_A0: w = F0^-1 T / N; u_k = flow(w, t/2) (checked, stored);
                 T = F0 flow(u_k, t/2) of step k + 1
       4 passes per 3D step: 144 B/pt.
+    3D grids with n1 == n2 >= 64 (CGL_FFT_PLANE=0 disables): the axis-1 passes
+    either side of a contiguous-axis program run with it in ONE persistent
+    plane-chunked launch (csrc/fftplane.cu: F1, program, F1^-1 per axis-0 plane,
+    the intermediates L2-resident).  if4 becomes 4 x (G0, plane B_i) = 8 launches
+    and 432 B/pt per step, strang (plane STR_MID, STR_A0) = 2 launches, 80 B/pt;
+    same arithmetic, bit-identical results.
     Divergence keys and positions are those of the stage kernels (same
     programs, same flag record), so diverged_at / reason are unchanged.
     """
@@ -692,6 +698,9 @@ class PencilFourierPlan(FourierPlan):
         self.graph_launches = {}
         self.replayed_launches = 0
         self.W = []
+        from . import fftpass as _fp
+        self.plane = (os.environ.get("CGL_FFT_PLANE", "1") != "0" and _fp.plane_supported(self.shape))
+        self._plane_ws = _fp.plane_workspace() if self.plane else None
 
     @staticmethod
     def applies(problem, scheme_name, like):
@@ -706,6 +715,10 @@ class PencilFourierPlan(FourierPlan):
     def _pass(self, prog, axis, src, dst, tau, inverse=False, **kw):
         from .fftpass import axis_pass
         axis_pass(src, dst, axis, inverse=inverse, program=prog, ops=self._ops(tau, **kw), shape=self.shape)
+
+    def _plane(self, prog, field, tau, **kw):
+        from .fftpass import plane_pass
+        plane_pass(field, prog, self._ops(tau, **kw), self._plane_ws, shape=self.shape)
 
     def load_state(self, u0, tau):
         from .fftpass import fftn
@@ -722,6 +735,8 @@ class PencilFourierPlan(FourierPlan):
         last = len(self.shape) - 1
         if self.scheme == "if4":
             self._pass("if4_start", last, None, self.T, tau, u=self.U[0][0])
+            if self.plane:   # every eval then starts at G0: T = F1^-1 F2^-1 (stage input)
+                self._pass("plain", 1, self.T, self.T, tau, inverse=True)
         else:
             self._pass("str_start", 0, None, self.T, tau, u=self.U[0][0], scale=1.0 / self.n)
 
@@ -735,6 +750,13 @@ class PencilFourierPlan(FourierPlan):
             u = self.U[0][0]
             g1, g2, g3 = self.G
             for prog, gout in (("if4_b1", g1), ("if4_b2", g2), ("if4_b3", g3), ("if4_b4", None)):
+                if self.plane:
+                    self._pass("g", 0, T, T, tau, scale=inv_n)
+                    if gout is not None:
+                        self._plane(prog, T, tau, u=u, g_out=gout)
+                    else:
+                        self._plane(prog, T, tau, u=u, u_out=u, g=(g1, g2, g3))
+                    continue
                 if d == 3:
                     self._pass("plain", 1, T, T, tau, inverse=True)
                 self._pass("g", 0, T, T, tau, scale=inv_n)
@@ -746,11 +768,14 @@ class PencilFourierPlan(FourierPlan):
                     self._pass(prog, last, T, T, tau, u=u, u_out=u, g=(g1, g2, g3))
         else:
             out = self.U[k % 2][0]
-            if d == 3:
-                self._pass("plain", 1, T, T, tau)
-            self._pass("str_mid", last, T, T, tau)
-            if d == 3:
-                self._pass("plain", 1, T, T, tau, inverse=True)
+            if self.plane:
+                self._plane("str_mid", T, tau)
+            else:
+                if d == 3:
+                    self._pass("plain", 1, T, T, tau)
+                self._pass("str_mid", last, T, T, tau)
+                if d == 3:
+                    self._pass("plain", 1, T, T, tau, inverse=True)
             self._before_end(flag)
             self._pass("str_a0", 0, T, T, tau, u_out=out, scale=inv_n)
 
