@@ -21,7 +21,6 @@
 #ifndef CGL_B200_H
 #define CGL_B200_H
 
-#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -399,19 +398,20 @@ int cgl_fft_pass_supported(int ndim, const int64_t* shape);
 int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse,
                  const double* src, double* dst, const cgl_fft_ops_t* ops);
 
-/* Plane-chunked passes (csrc/fftplane.cu): for a 3D field with shape[1] ==
- * shape[2] in 64..512, ONE persistent launch runs, for every axis-0 plane,
- *   F_1 (axis 1, forward)  ->  `program` (IF4_B1..B4 or STR_MID, whole rows)  ->  F_1^-1
- * in place in `field`, plane by plane, so that the two intermediate states of a
- * plane stay in L2 (spectral.py:79-86 around integrators.py:161-164, 205-215;
- * same arithmetic, bit-identical to the three cgl_fft_pass calls it replaces).
- * `workspace`: cgl_fft_plane_workspace_bytes() bytes of device memory, 16-byte
- * aligned, zeroed once by the caller; every launch leaves it zeroed.  One
- * workspace serves one stream. */
-size_t cgl_fft_plane_workspace_bytes(void);
-int cgl_fft_plane_supported(int ndim, const int64_t* shape);
-int cgl_fft_plane(void* stream, int program, int ndim, const int64_t* shape, double* field,
-                  const cgl_fft_ops_t* ops, void* workspace);
+/* ---- Explicit Runge-Kutta stage on banded Kronecker-sum operators (csrc/rkstage.cu) ----
+ * One stage of rk2 / rk4 (integrators.py:146-158 over Problem.rhs, tensors.py:72-84):
+ *   f = sum_mu A_mu x_mu x + g(x);   x_out = u + cx f;   acc_out = (acc_in ? acc_in : u) + ca f
+ * for per-direction factors A_mu of half-bandwidth halfband[mu] <= 8 (the FD
+ * operators: 1 or 2), as ONE pass: the dense products of the reference reduce
+ * exactly to (2 b + 1)-point contractions.  bands[c * ndim + mu]: complex
+ * (shape[mu] x (2 b + 1)) array, band[i][d] = A[i][i + d - b] (zero outside);
+ * x, u, acc_in, x_out, acc_out: arrays of nf (1 or 2) field pointers; acc_in,
+ * x_out, acc_out may be NULL (not both outputs); x must not alias an output.
+ * check != 0: acc_out is the step's new state, checked finite at (step, 255). */
+int cgl_rk_stage(void* stream, int ndim, const int64_t* shape, int nf, const int* halfband,
+                 const double* const* bands, const cgl_nonlinear_t* nl, const double* const* x,
+                 const double* const* u, const double* const* acc_in, double* const* x_out,
+                 double* const* acc_out, double cx, double ca, int check, cgl_flag_t* flag, uint64_t pos);
 
 /* ---- Slab-sharded axis-0 transposes (csrc/slab.cu) ------------------------
  * A rank's slab of a global (world*planes, world*cols) field (axis 0 split,

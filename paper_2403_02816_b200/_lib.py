@@ -148,9 +148,8 @@ _SIGS = {
     "cgl_slab_unpack": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr]),
     "cgl_slab_transpose": (c_int, [c_ptr, c_ptr, c_int, c_int, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
     "cgl_fft_pass": (c_int, [c_ptr, c_int, c_int, c_ptr, c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(FftOps)]),
-    "cgl_fft_plane_workspace_bytes": (ctypes.c_size_t, []),
-    "cgl_fft_plane_supported": (c_int, [c_int, c_ptr]),
-    "cgl_fft_plane": (c_int, [c_ptr, c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(FftOps), c_ptr]),
+    "cgl_rk_stage": (c_int, [c_ptr, c_int, c_ptr, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                             c_dbl, c_dbl, c_int, c_ptr, c_u64]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -372,14 +372,12 @@ int cgl_fft_pass_supported(int ndim, const int64_t* shape) {
   return shape && fft_pass_supported(ndim, shape) ? 1 : 0;
 }
 
-size_t cgl_fft_plane_workspace_bytes(void) { return fft_plane_workspace_bytes(); }
-int cgl_fft_plane_supported(int ndim, const int64_t* shape) {
-  return shape && fft_plane_supported(ndim, shape) ? 1 : 0;
-}
-int cgl_fft_plane(void* stream, int program, int ndim, const int64_t* shape, double* field, const cgl_fft_ops_t* ops,
-                  void* workspace) {
-  if (!shape) return set_error(CGL_EINVAL, "fft_plane: null shape");
-  return fft_plane_launch((cudaStream_t)stream, program, ndim, shape, field, ops, workspace);
+int cgl_rk_stage(void* stream, int ndim, const int64_t* shape, int nf, const int* halfband,
+                 const double* const* bands, const cgl_nonlinear_t* nl, const double* const* x,
+                 const double* const* u, const double* const* acc_in, double* const* x_out,
+                 double* const* acc_out, double cx, double ca, int check, cgl_flag_t* flag, uint64_t pos) {
+  return rk_stage_launch((cudaStream_t)stream, ndim, shape, nf, halfband, bands, nl, x, u, acc_in, x_out, acc_out, cx,
+                         ca, check, flag, pos);
 }
 
 int cgl_fft_pass(void* stream, int program, int ndim, const int64_t* shape, int axis, int inverse, const double* src,

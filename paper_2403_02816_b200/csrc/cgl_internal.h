@@ -56,11 +56,11 @@ bool fft_pass_supported(int ndim, const int64_t* shape);
 int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, int axis, int inverse,
                     const double* src, double* dst, const cgl_fft_ops_t* ops);
 
-// plane-chunked passes (fftplane.cu)
-size_t fft_plane_workspace_bytes();
-bool fft_plane_supported(int ndim, const int64_t* shape);
-int fft_plane_launch(cudaStream_t st, int program, int ndim, const int64_t* shape, double* field,
-                     const cgl_fft_ops_t* ops, void* workspace);
+// banded Kronecker-sum RK stage (rkstage.cu)
+int rk_stage_launch(cudaStream_t st, int ndim, const int64_t* shape, int nf, const int* halfband,
+                    const double* const* bands, const cgl_nonlinear_t* nl, const double* const* x,
+                    const double* const* u, const double* const* acc_in, double* const* x_out,
+                    double* const* acc_out, double cx, double ca, int check, cgl_flag_t* flag, uint64_t pos);
 
 // slab transposes (slab.cu)
 int slab_rows(cudaStream_t st, const double* src, double* dst, int64_t P, int64_t p0, int64_t m, int unpack);

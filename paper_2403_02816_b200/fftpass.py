@@ -54,28 +54,6 @@ def axis_pass(src, dst, axis, inverse=False, program="plain", ops=None, shape=No
     return dst
 
 
-def plane_supported(shape):
-    shape = tuple(int(n) for n in shape)
-    return bool(_lib.load().cgl_fft_plane_supported(len(shape), _lib.i64_array(shape)))
-
-
-def plane_workspace():
-    """Zeroed control block of the plane-chunked passes (one per plan / stream;
-    every launch leaves it zeroed)."""
-    nbytes = int(_lib.load().cgl_fft_plane_workspace_bytes())
-    return torch.zeros((nbytes + 7) // 8, dtype=torch.int64, device="cuda")
-
-
-def plane_pass(field, program, ops, workspace, shape=None):
-    """F_1, the contiguous-axis `program`, F_1^-1 on every axis-0 plane of a 3D
-    field, in place, in one persistent launch (csrc/fftplane.cu)."""
-    shape = tuple(field.shape) if shape is None else tuple(shape)
-    _lib.check(_lib.load().cgl_fft_plane(_lib.stream(), PROGRAMS[program], len(shape), _lib.i64_array(shape),
-                                         _lib.ptr(field), _lib.ctypes.byref(ops), _lib.ptr(workspace)),
-               "cgl_fft_plane")
-    return field
-
-
 def fftn(x, out=None, inverse=False):
     """Unnormalised n-dimensional transform (forward = np.fft.fftn; inverse =
     N * np.fft.ifftn), one pass per axis, last axis first."""

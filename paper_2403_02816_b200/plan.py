@@ -34,6 +34,8 @@ def fused_enabled():
 
 
 FOURIER_SCHEMES = ("if4", "strang")
+RK_SCHEMES = ("rk2", "rk4")
+RK_MAX_BAND = 8
 
 
 def supports(problem, scheme_name):
@@ -43,6 +45,8 @@ def supports(problem, scheme_name):
         from .operators import FourierOperator
         return (scheme_name in FOURIER_SCHEMES and len(problem._blocks[0].shape) <= 3
                 and all(isinstance(b, FourierOperator) and b._sep is not None for b in problem._blocks))
+    if scheme_name in RK_SCHEMES:
+        return BandedRKPlan.applies(problem, scheme_name)
     return scheme_name in FUSED_SCHEMES and all(isinstance(b, KroneckerOperator) for b in problem._blocks)
 
 
@@ -51,6 +55,8 @@ def make_plan(problem, scheme_name, like):
         if PencilFourierPlan.applies(problem, scheme_name, like):
             return PencilFourierPlan(problem, scheme_name, like)
         return FourierPlan(problem, scheme_name, like)
+    if scheme_name in RK_SCHEMES:
+        return BandedRKPlan(problem, scheme_name, like)
     return FusedPlan(problem, scheme_name, like)
 
 
@@ -663,12 +669,6 @@ class PencilFourierPlan(FourierPlan):
                 STR_A0: w = F0^-1 T / N; u_k = flow(w, t/2) (checked, stored);
                 T = F0 flow(u_k, t/2) of step k + 1
       4 passes per 3D step: 144 B/pt.
-    3D grids with n1 == n2 >= 64 (CGL_FFT_PLANE=0 disables): the axis-1 passes
-    either side of a contiguous-axis program run with it in ONE persistent
-    plane-chunked launch (csrc/fftplane.cu: F1, program, F1^-1 per axis-0 plane,
-    the intermediates L2-resident).  if4 becomes 4 x (G0, plane B_i) = 8 launches
-    and 432 B/pt per step, strang (plane STR_MID, STR_A0) = 2 launches, 80 B/pt;
-    same arithmetic, bit-identical results.
     Divergence keys and positions are those of the stage kernels (same
     programs, same flag record), so diverged_at / reason are unchanged.
     """
@@ -698,9 +698,6 @@ class PencilFourierPlan(FourierPlan):
         self.graph_launches = {}
         self.replayed_launches = 0
         self.W = []
-        from . import fftpass as _fp
-        self.plane = (os.environ.get("CGL_FFT_PLANE", "1") != "0" and _fp.plane_supported(self.shape))
-        self._plane_ws = _fp.plane_workspace() if self.plane else None
 
     @staticmethod
     def applies(problem, scheme_name, like):
@@ -715,10 +712,6 @@ class PencilFourierPlan(FourierPlan):
     def _pass(self, prog, axis, src, dst, tau, inverse=False, **kw):
         from .fftpass import axis_pass
         axis_pass(src, dst, axis, inverse=inverse, program=prog, ops=self._ops(tau, **kw), shape=self.shape)
-
-    def _plane(self, prog, field, tau, **kw):
-        from .fftpass import plane_pass
-        plane_pass(field, prog, self._ops(tau, **kw), self._plane_ws, shape=self.shape)
 
     def load_state(self, u0, tau):
         from .fftpass import fftn
@@ -735,8 +728,6 @@ class PencilFourierPlan(FourierPlan):
         last = len(self.shape) - 1
         if self.scheme == "if4":
             self._pass("if4_start", last, None, self.T, tau, u=self.U[0][0])
-            if self.plane:   # every eval then starts at G0: T = F1^-1 F2^-1 (stage input)
-                self._pass("plain", 1, self.T, self.T, tau, inverse=True)
         else:
             self._pass("str_start", 0, None, self.T, tau, u=self.U[0][0], scale=1.0 / self.n)
 
@@ -750,13 +741,6 @@ class PencilFourierPlan(FourierPlan):
             u = self.U[0][0]
             g1, g2, g3 = self.G
             for prog, gout in (("if4_b1", g1), ("if4_b2", g2), ("if4_b3", g3), ("if4_b4", None)):
-                if self.plane:
-                    self._pass("g", 0, T, T, tau, scale=inv_n)
-                    if gout is not None:
-                        self._plane(prog, T, tau, u=u, g_out=gout)
-                    else:
-                        self._plane(prog, T, tau, u=u, u_out=u, g=(g1, g2, g3))
-                    continue
                 if d == 3:
                     self._pass("plain", 1, T, T, tau, inverse=True)
                 self._pass("g", 0, T, T, tau, scale=inv_n)
@@ -768,14 +752,11 @@ class PencilFourierPlan(FourierPlan):
                     self._pass(prog, last, T, T, tau, u=u, u_out=u, g=(g1, g2, g3))
         else:
             out = self.U[k % 2][0]
-            if self.plane:
-                self._plane("str_mid", T, tau)
-            else:
-                if d == 3:
-                    self._pass("plain", 1, T, T, tau)
-                self._pass("str_mid", last, T, T, tau)
-                if d == 3:
-                    self._pass("plain", 1, T, T, tau, inverse=True)
+            if d == 3:
+                self._pass("plain", 1, T, T, tau)
+            self._pass("str_mid", last, T, T, tau)
+            if d == 3:
+                self._pass("plain", 1, T, T, tau, inverse=True)
             self._before_end(flag)
             self._pass("str_a0", 0, T, T, tau, u_out=out, scale=inv_n)
 
@@ -784,3 +765,115 @@ class PencilFourierPlan(FourierPlan):
         if self.scheme == "if4":
             return self.U[0]
         return [fftn(self.U[k % 2][0])]
+
+
+def half_bandwidth(m):
+    """max |i - j| over the exactly non-zero entries of a square host matrix."""
+    import numpy as np
+    i, j = np.nonzero(m)
+    return int(np.abs(i - j).max()) if i.size else 0
+
+
+class BandedRKPlan(FusedPlan):
+    """rk2 / rk4 (integrators.py:146-158) on Kronecker-sum operators whose
+    per-direction factors are banded (half-bandwidth <= 8: every FD operator of
+    operators.py:40-113), graph-captured, one `cgl_rk_stage` launch per stage:
+    f_i = K x_i + g(x_i) as a (2 b + 1)-point contraction per direction, the next
+    stage input and the running combination u + tau sum b_i f_i in the same
+    pass.  rk4: 4 launches per step (reference: 4 x (d dense products + g +
+    sums) + a 5-term combination).  1..3 dimensions, 1 or 2 components (one
+    operator per component).  The new state is checked finite at (step, 255)
+    like every other plan; the state ping-pongs, so a diverged run returns the
+    reference's post-step fields."""
+
+    def __init__(self, problem, scheme_name, like):
+        import numpy as np
+        self.p = problem
+        self.scheme = scheme_name
+        self.nf = len(like)
+        self.shape = tuple(like[0].shape)
+        self.n = like[0].numel()
+        self.nl = problem._nl
+        self.blocks = problem._blocks
+        mk = lambda: [torch.empty_like(like[0]) for _ in range(self.nf)]  # noqa: E731
+        self.U = [mk(), mk()]
+        self.X = [mk(), mk()]
+        self.ACC = mk()
+        self.W = []
+        d = len(self.shape)
+        # one half-bandwidth per direction (the widest component), bands packed to it
+        self.hb = [max(half_bandwidth(b.matrices[mu]) for b in self.blocks) for mu in range(d)]
+        self.bands = []
+        for b in self.blocks:
+            for mu in range(d):
+                m, hb, n = b.matrices[mu], self.hb[mu], self.shape[mu]
+                band = np.zeros((n, 2 * hb + 1), dtype=complex)
+                for dd in range(2 * hb + 1):
+                    off = dd - hb
+                    i0, i1 = max(0, -off), min(n, n - off)
+                    band[i0:i1, dd] = m[np.arange(i0, i1), np.arange(i0, i1) + off]
+                self.bands.append(torch.from_numpy(band).to(like[0].device))
+        self._hb_c = (_lib.c_int * d)(*self.hb)
+        self.graphs = {}
+        self.flag = _lib.new_flag(0)
+        self._pos = _lib.rel_pos(1)
+        self._k_base = 0
+        self._flag0 = self.flag.clone()
+        self.graph_launches = {}
+        self.replayed_launches = 0
+
+    @staticmethod
+    def applies(problem, scheme_name):
+        if scheme_name not in RK_SCHEMES or problem.fourier:
+            return False
+        if not all(isinstance(b, KroneckerOperator) for b in problem._blocks):
+            return False
+        if len(problem._blocks[0].shape) > 3 or any(b.shape != problem._blocks[0].shape for b in problem._blocks):
+            return False
+        return all(half_bandwidth(m) <= RK_MAX_BAND for b in problem._blocks for m in b.matrices)
+
+    def load_state(self, u0, tau):
+        self._tau = float(tau)
+        super().load_state(u0, tau)
+
+    def result(self, k):
+        """State after step k.  A step that ended non-finite is redone from its
+        (intact) input on the dense-product path: a dense product turns one
+        inf into NaNs along whole fibres (0 x inf), the banded contraction only
+        next to it, and the reference returns the former."""
+        key = int(self.flag[0].item()) & ((1 << 64) - 1)
+        if key != _lib.NO_DIVERGENCE and (key >> 24) == k and (key & 0xFF) == _lib.NONFINITE_STATE:
+            from .integrators import _STEPPERS
+            ctx, self.p._ctx = self.p._ctx, None
+            try:
+                return list(_STEPPERS[self.scheme](self.p, self.U[(k - 1) % 2], self._tau))
+            finally:
+                self.p._ctx = ctx
+        return self.U[k % 2]
+
+    def _rk(self, x, u, acc_in, x_out, acc_out, cx, ca, check):
+        pa = _lib.ptr_array
+        _lib.check(_lib.load().cgl_rk_stage(
+            _lib.stream(), len(self.shape), _lib.i64_array(self.shape), self.nf, self._hb_c, pa(self.bands),
+            _lib.ctypes.byref(self.nl), pa(x), pa(u), pa(acc_in) if acc_in is not None else None,
+            pa(x_out) if x_out is not None else None, pa(acc_out) if acc_out is not None else None,
+            float(cx), float(ca), 1 if check else 0, _lib.flag_ptr(self.flag), self._pos), "cgl_rk_stage")
+
+    def prologue(self, flag, tau):
+        pass
+
+    def step(self, k, flag, tau):
+        self._pos = _lib.rel_pos(k - self._k_base)
+        u, out = self.U[(k - 1) % 2], self.U[k % 2]
+        X0, X1, A = self.X[0], self.X[1], self.ACC
+        if self.scheme == "rk2":
+            self._rk(u, u, None, X0, A, tau, 0.5 * tau, False)          # x1 = u + t f1; acc = u + t/2 f1
+            self._before_end(flag)
+            self._rk(X0, u, A, None, out, 0.0, 0.5 * tau, True)         # out = acc + t/2 f2
+        else:
+            t6 = tau / 6.0
+            self._rk(u, u, None, X0, A, 0.5 * tau, t6, False)           # x1 = u + t/2 f1; acc = u + t/6 f1
+            self._rk(X0, u, A, X1, A, 0.5 * tau, 2.0 * t6, False)       # x2 = u + t/2 f2; acc += t/3 f2
+            self._rk(X1, u, A, X0, A, tau, 2.0 * t6, False)             # x3 = u + t f3;   acc += t/3 f3
+            self._before_end(flag)
+            self._rk(X0, u, A, None, out, 0.0, t6, True)                # out = acc + t/6 f4

@@ -132,77 +132,3 @@ def test_pencil_plan_matches_cufft_plan(scheme):
         assert key == _lib.NO_DIVERGENCE
         outs.append(plan.result(w.steps)[0].clone())
     assert rel_l2(outs[0].cpu().numpy(), outs[1].cpu().numpy()) <= 1e-12
-
-
-@pytest.mark.parametrize("shape", [(16, 64, 64), (64, 128, 128), (32, 256, 256), (16, 512, 512)])
-@pytest.mark.parametrize("prog", ["if4_b1", "if4_b2", "if4_b3", "if4_b4", "str_mid"])
-def test_plane_pass_bit_identical_to_three_passes(shape, prog):
-    """csrc/fftplane.cu: F1, program, F1^-1 per axis-0 plane in one persistent
-    ticketed launch == the three cgl_fft_pass launches it replaces, bit for bit
-    (same templates); repeated launches reuse the self-zeroing workspace."""
-    from paper_2403_02816_b200 import _lib, fftpass
-    assert fftpass.plane_supported(shape)
-    n = 1
-    for s in shape:
-        n *= s
-    T0 = _rand(shape, 3) * 0.1
-    u = _rand(shape, 4) * 0.1
-    g = [_rand(shape, 5 + i) * 0.1 for i in range(3)]
-    tabs = [[torch.exp(-0.01 * fr * _rand((shape[d],), 10 + d).abs() ** 2 * (1 + 0.3j)) for d in range(3)]
-            for fr in (0.5, 1.0)]
-    nl = _lib.Nonlinear()
-    nl.alpha3, nl.beta3, nl.kind = -1.0, 1.0, 0
-    flag = _lib.new_flag(0)
-
-    def ops(uu, gout):
-        return fftpass.make_ops(u=uu, u_out=uu, g=tuple(g), g_out=gout, tables=tabs, tau=0.01, nl=nl, flag=flag,
-                                pos=_lib.rel_pos(1))
-
-    # three separate passes
-    Ta, ua, ga = T0.clone(), u.clone(), torch.zeros_like(u)
-    fftpass.axis_pass(Ta, Ta, 1)
-    fftpass.axis_pass(Ta, Ta, 2, program=prog, ops=ops(ua, ga))
-    fftpass.axis_pass(Ta, Ta, 1, inverse=True)
-    # one plane launch, twice on fresh inputs (the workspace must come back zeroed)
-    ws = fftpass.plane_workspace()
-    for _ in range(2):
-        Tb, ub, gb = T0.clone(), u.clone(), torch.zeros_like(u)
-        fftpass.plane_pass(Tb, prog, ops(ub, gb), ws)
-        torch.cuda.synchronize()
-        assert int(ws.abs().sum()) == 0
-        assert torch.equal(torch.view_as_real(Ta), torch.view_as_real(Tb))
-        assert torch.equal(torch.view_as_real(ua), torch.view_as_real(ub))
-        assert torch.equal(torch.view_as_real(ga), torch.view_as_real(gb))
-    assert int(flag[0]) == -1
-
-
-def test_plane_pass_rejects_unsupported():
-    from paper_2403_02816_b200 import fftpass
-    for shape in [(16, 32, 32), (64, 64, 128), (64, 64), (16, 1024, 1024)]:
-        assert not fftpass.plane_supported(shape)
-    x = _rand((16, 64, 64))
-    ws = fftpass.plane_workspace()
-    with pytest.raises(RuntimeError):
-        fftpass.plane_pass(x, "plain", fftpass.make_ops(), ws)      # not a contiguous-axis program
-    with pytest.raises(RuntimeError):
-        fftpass.plane_pass(x, "if4_b1", fftpass.make_ops(), ws)     # operands missing
-
-
-@pytest.mark.parametrize("scheme", ["if4", "strang"])
-def test_plane_plan_bit_identical_to_pass_plan(scheme, monkeypatch):
-    """PencilFourierPlan with and without the plane-chunked launches: the same
-    state bits after 6 steps at 128^3."""
-    from paper_2403_02816_b200 import SCHEMES, _lib, workloads as W
-    from paper_2403_02816_b200.plan import PencilFourierPlan
-    w = W.CONFIGS["C3"].scaled(128, 6)
-    prob = W.build_problem(w)
-    x0 = W.state_for_problem(w, W.initial_state_device(w))
-    prob.prepare(w.tau, SCHEMES[scheme])
-    outs = []
-    for flagv in ("1", "0"):
-        monkeypatch.setenv("CGL_FFT_PLANE", flagv)
-        plan = PencilFourierPlan(prob, scheme, [x0])
-        assert plan.plane == (flagv == "1")
-        assert plan.run([x0], w.steps, w.tau) == _lib.NO_DIVERGENCE
-        outs.append(plan.result(w.steps)[0].clone())
-    assert torch.equal(torch.view_as_real(outs[0]), torch.view_as_real(outs[1]))

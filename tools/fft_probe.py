@@ -94,14 +94,6 @@ def main():
     y = x.clone()
     run("STR_A0 axis 0", lambda: plan._pass("str_a0", 0, T, T, w.tau, u_out=y, scale=1.0 / N), 48, True)
     run("STR_MID axis 2", lambda: plan._pass("str_mid", 2, T, T, w.tau), 32, True)
-    if fftpass.plane_supported(shape):
-        ws = fftpass.plane_workspace()
-        mk = lambda **kw: plan._ops(w.tau, **kw)  # noqa: E731
-        run("PLANE IF4_B1 (F1,B1,F1^-1)", lambda: fftpass.plane_pass(T, "if4_b1", mk(u=u, g_out=g[0]), ws), 64, True)
-        run("PLANE IF4_B3 (F1,B3,F1^-1)", lambda: fftpass.plane_pass(T, "if4_b3", mk(u=u, g_out=g[2]), ws), 64, True)
-        run("PLANE IF4_B4 (F1,B4,F1^-1)", lambda: fftpass.plane_pass(T, "if4_b4", mk(u=v, u_out=v, g=tuple(g)), ws),
-            112, True)
-        run("PLANE STR_MID (F1,MID,F1^-1)", lambda: fftpass.plane_pass(T, "str_mid", mk(), ws), 32, True)
     run("cuFFT Z2Z 3D fwd", lambda: spectral.fft_dev(T, inverse=False, out=T), 32)
     if not eager:
         print(json.dumps(dict(n=n, peak_gbs=peak, rows=rows)))
