@@ -183,3 +183,24 @@ def test_snapshot_errors(tmp_path):
         cio.read_snapshot(p)
     with pytest.raises(ValueError):
         cio.write_snapshot(tmp_path / "x.cgls", (np.zeros((2, 3)), np.zeros((3, 2))), 0.0, [range(2), range(3)])
+
+
+@pytest.mark.parametrize("shape,world", [((8, 6, 4), 2), ((12, 5), 4), ((6,), 3)])
+def test_sharded_snapshot_writer_matches_single_writer(tmp_path, shape, world):
+    """Every rank storing its axis-0 slab through the shared file map gives the
+    reference writer's bytes (io.py:35-59) -- no gather of the field."""
+    from paper_2403_02816_b200 import io as cio
+    rng = np.random.default_rng(1)
+    fields = [rng.standard_normal(shape) + 1j * rng.standard_normal(shape) for _ in range(2)]
+    grids = [np.linspace(-1.0, 1.0, n) for n in shape]
+    whole, parts = tmp_path / "whole.cgls", tmp_path / "parts.cgls"
+    cio.write_snapshot(whole, fields, 1.25, grids)
+    p0 = shape[0] // world
+    for rank in range(world):
+        a, b = rank * p0, (rank + 1) * p0
+        cio.write_snapshot_sharded(parts, [f[a:b] for f in fields], 1.25, grids, shape, (a, b), rank=rank,
+                                   chunk_bytes=64)
+    assert parts.read_bytes() == whole.read_bytes()
+    assert (tmp_path / "parts.cgls.grid.txt").read_text() == (tmp_path / "whole.cgls.grid.txt").read_text()
+    with pytest.raises(ValueError):
+        cio.write_snapshot_sharded(parts, [fields[0]], 0.0, grids, shape, (0, p0))

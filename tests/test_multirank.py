@@ -39,7 +39,7 @@ def _mode(u, m, axis):
     return torch.movedim(torch.tensordot(m, u, dims=([1], [axis])), 0, axis)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, tmpdir=None):
     import sys
     sys.path.insert(0, REPO)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -88,17 +88,26 @@ def _worker(rank, world, port, q):
         back2 = [torch.empty_like(local)]
         ex.to_slabs(cols, back2)
         res["froundtrip"] = torch.equal(back2[0], local)
+        # sharded snapshot: both ranks store their slab into one file concurrently
+        from paper_2403_02816_b200 import io as cio
+        grids = [np.linspace(0.0, 1.0, n) for n in SHAPE]
+        path = os.path.join(tmpdir, "sharded.cgls")
+        cio.write_snapshot_sharded(path, [local.numpy()], 0.5, grids, SHAPE, (a, b), rank=rank, barrier=dist.barrier)
+        if rank == 0:
+            ref = os.path.join(tmpdir, "whole.cgls")
+            cio.write_snapshot(ref, [u.numpy()], 0.5, grids)
+            res["snapshot"] = open(path, "rb").read() == open(ref, "rb").read()
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2])
-def test_slab_sharded_path_gloo(world):
+def test_slab_sharded_path_gloo(world, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, str(tmp_path))) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=120) for _ in range(world))
@@ -111,6 +120,7 @@ def test_slab_sharded_path_gloo(world):
         assert res["mode0"] <= 1e-14 and res["tucker"] <= 1e-14, (rank, res)
         assert res["key"] == (3 << 24) | (1 << 8) | 4
         assert res["key2"] == (7 << 24) | 5
+    assert results[0]["snapshot"]
 
 
 def test_slab_layout_validation():
