@@ -338,8 +338,12 @@ def fourier_roofline(torch, w, scheme, step_seconds):
                         "frac": a / peak}
     d = passes[dom]
     step_bytes = FOURIER_BYTES.get(scheme, 0) * n
+    # DRAM bytes per launch of the dominant program from the ncu --set full capture of this
+    # round at 512^3 (profiles/r02c_fft_passes.txt: dram__bytes_read.sum + dram__bytes_write.sum)
+    traffic = {"if4": 2.147515e9 + 2.534077e9, "strang": 2.149681e9 + 4.291060e9}.get(scheme) \
+        if tuple(w.extents) == (512, 512, 512) else None
     return {"bound": "hbm", "achieved": d["gbs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
-            "traffic": None,
+            "traffic": traffic,
             "kernel": f"cgl::fftp::fft_*_kernel, dominant program: {dom} (largest share of the step in "
                       "profiles/r02_launches_C3_if4.txt / _strang.txt)",
             "algorithmic_bytes_per_launch": d["bytes_per_point"] * n, "per_launch_ms": d["ms"], "peak_source": src,

@@ -56,7 +56,14 @@ __global__ void __launch_bounds__(kRkThreads) rk_stage_kernel(const RkArgs a) {
   const uint64_t check_pos = (step << 24) | (255ull << 8);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.N; i += (int64_t)gridDim.x * blockDim.x) {
     int idx[3] = {0, 0, 0};
-    {
+    if (a.N <= 0x7fffffff) {  // 32-bit divisions (every grid up to 1024^3 but itself)
+      unsigned r = (unsigned)i;
+      for (int mu = a.nd - 1; mu >= 0; --mu) {
+        const unsigned q = r / (unsigned)a.n[mu];
+        idx[mu] = (int)(r - q * (unsigned)a.n[mu]);
+        r = q;
+      }
+    } else {
       int64_t r = i;
       for (int mu = a.nd - 1; mu >= 0; --mu) {
         idx[mu] = (int)(r % a.n[mu]);
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(kRkThreads) rk_stage_kernel(const RkArgs a) {
         double2 t = make_double2(0.0, 0.0);
         for (int d = d0; d <= d1; ++d) {
           const double2 coef = ld2(band + d);
-          const double2 v = d == b ? xv.c[c] : a.x[c][i + (int64_t)(d - b) * a.stride[mu]];
+          const double2 v = d == b ? xv.c[c] : ld2(a.x[c] + i + (int64_t)(d - b) * a.stride[mu]);
           // t += coef * v (complex multiply-add, fixed rounding structure)
           t.x = fma(coef.x, v.x, fma(-coef.y, v.y, t.x));
           t.y = fma(coef.x, v.y, fma(coef.y, v.x, t.y));

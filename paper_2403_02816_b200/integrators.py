@@ -440,7 +440,7 @@ def _detach(fields, host, cache, key):
     device clones, or -- when a clone does not fit (1024^3 fields) -- the
     buffers themselves, handed over by dropping the plan from the cache."""
     if host:
-        return tuple(f.cpu().numpy() for f in fields)
+        return tuple(to_host_if(f, True) for f in fields)
     try:
         return tuple(f.clone() for f in fields)
     except torch.OutOfMemoryError:

@@ -32,9 +32,13 @@ class LoopbackTransposer(D.Transposer):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 4
-    ranks = [int(a) for a in args if a.isdigit() and a != str(steps)] or [1, 2, 4, 8]
+    argv = sys.argv[1:]
+    steps = 4
+    if "--steps" in argv:
+        i = argv.index("--steps")
+        steps = int(argv[i + 1])
+        argv = argv[:i] + argv[i + 2:]
+    ranks = [int(a) for a in argv if a.isdigit()] or [1, 4, 8]
     if len(ranks) > 1:
         # one process per rank count: every case gets the whole HBM
         import subprocess
