@@ -431,7 +431,7 @@ int cgl_slab_transpose(void* stream, void* comm, int world, int dir, int64_t pla
                        const double* in, double* out, double* work);
 
 /* ---- Cross-mode fused 2D Tucker (csrc/tucker2d.cu) ------------------------
- * out_q = E0_q in_q E1_q^T for (n0 x n1) fields (n1 <= 1024), mode 0 then
+ * out_q = E0_q in_q E1_q^T for (n0 x n1) fields (n0, n1 <= 1024), mode 0 then
  * mode 1 (tensors.py:62-69) in ONE launch, the intermediate row in shared
  * memory.  e1t = E1^T.  band0/band1: int pairs [lo, hi] per row of E0 / E1,
  * the significant band (entries >= 2^-60 of the row max).

@@ -46,6 +46,7 @@ struct T2Args {
 template <int PROG>
 __global__ void __launch_bounds__(kT2Threads) tucker2d_kernel(const T2Args a) {
   __shared__ double2 trow[kT2MaxN];
+  __shared__ double2 erow[kT2MaxN];  // row i of E0 inside its band
   pdl_wait();
   pdl_trigger();
   const T2Item& it = a.it[blockIdx.y];
@@ -60,10 +61,16 @@ __global__ void __launch_bounds__(kT2Threads) tucker2d_kernel(const T2Args a) {
   const int64_t i = blockIdx.x;
   // phase 1: T[i, :] = sum_k E0[i, k] In[k, :]
   const int2 b0 = __ldg(it.band0 + i);
+  // the band of E0's row is read once, coalesced (constant factor: it does not
+  // wait for the previous kernel's data); the loop below then has one
+  // independent global load per term and runs 8 terms deep
+  for (int k = b0.x + (int)threadIdx.x; k <= b0.y; k += blockDim.x) erow[k - b0.x] = ld2(it.e0 + i * n0 + k);
+  __syncthreads();
   for (int64_t j = threadIdx.x; j < n1; j += blockDim.x) {
     double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
     for (int k = b0.x; k <= b0.y; ++k) {
-      const double2 e = ld2(it.e0 + i * n0 + k);
+      const double2 e = erow[k - b0.x];
       const double2 x = ld2(it.in + (int64_t)k * n1 + j);
       acc.x = fma(e.x, x.x, fma(-e.y, x.y, acc.x));
       acc.y = fma(e.x, x.y, fma(e.y, x.x, acc.y));
@@ -89,6 +96,7 @@ __global__ void __launch_bounds__(kT2Threads) tucker2d_kernel(const T2Args a) {
     }
     if (j >= n1) continue;
     double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
     for (int k = lo; k <= hi; ++k) {
       const double2 t = trow[k];
       const double2 e = ld2(it.e1t + (int64_t)k * n1 + j);
@@ -115,7 +123,7 @@ int tucker2d_launch(cudaStream_t st, int program, int nitems, int64_t n0, int64_
                     const int* const* band1, const cgl_nonlinear_t* nl, double tau, cgl_flag_t* flag,
                     uint64_t pos) {
   if (nitems < 1 || nitems > kMaxItems) return set_error(CGL_EINVAL, "tucker2d: 1..8 items");
-  if (n0 < 1 || n1 < 1 || n0 > 65535 || n1 > kT2MaxN) return set_error(CGL_ESHAPE, "tucker2d: n1 <= 1024");
+  if (n0 < 1 || n1 < 1 || n0 > kT2MaxN || n1 > kT2MaxN) return set_error(CGL_ESHAPE, "tucker2d: n0, n1 <= 1024");
   if (program != 0 && program != 1) return set_error(CGL_EINVAL, "tucker2d: program 0 (plain) or 1 (strang end)");
   program = program == 1 ? P_STRANG_END : -1;
   if (program == P_STRANG_END && (nitems != 1 || !nl || nl->kind == 2))

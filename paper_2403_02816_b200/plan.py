@@ -217,7 +217,7 @@ class FusedPlan:
         """Cross-mode fused 2D Tucker (cgl_tucker2d, one launch per Tucker
         group) for the small 2D grids the DMMA products serve."""
         if getattr(self, "_t2d", None) is None:
-            self._t2d = (len(self.shape) == 2 and self.shape[1] <= 1024 and self.shape[0] <= 65535
+            self._t2d = (len(self.shape) == 2 and self.shape[1] <= 1024 and self.shape[0] <= 1024
                          and not self.use_oz and all(isinstance(b, KroneckerOperator) for b in self.blocks)
                          and type(self) is FusedPlan and os.environ.get("CGL_TUCKER2D", "1") != "0")
         return self._t2d
