@@ -63,7 +63,11 @@ enum cgl_reason {
 };
 
 /* Nonlinearity (flows.py:42-78). kind: 0 cubic, 1 cubic_quintic,
- * 2 coupled_cubic_quintic (two components). */
+ * 2 coupled_cubic_quintic (two components); 3 (cgl_stage flow programs only):
+ * cubic_quintic under the three-term splitting -- every flow of a strang /
+ * split4 program is the pair of exact flows of integrators.py:178-195
+ * (quintic then cubic in the first half of a Strang step, cubic then quintic
+ * in the second), two sequence positions per flow. */
 typedef struct cgl_nonlinear_t {
   double alpha3, beta3, alpha4, beta4, alpha5;
   int kind;

@@ -368,7 +368,7 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
     a.scale = ops->scale;
     const cgl_nonlinear_t& nl = ops->nl;
     a.nl = StageNL{nl.alpha3, nl.beta3, nl.alpha4, nl.beta4, nl.alpha5, nl.kind};
-    if (nl.kind == 2) return set_error(CGL_EINVAL, "fft_pass: scalar fields only");
+    if (nl.kind >= 2) return set_error(CGL_EINVAL, "fft_pass: scalar two-term kinds only");
     a.fw = 1;
     a.flag = ops->flag;
     a.pos = ops->pos;

@@ -1632,7 +1632,7 @@ int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int n
       case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
       default: return set_error(CGL_EINVAL, "oz_gemm_fused: stage program must be if4 MID/END, strang END, split4 MID/END");
     }
-    if (!p->nl || p->nl->kind == 2) return set_error(CGL_EINVAL, "oz_gemm_fused: single-component nonlinearity required");
+    if (!p->nl || p->nl->kind >= 2) return set_error(CGL_EINVAL, "oz_gemm_fused: single-component nonlinearity required");
     if (nout && (!p->out || !p->out[0])) return set_error(CGL_EINVAL, "oz_gemm_fused: program writes an FP64 output");
     prog = p->program;
     StageArgs& a = R.s;

@@ -14,8 +14,10 @@ constexpr int kStageThreads = 256;
 
 struct StageNL {
   double a3, b3, a4, b4, a5;
-  int kind;  // 0 cubic (exact flow), 1 cubic_quintic, 2 coupled
+  int kind;  // 0 cubic (exact flow), 1 cubic_quintic, 2 coupled, 3 cubic_quintic with the
+             // three-term splitting: every flow is a pair of exact flows (strang_3t / split4_3t)
 };
+constexpr int kKindThreeTerm = 3;
 
 template <int NF>
 struct V {
@@ -84,11 +86,42 @@ __device__ __forceinline__ double2 cubic_exact(const StageNL& p, double2 u, doub
   return v;
 }
 
-// one flow call of the scheme: seq positions seq0, seq0+1, ... (exact) or seq0 (rk4)
+// exact quintic flow (flows.py:103-115) of one component at position pos;
+// |exp(-L/4)| = (1 - y)^(-1/4) as sqrt(rsqrt(1 - y)), the phase from L (as cubic_exact)
+__device__ __forceinline__ double2 quintic_exact(const StageNL& p, double2 u, double t, uint64_t pos, uint64_t& key) {
+  const double m = cabs2(u), m4 = m * m;
+  if (fabs(p.a4) < 1e-14) {
+    double sn, cs;
+    sincos(p.b4 * m4 * t, &sn, &cs);
+    return cmul(u, make_double2(cs, sn));
+  }
+  const double y = 4.0 * p.a4 * m4 * t;
+  if (y >= 1.0) note(key, pos, CGL_BLOWUP_QUINTIC);
+  const double L = log1p(-y);
+  double sn, cs;
+  sincos((-p.b4 / (4.0 * p.a4)) * L, &sn, &cs);
+  const double r = sqrt(rsqrt(1.0 - y));
+  const double2 v = cmul(u, make_double2(__dmul_rn(r, cs), __dmul_rn(r, sn)));
+  if (!cfinite(v)) note(key, pos, CGL_NONFINITE_QUINTIC);
+  return v;
+}
+
+// one flow call of the scheme: seq positions seq0, seq0+1, ... (exact) or seq0 (rk4).
+// Three-term splitting (kind 3, integrators.py:178-195 `_strang3`): the flow over t is
+// quintic(t) then cubic(t) at seq0, seq0 + 1 in the first half of a Strang step and
+// cubic(t) then quintic(t) in the second half (`second`).
 template <int NF>
 __device__ __forceinline__ V<NF> flow(const StageNL& p, const V<NF>& u, double t, uint64_t step, int seq0,
-                                      uint64_t& key) {
+                                      uint64_t& key, bool second = false) {
   V<NF> r;
+  if (p.kind == kKindThreeTerm) {
+    const uint64_t p0 = (step << 24) | ((uint64_t)seq0 << 8), p1 = (step << 24) | ((uint64_t)(seq0 + 1) << 8);
+#pragma unroll
+    for (int c = 0; c < NF; ++c)
+      r.c[c] = second ? quintic_exact(p, cubic_exact(p, u.c[c], t, p0, key), t, p1, key)
+                      : cubic_exact(p, quintic_exact(p, u.c[c], t, p0, key), t, p1, key);
+    return r;
+  }
   if (p.kind == 0) {
 #pragma unroll
     for (int c = 0; c < NF; ++c) r.c[c] = cubic_exact(p, u.c[c], t, (step << 24) | ((uint64_t)(seq0 + c) << 8), key);

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
   // first flow seq of the program (skip position); non-flow programs: 0
   int first = 0;
   if (PROG == P_SPLIT4_MID) first = a.fw;           // seq w (coarse second flow)
-  if (PROG == P_SPLIT4_END) first = 4 * a.fw;       // seq 4w
+  if (PROG == P_SPLIT4_END) first = (a.nl.kind == kKindThreeTerm ? 5 : 4) * a.fw;  // seq 4w (three-term: 5w)
   if (PROG == P_STRANG_END || PROG == P_FLOW_END) first = a.fw;  // seq w
   const bool is_end = (PROG == P_IF4_END || PROG == P_SPLIT4_END || PROG == P_STRANG_END || PROG == P_IF2_END ||
                        PROG == P_FIF4_S4 || PROG == P_FLOW_END || PROG == P_IF4_ENDH || PROG == P_IF4_ENDQ);
@@ -127,11 +127,18 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       store<NF>(a.out, NF, i, flow<NF>(a.nl, u, 0.25 * t, step, 2 * a.fw, key));
     } else if (PROG == P_SPLIT4_MID) {
       const V<NF> v = load<NF>(a.in, 0, i, s), f = load<NF>(a.in, NF, i, s);
-      store<NF>(a.out, 0, i, flow<NF>(a.nl, v, 0.5 * t, step, a.fw, key));
-      store<NF>(a.out, NF, i, flow<NF>(a.nl, f, 0.5 * t, step, 3 * a.fw, key));
+      store<NF>(a.out, 0, i, flow<NF>(a.nl, v, 0.5 * t, step, a.fw, key, true));
+      if (a.nl.kind == kKindThreeTerm) {
+        // the two quarter-step flows either side of the fine substep boundary do not
+        // merge: end of fine substep 1 (seq 3w), start of fine substep 2 (seq 4w)
+        const V<NF> f1 = flow<NF>(a.nl, f, 0.25 * t, step, 3 * a.fw, key, true);
+        store<NF>(a.out, NF, i, flow<NF>(a.nl, f1, 0.25 * t, step, 4 * a.fw, key));
+      } else {
+        store<NF>(a.out, NF, i, flow<NF>(a.nl, f, 0.5 * t, step, 3 * a.fw, key));
+      }
     } else if (PROG == P_SPLIT4_END) {
       const V<NF> f = load<NF>(a.in, 0, i, s), c = load<NF>(a.in, NF, i, s);
-      const V<NF> fine = flow<NF>(a.nl, f, 0.25 * t, step, 4 * a.fw, key);
+      const V<NF> fine = flow<NF>(a.nl, f, 0.25 * t, step, (a.nl.kind == kKindThreeTerm ? 5 : 4) * a.fw, key, true);
       V<NF> out;
 #pragma unroll
       for (int q = 0; q < NF; ++q) out.c[q] = cadd(cscale(4.0 / 3.0, fine.c[q]), cscale(-1.0 / 3.0, c.c[q]));
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       store<NF>(a.out, 2 * NF, i, flow<NF>(a.nl, out, 0.25 * t, step + 1, 2 * a.fw, key));
     } else if (PROG == P_STRANG_END) {
       const V<NF> w = load<NF>(a.in, 0, i, s);
-      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key);
+      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key, true);
       if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
       store<NF>(a.out, 0, i, out);
       store<NF>(a.out, NF, i, flow<NF>(a.nl, out, 0.5 * t, step + 1, 0, key));
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(kStageThreads) stage_kernel(const StageArgs a)
       // out = flow(w, t/2) at seq w; finiteness of the physical result stands in for the
       // spectral state's (an FFT of finite values is finite barring overflow)
       const V<NF> w = load<NF>(a.in, 0, i, s);
-      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key);
+      const V<NF> out = flow<NF>(a.nl, w, 0.5 * t, step, a.fw, key, true);
       if (!finite_all<NF>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
       store<NF>(a.out, 0, i, out);
     } else if (PROG == P_IF2_END) {
@@ -535,7 +542,8 @@ int stage_slice_launch(cudaStream_t st, int prog, int64_t n0, int64_t Q, const c
   a.nl.b4 = nl->beta4;
   a.nl.a5 = nl->alpha5;
   a.nl.kind = nl->kind;
-  if (nl->kind == 2) return set_error(CGL_EINVAL, "stage_slice: single-component nonlinearities only");
+  if (nl->kind == 2 || nl->kind == kKindThreeTerm)
+    return set_error(CGL_EINVAL, "stage_slice: single-component two-term nonlinearities only");
   a.flag = flag;
   a.pos = pos;
   a.fw = 1;
@@ -653,7 +661,8 @@ int stage_launch(cudaStream_t st, int prog, int nf, int64_t n, const cgl_nonline
   a.nl = StageNL{nl->alpha3, nl->beta3, nl->alpha4, nl->beta4, nl->alpha5, nl->kind};
   a.flag = flag;
   a.pos = pos;
-  a.fw = nl->kind == 0 ? nf : 1;
+  if (nl->kind < 0 || nl->kind > kKindThreeTerm) return set_error(CGL_EINVAL, "stage: unknown nonlinearity kind");
+  a.fw = nl->kind == 0 ? nf : (nl->kind == kKindThreeTerm ? 2 : 1);
   if (prog >= P_FIF4_S1 && prog <= P_FIF4_S4) {
     if (ndim < 1 || ndim > 4 || !shape || !tables) return set_error(CGL_EINVAL, "stage: Fourier programs need tables");
     a.nd = ndim;

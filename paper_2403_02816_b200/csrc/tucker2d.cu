@@ -126,7 +126,7 @@ int tucker2d_launch(cudaStream_t st, int program, int nitems, int64_t n0, int64_
   if (n0 < 1 || n1 < 1 || n0 > kT2MaxN || n1 > kT2MaxN) return set_error(CGL_ESHAPE, "tucker2d: n0, n1 <= 1024");
   if (program != 0 && program != 1) return set_error(CGL_EINVAL, "tucker2d: program 0 (plain) or 1 (strang end)");
   program = program == 1 ? P_STRANG_END : -1;
-  if (program == P_STRANG_END && (nitems != 1 || !nl || nl->kind == 2))
+  if (program == P_STRANG_END && (nitems != 1 || !nl || nl->kind >= 2))
     return set_error(CGL_EINVAL, "tucker2d: STRANG_END takes one scalar field");
   T2Args a{};
   for (int q = 0; q < nitems; ++q) {

@@ -26,7 +26,11 @@ from . import _lib
 from .operators import KroneckerOperator
 from .tensors import tucker_dev
 
-FUSED_SCHEMES = ("if4", "strang", "split4", "if2")
+FUSED_SCHEMES = ("if4", "strang", "split4", "if2", "strang_3t", "split4_3t")
+# three-term schemes run the strang / split4 bodies with every flow a pair of
+# exact flows (integrators.py:178-195): nonlinearity kind 3 in the stage kernels
+THREE_TERM = {"strang_3t": "strang", "split4_3t": "split4"}
+KIND_THREE_TERM = 3
 
 
 def fused_enabled():
@@ -47,6 +51,8 @@ def supports(problem, scheme_name):
                 and all(isinstance(b, FourierOperator) and b._sep is not None for b in problem._blocks))
     if scheme_name in RK_SCHEMES:
         return BandedRKPlan.applies(problem, scheme_name)
+    if scheme_name in THREE_TERM and len(problem._blocks) != 1:
+        return False
     return scheme_name in FUSED_SCHEMES and all(isinstance(b, KroneckerOperator) for b in problem._blocks)
 
 
@@ -67,10 +73,15 @@ class FusedPlan:
     def __init__(self, problem, scheme_name, like):
         from fractions import Fraction
         self.p = problem
+        self.three = scheme_name in THREE_TERM
+        scheme_name = THREE_TERM.get(scheme_name, scheme_name)
         self.scheme = scheme_name
         self.nf = len(like)
         self.n = like[0].numel()
         self.nl = problem._nl
+        if self.three:
+            self.nl = _lib.Nonlinear.from_buffer_copy(problem._nl)
+            self.nl.kind = KIND_THREE_TERM
         self.blocks = problem._blocks
         self.half, self.one = Fraction(1, 2), Fraction(1)
         mk = lambda: [torch.empty_like(like[0]) for _ in range(self.nf)]  # noqa: E731
@@ -114,7 +125,7 @@ class FusedPlan:
         if self.use_oz is None:
             self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
         if (self.FUSE_STAGE_SLICE and self.scheme in ("if4", "strang", "split4") and self.use_oz and not self.lean
-                and self.nf == 1
+                and self.nf == 1 and not self.three
                 and len(self.shape) >= 2 and self.shape[0] <= 1024 and self.nl.kind != 2
                 and ozaki.single_chunk(self.shape, 4) and os.environ.get("CGL_FUSE_STAGE", "1") != "0"):
             n0, Q = self.shape[0], math.prod(self.shape[1:])
@@ -381,8 +392,8 @@ class FusedPlan:
                 self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
             self._before_end(flag)
             self._end_stage("split4_end", [v, v2], self.state_after(k)[0], [F[0], F[1]], flag, tau)
-        elif self.scheme == "strang" and self.nf == 1 and self.nl.kind != 2 and self._ensure_oz() is False \
-                and self._tucker2d_ok():
+        elif self.scheme == "strang" and self.nf == 1 and self.nl.kind != 2 and not self.three \
+                and self._ensure_oz() is False and self._tucker2d_ok():
             # one launch per step: Tucker + flow, check, next step's flow (cgl_tucker2d);
             # v ping-pongs between B[0] and B[1] (every output row reads a band of input rows)
             v_in, v_out = B[(k - 1) % 2], B[k % 2]

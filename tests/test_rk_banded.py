@@ -1,4 +1,6 @@
-"""Banded Kronecker-sum Runge-Kutta stages (csrc/rkstage.cu, plan.BandedRKPlan)
+"""Fused plans added in round 2 for the schemes that stepped eagerly before.
+
+Banded Kronecker-sum Runge-Kutta stages (csrc/rkstage.cu, plan.BandedRKPlan)
 against dense products (torch) for one stage, and the graph-captured rk2 / rk4
 plans against the generic dense-GEMM path (CGL_FUSED=0) for whole runs:
 1..3 dimensions, both FD orders, one and two components, a blow-up.
@@ -173,3 +175,35 @@ def test_dense_factors_stay_on_the_gemm_path():
     prob = Problem(KroneckerOperator(mats), NonlinearSpec("cubic", p))
     assert not plan.supports(prob, "rk4")
     assert plan.half_bandwidth(np.eye(5)) == 0 and plan.half_bandwidth(np.zeros((4, 4))) == 0
+
+
+@pytest.mark.parametrize("scheme", ["strang_3t", "split4_3t"])
+@pytest.mark.parametrize("extents", [(40, 56), (512, 512), (16, 20, 24)])
+def test_three_term_schemes_run_fused(scheme, extents, monkeypatch):
+    """strang_3t / split4_3t (integrators.py:178-195) on the graph-captured FD
+    plan (strang / split4 bodies, every flow a pair of exact flows, kind 3 in the
+    stage kernels; 512^2 takes the INT8-emulated products) == the eager generic
+    path, and a quintic blow-up is reported at the same step with the same reason."""
+    import paper_2403_02816_b200 as P
+    from paper_2403_02816_b200.plan import FusedPlan
+    rng = np.random.default_rng(11)
+    ic = [0.4 * (rng.standard_normal(extents) + 1j * rng.standard_normal(extents))]
+    steps, t_final = 12, 0.06
+    prob = _problem(extents, "dirichlet2", "cubic_quintic")
+    got = P.integrate(prob, scheme, ic, t_final, steps)
+    plans = list(prob._plans.values())
+    assert plans and all(type(pl) is FusedPlan and pl.three for pl in plans), "three-term plan not used"
+    # explosive quintic term: finite-time blow-up of the exact quintic flow
+    big = [8.0 * ic[0]]
+    from paper_2403_02816_b200 import CglParameters, NonlinearSpec, Problem, build_fd_operator
+    pp = CglParameters(alpha1=1.0, beta1=0.5, alpha2=1.0, alpha3=-1.0, beta3=1.0, alpha4=0.5, beta4=0.05)
+    mk = lambda: Problem(build_fd_operator(pp, tuple(extents), tuple(10.0 + i for i in range(len(extents))),  # noqa: E731
+                                           "dirichlet2"), NonlinearSpec("cubic_quintic", pp))
+    got_b = P.integrate(mk(), scheme, big, t_final, steps)
+    monkeypatch.setenv("CGL_FUSED", "0")
+    want = P.integrate(_problem(extents, "dirichlet2", "cubic_quintic"), scheme, ic, t_final, steps)
+    want_b = P.integrate(mk(), scheme, big, t_final, steps)
+    assert not got.diverged and not want.diverged
+    assert rel_l2(got.fields[0], want.fields[0]) <= 1e-11
+    assert want_b.diverged and "quintic" in want_b.reason
+    assert (got_b.diverged, got_b.diverged_at, got_b.reason) == (True, want_b.diverged_at, want_b.reason)
