@@ -34,6 +34,7 @@
 // correctly rounded 512-entry table (fft_twiddles.h).  Unnormalised both
 // ways (the 1/N of ifftn is applied by the program that consumes the inverse).
 #include "fftpass.cuh"
+#include "fftr32.cuh"
 
 namespace cgl {
 namespace fftp {
@@ -295,8 +296,31 @@ static int launch_nt(const Args& a, cudaStream_t st) {
   return check_launch("fft_pass_kernel");
 }
 
+// 32 points per thread (fftr32.cuh): the 512-point strided G pass, one chunk per CTA
+template <int PROG, bool INV>
+static int launch_r32(const Args& a, cudaStream_t st) {
+  auto kern = fft_r32_kernel<PROG, INV>;
+  const int smem = 4096 * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "fft_r32 attribute");
+    attr = true;
+  }
+  const int64_t chunks = a.O * (a.I / 8);
+  if (chunks <= 0) return 0;
+  cudaError_t e = launch_k(kern, dim3((unsigned)chunks), dim3(128), (size_t)smem, st, dim3(1), a, (int)chunks);
+  if (e != cudaSuccess) return set_cuda_error(e, "fft_r32 launch");
+  return check_launch("fft_r32_kernel");
+}
+
 template <int L, bool CONTIG, int PROG, bool INV>
 static int launch_one(const Args& a, cudaStream_t st) {
+  // the two-transform G pass is bound by the shared-memory data pipe: 32 points per thread
+  // (one exchange per transform) take 1.15 ms at 512^3 against 1.50 ms for the radix-8 plan;
+  // the single-transform passes are HBM/latency-bound and keep the 8-point kernel (0.76-0.87
+  // vs 0.85-1.0 ms), profiles/r02e_fft_r32.txt
+  if constexpr (L == 512 && !CONTIG && PROG == FP_G) return launch_r32<PROG, INV>(a, st);
   if constexpr (L == 512 && !CONTIG) {
     if (threads_for(L, CONTIG, PROG) == 512) return launch_nt<L, CONTIG, PROG, INV, 512>(a, st);
   }

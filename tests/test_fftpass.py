@@ -65,6 +65,26 @@ def test_single_axis_passes(shape):
             assert _relmax(y, ref) <= 1e-14
 
 
+@pytest.mark.parametrize("shape,axis", [((512, 16, 16), 0), ((32, 512, 16), 1), ((64, 16, 32), 0), ((16, 256), 1)])
+def test_fused_g_pass(shape, axis):
+    """program g = F g(scale F^-1 .) along one axis (integrators.py:99-101 on one
+    axis) against torch; 512-point strided pencils take the 32-points-per-thread
+    kernel (csrc/fftr32.cuh), the others the radix-8 plan."""
+    from paper_2403_02816_b200 import _lib, fftpass
+    x = _rand(shape, 2)
+    nl = _lib.Nonlinear()
+    nl.alpha3, nl.beta3, nl.kind = -1.0, 0.7, 0
+    scale = 0.05
+    y = torch.fft.ifft(x, dim=axis) * shape[axis] * scale
+    want = torch.fft.fft((nl.alpha3 + 1j * nl.beta3) * y.abs() ** 2 * y, dim=axis)
+    got = torch.empty_like(x)
+    fftpass.axis_pass(x, got, axis, program="g", ops=fftpass.make_ops(nl=nl, scale=scale))
+    assert _relmax(got, want) <= 1e-13
+    z = x.clone()   # in place
+    fftpass.axis_pass(z, z, axis, program="g", ops=fftpass.make_ops(nl=nl, scale=scale))
+    assert torch.equal(torch.view_as_real(z), torch.view_as_real(got))
+
+
 def test_unsupported_shapes_are_rejected():
     from paper_2403_02816_b200 import _lib, fftpass
     for shape in [(12, 16, 16), (16, 16, 1024), (8, 16, 16), (32,), (16, 16, 16, 16)]:
