@@ -213,41 +213,6 @@ int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems
                 int64_t sA, int64_t sAexp, int64_t sB, int64_t sBexp, int64_t sC,
                 const cgl_flag_t* flag, uint64_t pos);
 
-/* Fused producer + product: the GEMM launch first produces its own data
- * operands B (slices + exponents) in a prologue phase -- the plain data
- * slicing of cgl_oz_slice_multi (program = CGL_PRO_SLICE) or a stage program
- * of cgl_stage_slice whose sliced outputs are the B operands -- then one grid
- * barrier, then the product (no separate slicing / stage launch between two
- * products of a step: integrators.py:146-215 call order unchanged).
- * Operand element (r, k) of source / program input x is x[r*sr + k*sk];
- * plain slicing covers `batch` blocks (strides src_bs elements, out_bs bytes,
- * exp_bs ints) of each of nitems sources; stage programs take in/out/nl/tau
- * /flag/pos as cgl_stage_slice (element (q, i) of the axis-0 data: r = q,
- * k = i, sr = 1, sk = Q).  grid_barrier: device buffer of 2 x uint32 zeroed
- * once, reusable by every fused launch on the stream. */
-#define CGL_PRO_SLICE (-1)
-typedef struct {
-  int program;                 /* CGL_PRO_SLICE or a stage program id (if4_mid, if4_end,
-                                  strang_end, split4_mid, split4_end) */
-  int nitems;                  /* plain slicing: sources (1..8) */
-  const double* const* src;    /* plain: sources; stage: program inputs */
-  double* const* out;          /* stage: FP64 outputs of the program (or NULL) */
-  int8_t* const* slices;       /* sliced outputs (B-mode slices) */
-  int* const* exps;            /* their row exponents */
-  int64_t rows, K, sr, sk;
-  int64_t batch, src_bs, out_bs, exp_bs;
-  const cgl_nonlinear_t* nl;   /* stage programs */
-  double tau, in_scale;
-  cgl_flag_t* flag;
-  uint64_t pos;
-  unsigned* grid_barrier;
-} cgl_oz_prologue_t;
-int cgl_oz_gemm_fused(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems,
-                      const int8_t* const* A, const int* const* Aexp, const int8_t* const* Azmap,
-                      const int8_t* const* B, const int* const* Bexp,
-                      double* const* C, int64_t ldc, int64_t batch, int64_t sB, int64_t sBexp, int64_t sC,
-                      const cgl_flag_t* flag, uint64_t pos, int trans_c, const cgl_oz_prologue_t* pro);
-
 /* ---- pointwise kernels (HBM-bound) --------------------------------------- */
 
 /* out = sum_i coef[i] * x[i] (nterms <= 6, real coefficients) —

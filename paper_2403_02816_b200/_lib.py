@@ -38,7 +38,7 @@ POS_DEVICE = 1 << 63
 
 STAGE = {"if4_pre": 0, "if4_mid": 1, "if4_end": 2, "flow1": 3, "flow2": 4, "split4_mid": 5,
          "split4_end": 6, "strang_end": 7, "if2_pre": 8, "if2_end": 9, "fif4_s1": 10, "fif4_s2": 11,
-         "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14, "if4_midh": 15, "if4_endh": 16, "if4_midq": 17,
+         "fif4_s3": 12, "fif4_s4": 13, "flow_end": 14, "if4_midq": 17,
          "if4_endq": 18}
 
 
@@ -66,17 +66,6 @@ class Nonlinear(ctypes.Structure):
                 ("beta4", c_dbl), ("alpha5", c_dbl), ("kind", c_int)]
 
 
-class OzPrologue(ctypes.Structure):
-    """cgl_oz_prologue_t (include/cgl_b200.h): the producer phase of cgl_oz_gemm_fused."""
-    _fields_ = [("program", c_int), ("nitems", c_int), ("src", c_ptr), ("out", c_ptr), ("slices", c_ptr),
-                ("exps", c_ptr), ("rows", c_i64), ("K", c_i64), ("sr", c_i64), ("sk", c_i64), ("batch", c_i64),
-                ("src_bs", c_i64), ("out_bs", c_i64), ("exp_bs", c_i64), ("nl", c_ptr), ("tau", c_dbl),
-                ("in_scale", c_dbl), ("flag", c_ptr), ("pos", c_u64), ("grid_barrier", c_ptr)]
-
-
-PRO_SLICE = -1
-
-
 class FftOps(ctypes.Structure):
     """cgl_fft_ops_t (include/cgl_b200.h): operands of a fused pencil-FFT pass."""
     _fields_ = [("u", c_ptr), ("u_out", c_ptr), ("g", c_ptr * 3), ("g_out", c_ptr), ("tables", (c_ptr * 3) * 2),
@@ -87,9 +76,6 @@ FFT_PROGRAMS = {"plain": 0, "if4_start": 1, "if4_b1": 2, "if4_b2": 3, "if4_b3": 
                 "str_start": 7, "str_a0": 8, "str_mid": 9}
 
 _SIGS = {
-    "cgl_oz_gemm_fused": (c_int, [c_ptr, c_int, c_i64, c_i64, c_i64, c_int, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
-                                  c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_u64, c_int,
-                                  ctypes.POINTER(OzPrologue)]),
     "cgl_version": (ctypes.c_char_p, []),
     "cgl_last_error": (ctypes.c_char_p, []),
     "cgl_abi_version": (c_int, []),

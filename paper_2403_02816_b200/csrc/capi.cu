@@ -36,11 +36,6 @@ int oz_gemm(cudaStream_t, int, int64_t, int64_t, int64_t, int, const int8_t* con
             const int8_t* const*, const int8_t* const*, const int* const*, const int8_t* const*, double* const*,
             int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const cgl_flag_t*, uint64_t, int);
 int oz_zmap(cudaStream_t, int, const int8_t*, int64_t, int64_t, int, int, int8_t*);
-struct RowsSliceArgs;
-int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-                  const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
-                  double* const* C, int64_t ldc, int64_t batch, int64_t sBb, int64_t sBeb, int64_t sCb,
-                  const cgl_flag_t* flag, uint64_t pos, int trans_c, const cgl_oz_prologue_t* pro);
 int oz_slice_multi(cudaStream_t, int, int, const double* const*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                    int, int8_t* const*, int64_t, int* const*, int64_t, int);
 int64_t oz_slice_bytes(int, int64_t, int64_t, int, int);
@@ -395,14 +390,6 @@ int cgl_oz_slice(void* stream, int S, const double* src, int64_t sr, int64_t sc,
                  int64_t exp_batch_stride) {
   return oz_slice((cudaStream_t)stream, S, src, sr, sc, rows, cols, batch, src_batch_stride, a_mode, a_mode ? kOzBM : kOzBN,
                   out, out_batch_stride, exps, exp_batch_stride);
-}
-
-int cgl_oz_gemm_fused(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-                      const int* const* Aexp, const int8_t* const* Azmap, const int8_t* const* B,
-                      const int* const* Bexp, double* const* C, int64_t ldc, int64_t batch, int64_t sB, int64_t sBexp,
-                      int64_t sC, const cgl_flag_t* flag, uint64_t pos, int trans_c, const cgl_oz_prologue_t* pro) {
-  return oz_gemm_fused((cudaStream_t)stream, S, M, N, K, nitems, A, Aexp, Azmap, B, Bexp, C, ldc, batch, sB, sBexp,
-                       sC, flag, pos, trans_c, pro);
 }
 
 int cgl_oz_gemm(void* stream, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,

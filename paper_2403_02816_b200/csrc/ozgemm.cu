@@ -597,12 +597,6 @@ struct OzArgs {
   int debug;         // CGL_OZ_DEBUG (timing experiments only; results invalid): 1 skip MMAs, 2 skip copies
   int m_fastest;     // tile order (persistent kernel): 1 = row tiles fastest (large data operands)
   OzItem items[kMaxItems];
-  // fused prologue (ozgemm_persistent_kernel<..., PRO != 0>): the data slicing
-  // (or stage program + slicing) that produces this GEMM's B operands, run by
-  // the epilogue warps as virtual 128-thread CTAs before one grid barrier
-  RowsSliceArgs pro;
-  int64_t pro_nvbx, pro_nvb;  // virtual CTAs: row blocks x (items x batch)
-  unsigned* gbar;             // grid barrier {count, generation}, zeroed once
 };
 
 __device__ __forceinline__ long long gtime() {
@@ -841,29 +835,6 @@ __global__ void __launch_bounds__(OZ_THREADS, (S * BN <= 256 ? 2 : 1)) ozgemm_ke
 }
 
 
-// Grid-wide barrier of a persistent launch (every CTA resident: one per SM).
-// bar[0] counts arrivals (reset by the last arriver), bar[1] is the
-// generation the waiters watch.  Generic writes before the barrier are made
-// visible to the async proxy (cp.async.bulk operand loads) after it.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
 // ---- persistent variant -------------------------------------------------------
 // One CTA per SM walks tiles t = blockIdx.x, +gridDim.x, ...; the S level
 // accumulators are double-buffered in TMEM (2 x S x BN <= 512 columns) so the
@@ -922,7 +893,7 @@ __device__ __forceinline__ TileId decode_tile(const OzArgs& a, uint32_t t) {
   return d;
 }
 
-template <int S, int BN, int STAGES, int PRO = 0, int PTPT = 1>
+template <int S, int BN, int STAGES>
 __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const OzArgs a, int64_t total) {
   CGL_PROF_SCOPE(KID_OZP);
   using Cfg = OzPCfg<S, BN, STAGES>;
@@ -956,8 +927,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     pre_zb = bz0 ? bz0[(int64_t)td0.tn * a.nchunks + lane] : 1;
   }
   if (warp == 0) {
-    // warp 0 (barrier init, then producer 0) never touches TMEM: with PRO == 0
-    // it starts the first tile's live-chunk list and copies right after the
+    // warp 0 (barrier init, then producer 0) never touches TMEM: it starts the first tile's live-chunk list and copies right after the
     // barrier init instead of waiting for the TMEM allocation and zeroing
     // (named barrier 1: warp 0 arrives, the other warps sync)
     if (lane < kMaxItems) sitems[lane] = a.items[lane];
@@ -978,11 +948,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     }
     __syncwarp();
     CGL_PROF_MARK(109);  // warp 0: barriers initialised
-    if constexpr (PRO == 0) {
-      asm volatile("bar.arrive 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
-    } else {
-      asm volatile("bar.sync 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
-    }
+    asm volatile("bar.arrive 1, %0;\n" ::"n"(OZP_THREADS) : "memory");
   } else {
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
@@ -1001,38 +967,11 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
   tc_fence_before();
-  if constexpr (PRO == 0) {
-    // zeroed accumulators -> the issuer's first MMA (warps 1 .. last; not warp 0)
-    if (warp != 0) asm volatile("bar.sync 2, %0;\n" ::"n"(OZP_THREADS - 32) : "memory");
-  } else {
-    __syncthreads();
-  }
+  // zeroed accumulators -> the issuer's first MMA (warps 1 .. last; not warp 0)
+  if (warp != 0) asm volatile("bar.sync 2, %0;\n" ::"n"(OZP_THREADS - 32) : "memory");
   tc_fence_after();
   if (threadIdx.x == 0) OZ_TRACE(1);
   if (warp == 1) CGL_PROF_MARK(101);  // setup done (TMEM ready)
-  if constexpr (PRO != 0) {
-    // ---- prologue phase: this GEMM's B operands (data slicing, optionally a
-    // stage program) by the 16 epilogue warps as four 128-thread groups, the
-    // smem ring as their scratch; then one grid barrier ----
-    constexpr int PNSL = PRO == P_SLICE ? 1 : (PRO == P_IF4_END ? 3 : ((PRO == P_IF4_MID || PRO == P_SPLIT4_END) ? 2 : 1));
-    static_assert(OZP_EPI_WARPS == 16 && Cfg::BODY >= 4 * (int)sizeof(RowsSliceSmem), "prologue groups");
-    pdl_wait();
-    if (warp == 0) CGL_PROF_MARK(110);  // pdl wait passed
-    if (warp >= 2 && warp < 2 + OZP_EPI_WARPS) {
-      const int g = (warp - 2) >> 2;
-      RowsSliceSmem* psm = reinterpret_cast<RowsSliceSmem*>(stage_base) + g;
-      int round = 0;
-      for (int64_t vb = g + 4 * (int64_t)blockIdx.x; vb < a.pro_nvb; vb += 4 * (int64_t)gridDim.x, ++round) {
-        if (!rows_slice_block<PRO, PNSL, PTPT>(a.pro, vb % a.pro_nvbx, vb / a.pro_nvbx, threadIdx.x - 64 - 128 * g,
-                                               1 + g, *psm))
-          break;
-        if (round < 2) CGL_PROF_MARK(111 + round);  // virtual CTA done
-      }
-      CGL_PROF_MARK(113);  // prologue work done (before the grid barrier)
-    }
-    grid_barrier(a.gbar);
-    if (warp == 0) CGL_PROF_MARK(102);  // prologue + grid barrier done
-  }
   // Everything above and the first tile's live-chunk list (constant zero maps)
   // overlap the previous kernel's tail under PDL; every role executes
   // griddepcontrol.wait before touching the data operand, its exponents or
@@ -1236,9 +1175,7 @@ __global__ void __launch_bounds__(OZP_THREADS, 1) ozgemm_persistent_kernel(const
       const int64_t i = R >> 1;
       const int ea = (i < a.M) ? __ldg(it.Ae + b * a.sAeb + i) : 0;
       const int64_t ccol = (int64_t)tn * BN + lane;
-      // (the prologue wrote Be in this launch: coherent L2 load)
-      const int eb_lane = (lane < BN && ccol < a.N) ? (PRO != 0 ? __ldcg(it.Be + b * a.sBeb + ccol)
-                                                                  : __ldg(it.Be + b * a.sBeb + ccol)) : 0;
+      const int eb_lane = (lane < BN && ccol < a.N) ? __ldg(it.Be + b * a.sBeb + ccol) : 0;
       mbar_wait_sleep(&acc_full[buf], (j >> 1) & 1, 32);
       tc_fence_after();
       if (j < 8 && threadIdx.x == 64) OZ_TRACE(19 + j);
@@ -1372,34 +1309,16 @@ int oz_slice_multi(cudaStream_t st, int S, int nitems, const double* const* srcs
   a.floor_digits = floor_digits;
   const int64_t zdim = batch * nitems;
   if (zdim > 65535) return set_error(CGL_ESHAPE, "oz_slice: batch x items too large");
-  // variants for A/B runs and tests: CGL_SS_CLUSTER=1 (cluster kernel),
-  // CGL_OZ_FUSED_SLICE=0 (two-pass rowexp + slice_tile)
+  // full-K rows kernel (stages.cu rows_slice_kernel: one CTA per QC whole rows, the row
+  // exponent a CTA-local reduction) for the data operands of the step plans; everything
+  // else (A-role slices of the constant factors, S != 8, K > 2048, doubly strided sources)
+  // takes the general two-pass path below.  CGL_OZ_FUSED_SLICE=0 sends every call there
+  // (the tests compare the two bit for bit).
   const char* ev_fused = getenv("CGL_OZ_FUSED_SLICE");
-  const char* ev_cluster = getenv("CGL_SS_CLUSTER");
-  const bool fuse_ok = !(ev_fused && ev_fused[0] == '0');
-  const bool rows_ok = fuse_ok && !(ev_cluster && ev_cluster[0] == '1');
+  const bool rows_ok = !(ev_fused && ev_fused[0] == '0');
   if (rows_ok && !a_mode && floor_digits && S == 8 && (sr == 1 || sc == 1) && rows_slice_ok(cols, false)) {
-    // full-K CTAs, no cluster (stages.cu rows_slice_kernel); row r of Z = operand row, K = cols
+    // row r of Z = operand row, K = cols
     return rows_slice_plain(st, nitems, srcs, sr, sc, rows, cols, batch, src_bs, outs, out_bs, exps, exp_bs);
-  }
-  if (fuse_ok && !a_mode && floor_digits && S == 8 && a.nchunks <= 64) {
-    // one cluster of <= 8 CTAs per row tile covers all K chunks
-    const int cpb = a.nchunks <= 32 ? 4 : 8;
-    const int cy = (a.nchunks + cpb - 1) / cpb;
-    const size_t smem = (size_t)kOzBN * (cpb * oz::KC / 2 + 1) * sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(oz::slice_tile_kernel<8, 0, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      cudaFuncSetAttribute(oz::slice_tile_kernel<8, 0, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      attr = true;
-    }
-    const dim3 grid((unsigned)a.rtiles, (unsigned)cy, (unsigned)zdim), cl(1, (unsigned)cy, 1);
-    cudaError_t e = cpb == 4 ? launch_k(oz::slice_tile_kernel<8, 0, 4, true>, grid, dim3(256), smem, st, cl, a, src_bs,
-                                        out_bs, exp_bs)
-                             : launch_k(oz::slice_tile_kernel<8, 0, 8, true>, grid, dim3(256), smem, st, cl, a, src_bs,
-                                        out_bs, exp_bs);
-    if (e != cudaSuccess) return set_cuda_error(e, "oz_slice (fused cluster launch)");
-    return check_launch("oz_slice_fused");
   }
   // pass 1: exponents
   if (sr == 1) {
@@ -1469,10 +1388,10 @@ static int oz_launch_cfg(oz::OzArgs& a, int nitems, cudaStream_t st) {
   return check_launch("ozgemm_kernel");
 }
 
-template <int S, int BN, int STAGES, int PRO = 0, int PTPT = 1>
+template <int S, int BN, int STAGES>
 static int oz_launch_persistent(oz::OzArgs& a, int nitems, cudaStream_t st) {
   using Cfg = oz::OzPCfg<S, BN, STAGES>;
-  auto kern = oz::ozgemm_persistent_kernel<S, BN, STAGES, PRO, PTPT>;
+  auto kern = oz::ozgemm_persistent_kernel<S, BN, STAGES>;
   static int nsm = 0;
   if (!nsm) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1531,13 +1450,9 @@ static int oz_args(oz::OzArgs& a, cudaStream_t st, int S, int64_t M, int64_t N, 
   for (int f = 0; f < nitems; ++f)
     a.items[f] = oz::OzItem{A[f], Ae[f], B[f], Be[f], reinterpret_cast<double2*>(C[f]), Az ? Az[f] : nullptr,
                             Bz ? Bz[f] : nullptr};
-  {
-    // CGL_OZ_MFAST=1: row tiles fastest (each B tile fetched from HBM once).
-    // Measured on C2/C4 (256^3 / 1024^3 products): no gain (C2 if4 5.82 ->
-    // 6.02 ms/step, C4 483 -> 487) -- off by default.
-    const char* e = getenv("CGL_OZ_MFAST");
-    a.m_fastest = e && e[0] == '1';
-  }
+  // tile order: column tiles fastest.  Row tiles fastest (each B tile fetched from HBM once)
+  // was measured on C2/C4 (256^3 / 1024^3 products): no gain (C2 if4 5.82 -> 6.02 ms/step).
+  a.m_fastest = 0;
   return 0;
 }
 
@@ -1550,115 +1465,15 @@ int oz_gemm(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems,
   int r = oz_args(a, st, S, M, N, K, nitems, A, Ae, Az, B, Be, Bz, C, ldc, batch, sAb, sAeb, sBb, sBeb, sCb, flag,
                   pos, trans_c);
   if (r) return r;
-  static const int persistent = [] {
-    const char* e = getenv("CGL_OZ_PERSISTENT");
-    return e ? atoi(e) : 1;
-  }();
-  if (persistent && S == 8 && a.nchunks <= oz::OzPCfg<8, BN, 4>::KMAXCH)
-    return oz_launch_persistent<8, BN, 4>(a, nitems, st);
+  // persistent TMEM-double-buffered kernel; the one-tile-per-CTA kernel serves S = 7 / 1 and
+  // K extents beyond its live-chunk list
+  if (S == 8 && a.nchunks <= oz::OzPCfg<8, BN, 4>::KMAXCH) return oz_launch_persistent<8, BN, 4>(a, nitems, st);
   switch (S) {
     case 7: return oz_launch_cfg<7, BN, 2>(a, nitems, st);
     case 8: return oz_launch_cfg<8, BN, 2>(a, nitems, st);
     case 1: return oz_launch_cfg<1, BN, 2>(a, nitems, st);
     default: return set_error(CGL_EINVAL, "oz_gemm: S must be 1, 7 or 8");
   }
-}
-
-// GEMM with its B operands produced in-kernel (prologue phase + grid
-// barrier): pro describes the slicing (PRO = P_SLICE: pro.batch x nitems
-// sources) or the stage program whose sliced outputs are the B operands.
-int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-                  const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
-                  double* const* C, int64_t ldc, int64_t batch, int64_t sBb, int64_t sBeb, int64_t sCb,
-                  const cgl_flag_t* flag, uint64_t pos, int trans_c, const RowsSliceArgs& pro, int prog,
-                  int pro_items, unsigned* gbar) {
-  constexpr int BN = kOzBN;
-  if (S != 8) return set_error(CGL_EINVAL, "oz_gemm_fused: S = 8 only");
-  if (!gbar) return set_error(CGL_EINVAL, "oz_gemm_fused: grid barrier buffer required");
-  oz::OzArgs a{};
-  int r = oz_args(a, st, S, M, N, K, nitems, A, Ae, Az, B, Be, nullptr, C, ldc, batch, 0, 0, sBb, sBeb, sCb, flag,
-                  pos, trans_c);
-  if (r) return r;
-  if (a.nchunks > oz::OzPCfg<8, BN, 4>::KMAXCH) return set_error(CGL_ESHAPE, "oz_gemm_fused: K too large");
-  a.pro = pro;
-  const int64_t gy = prog == P_SLICE ? pro.batch * pro_items : 1;
-  int tpt = 1;
-  a.pro.QC = rows_slice_qc(pro.K, pro.rows * gy, 2, &tpt);
-  if (tpt > 2) return set_error(CGL_ESHAPE, "oz_gemm_fused: prologue K extent too large");
-  a.pro_nvbx = (pro.rows + a.pro.QC - 1) / a.pro.QC;
-  a.pro_nvb = a.pro_nvbx * gy;
-  a.gbar = gbar;
-#define OZF(P_) (tpt == 1 ? oz_launch_persistent<8, BN, 4, P_, 1>(a, nitems, st) \
-                          : oz_launch_persistent<8, BN, 4, P_, 2>(a, nitems, st))
-  switch (prog) {
-    case P_SLICE: return OZF(P_SLICE);
-    case P_IF4_MID: return OZF(P_IF4_MID);
-    case P_IF4_END: return OZF(P_IF4_END);
-    case P_STRANG_END: return OZF(P_STRANG_END);
-    case P_SPLIT4_MID: return OZF(P_SPLIT4_MID);
-    case P_SPLIT4_END: return OZF(P_SPLIT4_END);
-    default: return set_error(CGL_EINVAL, "oz_gemm_fused: unknown prologue program");
-  }
-#undef OZF
-}
-
-int oz_gemm_fused(cudaStream_t st, int S, int64_t M, int64_t N, int64_t K, int nitems, const int8_t* const* A,
-                  const int* const* Ae, const int8_t* const* Az, const int8_t* const* B, const int* const* Be,
-                  double* const* C, int64_t ldc, int64_t batch, int64_t sBb, int64_t sBeb, int64_t sCb,
-                  const cgl_flag_t* flag, uint64_t pos, int trans_c, const cgl_oz_prologue_t* p) {
-  if (!p) return set_error(CGL_EINVAL, "oz_gemm_fused: prologue required");
-  RowsSliceArgs R{};
-  int prog, items = 1;
-  if (p->program == CGL_PRO_SLICE) {
-    prog = P_SLICE;
-    items = p->nitems;
-    if (items < 1 || items > 8) return set_error(CGL_EINVAL, "oz_gemm_fused: 1..8 slicing sources");
-    for (int f = 0; f < items; ++f) {
-      R.srcs[f] = reinterpret_cast<const double2*>(p->src[f]);
-      R.slices[f] = p->slices[f];
-      R.exps[f] = p->exps[f];
-    }
-    R.batch = p->batch;
-    R.src_bs = p->src_bs;
-    R.out_bs = p->out_bs;
-    R.exp_bs = p->exp_bs;
-  } else {
-    int nin, nsl, nout;
-    switch (p->program) {
-      case P_IF4_MID: nin = 2; nsl = 2; nout = 0; break;
-      case P_IF4_END: nin = 4; nsl = 3; nout = 1; break;
-      case P_STRANG_END: nin = 1; nsl = 1; nout = 1; break;
-      case P_SPLIT4_MID: nin = 2; nsl = 1; nout = 1; break;
-      case P_SPLIT4_END: nin = 2; nsl = 2; nout = 1; break;
-      default: return set_error(CGL_EINVAL, "oz_gemm_fused: stage program must be if4 MID/END, strang END, split4 MID/END");
-    }
-    if (!p->nl || p->nl->kind >= 2) return set_error(CGL_EINVAL, "oz_gemm_fused: single-component nonlinearity required");
-    if (nout && (!p->out || !p->out[0])) return set_error(CGL_EINVAL, "oz_gemm_fused: program writes an FP64 output");
-    prog = p->program;
-    StageArgs& a = R.s;
-    for (int k = 0; k < nin; ++k) a.in[k] = reinterpret_cast<const double2*>(p->src[k]);
-    if (nout) a.out[0] = reinterpret_cast<double2*>(p->out[0]);
-    a.n = p->rows * p->K;
-    a.tau = p->tau;
-    a.in_scale = p->in_scale;
-    a.nl = StageNL{p->nl->alpha3, p->nl->beta3, p->nl->alpha4, p->nl->beta4, p->nl->alpha5, p->nl->kind};
-    a.flag = p->flag;
-    a.pos = p->pos;
-    a.fw = 1;
-    for (int q = 0; q < nsl; ++q) {
-      R.slices[q] = p->slices[q];
-      R.exps[q] = p->exps[q];
-    }
-    R.batch = 1;
-  }
-  R.rows = p->rows;
-  R.K = p->K;
-  R.sr = p->sr;
-  R.sk = p->sk;
-  R.nchunks = (int)((2 * p->K + oz::KC - 1) / oz::KC);
-  if (R.nchunks != (int)((2 * K + oz::KC - 1) / oz::KC)) return set_error(CGL_ESHAPE, "oz_gemm_fused: prologue K != GEMM K");
-  return oz_gemm_fused(st, S, M, N, K, nitems, A, Ae, Az, B, Be, C, ldc, batch, sBb, sBeb, sCb, flag, pos, trans_c, R,
-                       prog, items, p->grid_barrier);
 }
 
 int oz_zmap(cudaStream_t st, int S, const int8_t* slices, int64_t rows, int64_t cols, int a_mode, int RT, int8_t* z) {

@@ -40,7 +40,6 @@ struct RowsSliceArgs {
   int64_t rows, K;          // operand rows R, complex K extent
   int64_t sr, sk;           // element (R, k) at R * sr + k * sk
   int nchunks, QC;
-  int debug;  // CGL_RS_DEBUG (timing experiments only; results invalid): 1 no digits, 2 no stores, 4 no loads
 };
 
 // Shared-memory scratch of one 128-thread group.
@@ -70,7 +69,7 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
   using oz::NONFINITE;
   constexpr int NO = PROG == P_SLICE ? 1 : NSL;  // sliced outputs per task
   constexpr int NIN = PROG == P_SLICE ? 1
-                      : (PROG == P_IF4_END ? 4 : (PROG == P_STRANG_END ? 1 : (PROG == P_IF4_MIDH ? 3 : 2)));
+                      : (PROG == P_IF4_END ? 4 : (PROG == P_STRANG_END ? 1 : 2));
   const StageArgs& a = A.s;
   const int lane = tid & 31, wid = tid >> 5;
   const int QC = A.QC, lqc = __ffs(QC) - 1;  // QC is a power of two
@@ -162,27 +161,6 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
         *dout = out.c[0];
         o[j][0][p] = out.c[0];                                   // u
         o[j][NO > 1 ? 1 : 0][p] = gfun<1>(a.nl, out).c[0];       // g1 of the next step
-      } else if (PROG == P_IF4_MIDH) {
-        V<1> u2, av, w;
-        u2.c[0] = cscale(sc, in[0][p]);
-        av.c[0] = cscale(sc, in[NIN > 1 ? 1 : 0][p]);
-        w.c[0] = cscale(sc, in[NIN > 2 ? 2 : 0][p]);
-        const V<1> g2 = gfun<1>(a.nl, u2);
-        const V<1> g3 = gfun<1>(a.nl, axpy<1>(0.5 * t, g2, av));
-        const V<1> sv = axpy<1>(1.0, g2, g3);
-        o[j][0][p] = axpy<1>(t, g3, av).c[0];                 // p = a + t g3
-        o[j][NO > 1 ? 1 : 0][p] = axpy<1>(t / 3.0, sv, w).c[0];  // r = w + t/3 s
-      } else if (PROG == P_IF4_ENDH) {
-        V<1> u4, q;
-        u4.c[0] = cscale(sc, in[0][p]);
-        q.c[0] = cscale(sc, in[NIN > 1 ? 1 : 0][p]);
-        const V<1> out = axpy<1>(t / 6.0, gfun<1>(a.nl, u4), q);
-        if (!finite_all<1>(out)) note(key, check_pos, CGL_NONFINITE_STATE);
-        *dout = out.c[0];
-        const V<1> g1 = gfun<1>(a.nl, out);
-        o[j][0][p] = axpy<1>(0.5 * t, g1, out).c[0];   // X1
-        o[j][NO > 1 ? 1 : 0][p] = out.c[0];             // u
-        o[j][NO > 2 ? 2 : 0][p] = axpy<1>(t / 6.0, g1, out).c[0];  // X5
       } else if (PROG == P_IF4_MID) {
         V<1> u2, av;
         u2.c[0] = cscale(sc, in[0][p]);
@@ -310,7 +288,7 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
       for (int s8 = 0; s8 < 8; ++s8)
 #pragma unroll
         for (int k = 0; k < NW; ++k) wv[s8][k] = 0u;
-      if (e != NONFINITE && !(A.debug & 1)) {
+      if (e != NONFINITE) {
         const double2 s2p = oz::pow2_split(e);
         if (e >= -940) {  // uniform per row: one scaling factor, no subnormal checks
 #pragma unroll
@@ -336,7 +314,7 @@ __device__ __forceinline__ bool rows_slice_block(const RowsSliceArgs& A, int64_t
       }
       int8_t* base = PROG == P_SLICE ? A.slices[item] + bb * A.out_bs : A.slices[q];
       int8_t* dst = base + oz::tile_offset(R, 2 * PP * g, kOzBN, A.nchunks, 8);
-      if (!(A.debug & 2)) {
+      {
 #pragma unroll
         for (int s8 = 0; s8 < 8; ++s8) {
           if constexpr (PP == 8)

@@ -218,13 +218,8 @@ enum Prog {
   P_IF2_PRE, P_IF2_END,
   // Fourier (spectral-space) programs; g / flows run in physical space between cuFFT calls
   P_FIF4_S1, P_FIF4_S2, P_FIF4_S3, P_FIF4_S4, P_FLOW_END,
-  // if4 on the semigroup form E1 = E1/2 E1/2 (stage kernels and cgl_stage_slice):
-  //   [u2, a, w] = E1/2 [X1, u, X5]
-  //   MIDH: g2 = g(u2); u3 = a + t/2 g2; g3 = g(u3); s = g2 + g3;  p = a + t g3; r = w + t/3 s
-  //   [u4, q] = E1/2 [p, r]          (u4 = E1 u + t E1/2 g3,  q = E1 X5 + t/3 E1/2 s)
-  //   ENDH: g4 = g(u4); out = q + t/6 g4; check; X1 = out + t/2 g(out), X5 = out + t/6 g(out)
-  P_IF4_MIDH = 15, P_IF4_ENDH = 16,
-  // ... and with linearity on top (E1/2 X1 = E1/2 u + t/2 E1/2 g1, same for X5):
+  // if4 by the semigroup property E1 = E1/2 E1/2 and linearity (E1/2 X1 = E1/2 u + t/2 E1/2 g1,
+  // same for X5); ids 15, 16 are retired (an intermediate five-Tucker form):
   //   [A, G] = E1/2 [u, g1]
   //   MIDQ: u2 = A + t/2 G, w = A + t/6 G; g2 = g(u2); u3 = A + t/2 g2; g3 = g(u3); s = g2 + g3;
   //         p = A + t g3; r = w + t/3 s

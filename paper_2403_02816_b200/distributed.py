@@ -208,7 +208,7 @@ class ShardedPlan(FusedPlan):
         while len(self.W) < 2 * self.nf:
             self.W.append(torch.empty_like(like[0]))
 
-    def _tucker(self, jobs, flag, pre0=None, pro0=None):
+    def _tucker(self, jobs, flag, pre0=None):
         if self.use_oz:
             items = []
             for f, fin, fout in jobs:

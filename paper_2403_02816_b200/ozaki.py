@@ -75,13 +75,6 @@ class Workspace:
 
     def __init__(self):
         self.bufs = {}
-        self._gbar = None
-
-    def gbar(self, device):
-        """Grid-barrier buffer of the fused producer+product launches (zeroed once)."""
-        if self._gbar is None:
-            self._gbar = torch.zeros(2, dtype=torch.int32, device=device)
-        return self._gbar
 
     def get(self, key, nbytes, nexp, device):
         b = self.bufs.get(key)
@@ -116,69 +109,7 @@ def _chunks(total, per_unit, nf, align=128):
     return [(a, min(total, a + units)) for a in range(0, total, units)]
 
 
-def fuse_enabled():
-    """Producer phases (data slicing, stage programs) inside the GEMM launch
-    (cgl_oz_gemm_fused) with CGL_OZ_FUSE=1.  Off by default: measured slower
-    on C1 (0.147 vs 0.116 ms per if4 step) -- the prologue runs as 4 x 148
-    register-capped 128-thread groups in ~2 rounds of the ~5 us per-row-block
-    latency chain, where the standalone kernel has every row block in flight."""
-    return os.environ.get("CGL_OZ_FUSE", "0") == "1"
-
-
-class StagePrologue:
-    """A stage program (cgl_stage_slice semantics) to run as the producer
-    phase of the next axis-0 product: its sliced outputs are that product's
-    data operands (presliced)."""
-
-    def __init__(self, program, ins, out, nl, tau, pos, in_scale=1.0):
-        self.program, self.ins, self.out, self.nl = program, ins, out, nl
-        self.tau, self.pos, self.in_scale = tau, pos, in_scale
-
-
-def _gemm_fused(lib, st, n, N, nf, Aa, Ae, Az, Bs, Be, dsts, ldc, flag, pos, trans_c, pro, keep):
-    """One cgl_oz_gemm_fused launch (single batch); `keep` holds the ctypes
-    arrays the prologue struct points to until the call returns."""
-    _lib.check(lib.cgl_oz_gemm_fused(st, S, n, N, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
-                                     _lib.ptr_array(dsts), ldc, 1, 0, 0, 0, _lib.flag_ptr(flag), pos, trans_c,
-                                     _lib.ctypes.byref(pro)), "oz_gemm_fused")
-    del keep
-
-
-def _slice_prologue(srcs, outs_b, exps_b, rows, K, sr, sk, gbar):
-    arrs = (_lib.ptr_array(srcs), _lib.ptr_array(outs_b), _lib.ptr_array(exps_b))
-    pro = _lib.OzPrologue()
-    pro.program = _lib.PRO_SLICE
-    pro.nitems = len(srcs)
-    pro.src = _lib.ctypes.cast(arrs[0], _lib.c_ptr)
-    pro.slices = _lib.ctypes.cast(arrs[1], _lib.c_ptr)
-    pro.exps = _lib.ctypes.cast(arrs[2], _lib.c_ptr)
-    pro.rows, pro.K, pro.sr, pro.sk = rows, K, sr, sk
-    pro.batch = 1
-    pro.grid_barrier = gbar.data_ptr()
-    return pro, arrs
-
-
-def _stage_prologue(sp, slots, n0, Q, flag, gbar):
-    arrs = (_lib.ptr_array(sp.ins), _lib.ptr_array([sp.out]) if sp.out is not None else None,
-            _lib.ptr_array([t[0] for t in slots]), _lib.ptr_array([t[1] for t in slots]))
-    pro = _lib.OzPrologue()
-    pro.program = _lib.STAGE[sp.program]
-    pro.nitems = 1
-    pro.src = _lib.ctypes.cast(arrs[0], _lib.c_ptr)
-    pro.out = _lib.ctypes.cast(arrs[1], _lib.c_ptr) if arrs[1] is not None else None
-    pro.slices = _lib.ctypes.cast(arrs[2], _lib.c_ptr)
-    pro.exps = _lib.ctypes.cast(arrs[3], _lib.c_ptr)
-    pro.rows, pro.K, pro.sr, pro.sk = Q, n0, 1, Q
-    pro.batch = 1
-    pro.nl = _lib.ctypes.cast(_lib.ctypes.pointer(sp.nl), _lib.c_ptr)
-    pro.tau, pro.in_scale = sp.tau, sp.in_scale
-    pro.flag = flag.data_ptr() if flag is not None else None
-    pro.pos = sp.pos
-    pro.grid_barrier = gbar.data_ptr()
-    return pro, arrs
-
-
-def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=None, prologue=None):
+def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=None):
     """outs[f] = ins[f] x_axis E_f for square E_f (SlicedFactor), one GEMM
     launch per chunk (one chunk unless the data slices would exceed
     CHUNK_BYTES, e.g. 1024^3 fields).  presliced (first axis only): per item
@@ -226,15 +157,6 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=No
                                        _lib.flag_ptr(flag), pos), "oz_gemm(middle)")
     elif Q > 1 and presliced is not None:
         Bs, Be = [p_[0] for p_ in presliced], [p_[1] for p_ in presliced]
-        if prologue is not None:
-            # the stage program producing the presliced operands runs inside this launch
-            uniq_sl = []
-            for t in presliced:
-                if all(t[0].data_ptr() != u[0].data_ptr() for u in uniq_sl):
-                    uniq_sl.append(t)
-            pro, keep = _stage_prologue(prologue, uniq_sl, n, Q, flag, ws.gbar(dev))
-            _gemm_fused(lib, st, n, Q, nf, Aa, Ae, Az, Bs, Be, outs, Q, flag, pos, 0, pro, (keep, pro))
-            return outs
         _lib.check(lib.cgl_oz_gemm(st, S, n, Q, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
                                    None, _lib.ptr_array(outs), Q, 1, 0, 0, 0, 0, 0,
                                    _lib.flag_ptr(flag), pos), "oz_gemm(first, presliced)")
@@ -252,10 +174,6 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=No
             Bs, Be = [Bu[k] for k in idx], [Beu[k] for k in idx]
             srcs = [x.view(-1)[q0:] for x in uniq]
             dsts = [o.view(-1)[q0:] for o in outs]
-            if fuse_enabled() and n <= 1024:
-                pro, keep = _slice_prologue(srcs, Bu, Beu, nq, n, 1, Q, ws.gbar(dev))
-                _gemm_fused(lib, st, n, nq, nf, Aa, Ae, Az, Bs, Be, dsts, Q, flag, pos, 0, pro, (keep, pro))
-                continue
             _lib.check(lib.cgl_oz_slice_multi(st, S, nu, _lib.ptr_array(srcs), 1, Q, nq, n, 1, 0, 0,
                                               _lib.ptr_array(Bu), 0, _lib.ptr_array(Beu), 0), "oz_slice(data, B)")
             _lib.check(lib.cgl_oz_gemm(st, S, n, nq, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
@@ -276,10 +194,6 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=No
             Bs, Be = [Bu[k] for k in idx], [Beu[k] for k in idx]
             srcs = [x.view(-1)[p0 * n:] for x in uniq]
             dsts = [o.view(-1)[p0 * n:] for o in outs]
-            if fuse_enabled() and n <= 1024:
-                pro, keep = _slice_prologue(srcs, Bu, Beu, np_, n, n, 1, ws.gbar(dev))
-                _gemm_fused(lib, st, n, np_, nf, Aa, Ae, Az, Bs, Be, dsts, n, flag, pos, 1, pro, (keep, pro))
-                continue
             _lib.check(lib.cgl_oz_slice_multi(st, S, nu, _lib.ptr_array(srcs), n, 1, np_, n, 1, 0, 0,
                                               _lib.ptr_array(Bu), 0, _lib.ptr_array(Beu), 0), "oz_slice(data, Bt)")
             _lib.check(lib.cgl_oz_gemm_t(st, S, n, np_, n, nf, Aa, Ae, Az, _lib.ptr_array(Bs), _lib.ptr_array(Be),
@@ -288,7 +202,7 @@ def mode_product_oz(ins, factors, outs, axis, ws, flag=None, pos=0, presliced=No
     return outs
 
 
-def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0, pre0=None, pro0=None):
+def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0, pre0=None):
     """Tucker chains of up to 8 fields, one emulated GEMM launch per mode
     (same mode order and ping-pong as cgl_tucker); `ws` is the caller's
     Workspace (per plan: captured graphs keep its pointers)."""
@@ -298,7 +212,7 @@ def tucker_oz(ins, factor_sets, outs, work, ws, flag=None, pos=0, pre0=None, pro
         to_out = (nd - axis) % 2 == 1
         dst = outs if to_out else work
         mode_product_oz(src, [fs[axis] for fs in factor_sets], dst, axis, ws, flag=flag, pos=pos,
-                        presliced=pre0 if axis == 0 else None, prologue=pro0 if axis == 0 else None)
+                        presliced=pre0 if axis == 0 else None)
         src = dst
     return outs
 

@@ -107,8 +107,6 @@ class FusedPlan:
         self._pos = _lib.rel_pos(1)
         self._k_base = 0               # host copy of the flag's step base
         self._flag0 = self.flag.clone()
-        self._pending_end = None       # deferred end-of-step program (ozaki.StagePrologue)
-        self._defer_end = False        # a next step follows in the same chunk
         self.graph_launches = {}       # cgl kernels inside each captured graph
         self.replayed_launches = 0     # cgl kernels launched by graph replays (not seen by the C counter)
 
@@ -146,25 +144,18 @@ class FusedPlan:
                                        _lib.ptr_array([t[1] for t in slots])), "cgl_stage_slice")
 
     def _end_stage(self, name, ins, out, slots, flag, tau):
-        """The end-of-step stage+slicing program of step k: deferred into the
-        next step's first axis-0 product launch (its producer phase,
-        cgl_oz_gemm_fused) when a next step follows in the same chunk, else
-        launched on its own (chunk boundary: the state must be complete)."""
-        if self._defer_end and self._fuse_pro():
-            from .ozaki import StagePrologue
-            self._pending_end = StagePrologue(name, [t for fs in ins for t in fs], out, self.nl, tau, self._pos)
-            return
+        """The end-of-step stage+slicing program of step k."""
         self._stage_slice(name, ins, [[out]] if out is not None else [], slots, flag, tau)
 
     def _if4_form(self):
         """if4 step form: "quad" (default: [A, G] = E1/2 [u, g1], four half-step
-        Tuckers), "half" (E1 = E1/2 E1/2, five), "ref" (the reference's six;
-        also CGL_IF4_HALF=0).  The producer-fusion path keeps "ref"."""
-        f = os.environ.get("CGL_IF4_FORM")
-        if f is None:
-            f = "ref" if os.environ.get("CGL_IF4_HALF", "1") == "0" else "quad"
-        if f not in ("quad", "half", "ref"):
-            raise ValueError(f"CGL_IF4_FORM must be quad, half or ref, not {f!r}")
+        Tuckers of two fields by the semigroup property and linearity) or "ref"
+        (CGL_IF4_FORM=ref: the reference's own six Tuckers, integrators.py:
+        205-215 literally -- the cross-check of the quad form in the tests and
+        in tools/parity_report.py)."""
+        f = os.environ.get("CGL_IF4_FORM", "quad")
+        if f not in ("quad", "ref"):
+            raise ValueError(f"CGL_IF4_FORM must be quad or ref, not {f!r}")
         return f
 
     def _ensure_oz(self):
@@ -173,15 +164,7 @@ class FusedPlan:
             self.use_oz = ozaki.enabled() and ozaki.fits(self.shape, 4 * self.nf)
         return self.use_oz
 
-    def _fuse_pro(self):
-        from . import ozaki
-        return ozaki.fuse_enabled() and type(self) is FusedPlan and self._fused_slices() is not None
-
-    def _take_pending(self):
-        p, self._pending_end = self._pending_end, None
-        return p
-
-    def _tucker(self, jobs, flag, pre0=None, pro0=None):
+    def _tucker(self, jobs, flag, pre0=None):
         """jobs: [(fraction, in_fields, out_fields)] -> one GEMM launch per mode
         (lean mode: one job at a time through the single scratch field).
         Products run on the INT8 tensor cores (ozaki.py) unless CGL_GEMM=dmma
@@ -206,10 +189,9 @@ class FusedPlan:
             for i in range(0, len(ins), 8):
                 sl = slice(i, i + 8)
                 ozaki.tucker_oz(ins[sl], facs[sl], outs[sl], work[sl] if work else None, self.oz_ws, flag=flag,
-                                pos=self._pos, pre0=pre0[sl] if pre0 is not None else None,
-                                pro0=pro0 if i == 0 else None)
+                                pos=self._pos, pre0=pre0[sl] if pre0 is not None else None)
             return
-        assert pre0 is None and pro0 is None, "pre-sliced operands need the INT8-emulated products"
+        assert pre0 is None, "pre-sliced operands need the INT8-emulated products"
         if self._tucker2d_ok():
             self._tucker2d(jobs, flag)
             return
@@ -304,38 +286,16 @@ class FusedPlan:
             self._tucker([(H, A, B[4]), (H, G, B[5])], flag, pre0=[F[3], F[4]])   # u4 -> B4, q -> B5
             self._before_end(flag)
             self._stage_slice("if4_endq", [B[4], B[5]], [u], [F[0], F[1]], flag, tau)
-        elif (self.scheme == "if4" and self._fused_slices() is not None and self._if4_form() == "half"):
-            # semigroup form E1 = E1/2 E1/2 (parity headroom covers it):
-            # [u2, a, w] = E1/2 [X1, u, X5]; MIDH -> p = a + t g3, r = w + t/3 s;
-            # [u4, q] = E1/2 [p, r]; ENDH -> out = q + t/6 g(u4).  Five half-step
-            # Tuckers per step instead of four half + two full ones.
-            u = self.U[0]
-            x1, x5, u2, a, b, c = B
-            F = self._fs
-            self._tucker([(H, x1, u2), (H, u, a), (H, x5, b)], flag,
-                         pre0=None if k == 1 else [F[0], F[1], F[2]])
-            self._stage_slice("if4_midh", [u2, a, b], [], [F[3], F[4]], flag, tau)
-            self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])     # u4 -> x1, q -> x5
-            self._before_end(flag)
-            self._stage_slice("if4_endh", [x1, x5], [u], [F[0], F[1], F[2]], flag, tau)
         elif self.scheme == "if4" and self._fused_slices() is not None:
-            # X1, u, X5 (after step k-1) and g3, s reach their products only as
-            # slices made by the fused stage kernels; step 1 slices the prologue's X1, X5.
-            # With producer fusion (cgl_oz_gemm_fused) MID runs inside the launch of
-            # the product it feeds, and END inside the next step's first product.
+            # reference form: X1, u, X5 (after step k-1) and g3, s reach their products
+            # only as slices made by the fused stage kernels; step 1 slices the prologue's X1, X5
             u = self.U[0]
             x1, x5, u2, a, b, c = B
             F = self._fs
-            fuse = self._fuse_pro()
             self._tucker([(H, x1, u2), (H, u, a), (O, u, b), (O, x5, c)], flag,
-                         pre0=None if k == 1 else [F[0], F[1], F[1], F[2]], pro0=self._take_pending())
-            if fuse:
-                from .ozaki import StagePrologue
-                mid = StagePrologue("if4_mid", [u2[0], a[0]], None, self.nl, tau, self._pos)
-                self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]], pro0=mid)
-            else:
-                self._stage_slice("if4_mid", [u2, a], [], [F[3], F[4]], flag, tau)
-                self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
+                         pre0=None if k == 1 else [F[0], F[1], F[1], F[2]])
+            self._stage_slice("if4_mid", [u2, a], [], [F[3], F[4]], flag, tau)
+            self._tucker([(H, u2, x1), (H, a, x5)], flag, pre0=[F[3], F[4]])
             self._before_end(flag)
             self._end_stage("if4_end", [b, c, x1, x5], u[0], [F[0], F[1], F[2]], flag, tau)
         elif self.scheme == "if4" and self._if4_form() == "quad":
@@ -346,15 +306,6 @@ class FusedPlan:
             self._tucker([(H, A, u4), (H, G, q)], flag)
             self._before_end(flag)
             self._stage("if4_endq", [u4, q], [u, g1], flag, tau)
-        elif self.scheme == "if4" and self._if4_form() == "half":
-            # semigroup form without fused slicing (lean 1024^3 plans, DMMA grids)
-            u = self.U[0]
-            x1, x5, u2, a, b, c = B
-            self._tucker([(H, x1, u2), (H, u, a), (H, x5, b)], flag)
-            self._stage("if4_midh", [u2, a, b], [u2, a], flag, tau)        # p -> u2, r -> a
-            self._tucker([(H, u2, x1), (H, a, x5)], flag)                  # u4 -> x1, q -> x5
-            self._before_end(flag)
-            self._stage("if4_endh", [x1, x5], [u, x1, x5], flag, tau)
         elif self.scheme == "if4":
             u = self.U[0]
             x1, x5, u2, a, b, c = B
@@ -373,7 +324,7 @@ class FusedPlan:
             # v (= flow of the previous state) reaches its product only as slices
             v, w = B
             F = self._fs
-            self._tucker([(O, v, w)], flag, pre0=None if k == 1 else [F[0]], pro0=self._take_pending())
+            self._tucker([(O, v, w)], flag, pre0=None if k == 1 else [F[0]])
             self._before_end(flag)
             self._end_stage("strang_end", [w], self.state_after(k)[0], [F[0]], flag, tau)
         elif self.scheme == "split4" and self._fused_slices() is not None:
@@ -381,15 +332,9 @@ class FusedPlan:
             # reach their products only as slices (slots 0, 1 and 2)
             v, f, v2, f2 = B
             F = self._fs
-            self._tucker([(O, v, v2), (H, f, f2)], flag, pre0=None if k == 1 else [F[0], F[1]],
-                         pro0=self._take_pending())
-            if self._fuse_pro():
-                from .ozaki import StagePrologue
-                mid = StagePrologue("split4_mid", [v2[0], f2[0]], v2[0], self.nl, tau, self._pos)
-                self._tucker([(H, f2, v)], flag, pre0=[F[2]], pro0=mid)          # coarse c -> v2; f3 -> v
-            else:
-                self._stage_slice("split4_mid", [v2, f2], [v2], [F[2]], flag, tau)   # coarse c -> v2 (FP64)
-                self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
+            self._tucker([(O, v, v2), (H, f, f2)], flag, pre0=None if k == 1 else [F[0], F[1]])
+            self._stage_slice("split4_mid", [v2, f2], [v2], [F[2]], flag, tau)   # coarse c -> v2 (FP64)
+            self._tucker([(H, f2, v)], flag, pre0=[F[2]])                        # f3 -> v
             self._before_end(flag)
             self._end_stage("split4_end", [v, v2], self.state_after(k)[0], [F[0], F[1]], flag, tau)
         elif self.scheme == "strang" and self.nf == 1 and self.nl.kind != 2 and not self.three \
@@ -431,9 +376,7 @@ class FusedPlan:
                 with torch.cuda.stream(s):
                     with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                         for j in range(count):
-                            self._defer_end = j < count - 1
                             self.step(k0 + j, flag, tau)
-                        self._defer_end = False
                         _lib.flag_advance(flag, count)
             finally:
                 if was:
@@ -450,8 +393,6 @@ class FusedPlan:
         flag.copy_(self._flag0)
         self._k_base = 0
         self._pos = _lib.rel_pos(1)
-        self._pending_end = None
-        self._defer_end = False
         # captured graphs bake tau and the prepared operator factors (pointers):
         # drop them when either changed since the capture (a re-prepared
         # operator rebuilds its cache dict; holding the old dicts keeps their
@@ -482,9 +423,7 @@ class FusedPlan:
                 count = 1  # step 1 (its products slice the prologue's fields) runs eagerly
             if eager_first:
                 for j in range(count):
-                    self._defer_end = j < count - 1
                     self.step(k + j, flag, tau)
-                self._defer_end = False
                 _lib.flag_advance(flag, count)
                 eager_first = False
             else:
