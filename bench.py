@@ -339,13 +339,14 @@ def fourier_roofline(torch, w, scheme, step_seconds):
     d = passes[dom]
     step_bytes = FOURIER_BYTES.get(scheme, 0) * n
     # DRAM bytes per launch of the dominant program from the ncu --set full capture of this
-    # round at 512^3 (profiles/r02c_fft_passes.txt: dram__bytes_read.sum + dram__bytes_write.sum)
-    traffic = {"if4": 2.147515e9 + 2.534077e9, "strang": 2.149681e9 + 4.291060e9}.get(scheme) \
+    # round at 512^3 (if4: fft_r32_kernel, profiles/r02e_fft_r32.txt; strang: profiles/r02c_fft_passes.txt;
+    # dram__bytes_read.sum + dram__bytes_write.sum)
+    traffic = {"if4": 2.147565e9 + 2.119455e9, "strang": 2.149681e9 + 4.291060e9}.get(scheme) \
         if tuple(w.extents) == (512, 512, 512) else None
     return {"bound": "hbm", "achieved": d["gbs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
             "traffic": traffic,
             "kernel": f"cgl::fftp::fft_*_kernel, dominant program: {dom} (largest share of the step in "
-                      "profiles/r02_launches_C3_if4.txt / _strang.txt)",
+                      "profiles/r02f_launches_C3_if4.txt / _strang.txt: the largest single kernel instantiation; the 8 plain axis-1 passes together are 34 % at 0.80 of the peak)",
             "algorithmic_bytes_per_launch": d["bytes_per_point"] * n, "per_launch_ms": d["ms"], "peak_source": src,
             "passes": passes,
             "step_level": {"algorithmic_bytes_per_step": step_bytes,
@@ -454,7 +455,9 @@ def gpu_arm(args, w, scheme):
     x_pinned = x0.cpu().pin_memory()
     P.integrate(prob, scheme, (x_pinned,), w.t_final, w.steps)
     e2e_total = 0.0
+    r2 = None
     for _ in range(args.steps):
+        r2 = None  # the previous result's page-locked block goes back to torch's host cache
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
