@@ -308,7 +308,7 @@ def fourier_roofline(torch, w, scheme, step_seconds):
     T0 = fftpass.fftn(0.1 * x)  # coefficients of an O(0.1) field, as in C3
     T = T0.clone()
     u = x.clone()
-    gs = [x.clone() for _ in range(3)]
+    gs = [x.clone()]   # the accumulated Lawson combination
     reps = 10
     copy_dt = _time(torch, _graphed(torch, lambda: [T.copy_(T0) for _ in range(reps)]), reps=3) / reps
 
@@ -319,9 +319,9 @@ def fourier_roofline(torch, w, scheme, step_seconds):
         progs = {"g (axis 0: F^-1, g, F)": (lambda: plan._pass("g", 0, T, T, w.tau, scale=1.0 / n), 32, 4),
                  "plain axis 1": (lambda: plan._pass("plain", 1, T, T, w.tau), 32, 8),
                  "if4_b1 (axis 2)": (lambda: plan._pass("if4_b1", last, T, T, w.tau, u=u, g_out=gs[0]), 64, 1),
-                 "if4_b3 (axis 2)": (lambda: plan._pass("if4_b3", last, T, T, w.tau, u=u, g_out=gs[2]), 64, 2),
-                 "if4_b4 (axis 2)": (lambda: plan._pass("if4_b4", last, T, T, w.tau, u=u, u_out=u, g=tuple(gs)),
-                                     112, 1)}
+                 "if4_b3 (axis 2)": (lambda: plan._pass("if4_b3", last, T, T, w.tau, u=u, g=(gs[0], None, None),
+                                                        g_out=gs[0]), 80, 2),
+                 "if4_b4 (axis 2)": (lambda: plan._pass("if4_b4", last, T, T, w.tau, u=gs[0], u_out=u), 64, 1)}
         dom = "g (axis 0: F^-1, g, F)"
     else:
         y = x.clone()

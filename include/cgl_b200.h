@@ -340,11 +340,14 @@ int cgl_fft_destroy(void* plan);
 enum cgl_fft_program {
   CGL_FFT_PLAIN = 0,      /* transform src -> dst (direction from `inverse`)         */
   CGL_FFT_IF4_START = 1,  /* last axis, inverse: u (spectral state) -> dst             */
-  CGL_FFT_IF4_B1 = 2,     /* last axis: g1 = F src -> g_out; dst = F^-1 E1/2 (u + t/2 g1) */
-  CGL_FFT_IF4_B2 = 3,     /* g2 = F src -> g_out; dst = F^-1 (E1/2 u + t/2 g2)           */
-  CGL_FFT_IF4_B3 = 4,     /* g3 = F src -> g_out; dst = F^-1 (t E1/2 g3 + E1 u)          */
-  CGL_FFT_IF4_B4 = 5,     /* g4 = F src; u_out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3)
-                             + t/6 g4 (checked); dst = F^-1 u_out unless dst == NULL   */
+  /* B1..B4 accumulate the Lawson combination out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3)
+   * + t/6 g4 (integrators.py:205-215) in ONE field acc, one term per stage:          */
+  CGL_FFT_IF4_B1 = 2,     /* last axis: g1 = F src; g_out = acc = E1 (u + t/6 g1);
+                             dst = F^-1 E1/2 (u + t/2 g1)                              */
+  CGL_FFT_IF4_B2 = 3,     /* g2 = F src; g_out = g[0] + t/3 E1/2 g2; dst = F^-1 (E1/2 u + t/2 g2) */
+  CGL_FFT_IF4_B3 = 4,     /* g3 = F src; g_out = g[0] + t/3 E1/2 g3; dst = F^-1 (t E1/2 g3 + E1 u) */
+  CGL_FFT_IF4_B4 = 5,     /* g4 = F src; u_out = u + t/6 g4 with u = acc (checked);
+                             dst = F^-1 u_out unless dst == NULL                       */
   CGL_FFT_G = 6,          /* dst = F g(scale * F^-1 src) along one axis                */
   CGL_FFT_STR_START = 7,  /* strided: dst = F flow(scale * u, t/2)  [step, seq 0]      */
   CGL_FFT_STR_A0 = 8,     /* strided: w = scale F^-1 src; u_out = flow(w, t/2) [seq 1],
@@ -354,8 +357,8 @@ enum cgl_fft_program {
 typedef struct {
   const double* u;           /* state operand (spectral for if4, physical for strang) */
   double* u_out;             /* state output                                        */
-  const double* g[3];        /* g1, g2, g3 (IF4_B4)                                  */
-  double* g_out;             /* g_i output (IF4_B1..B3)                              */
+  const double* g[3];        /* g[0]: running combination acc (IF4_B2, B3); g[1..2] unused */
+  double* g_out;             /* acc output (IF4_B1..B3; may alias g[0])              */
   const double* tables[2][3];/* separable exp(f tau symbol): [1/2, 1][axis]           */
   double tau, scale;
   cgl_nonlinear_t nl;        /* scalar kinds only (cubic / cubic_quintic)            */

@@ -104,6 +104,13 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, CONTIG>::MINB) fft_pass_kern
       // the next tile's prefetch so that wait_group 1 covers them)
 #pragma unroll
       for (int r = 0; r < 8; ++r) cp_async16(aux + r * NT + tid, a.u + gbase + (t + T * r));
+      // B2 / B3: the running combination is read straight from global memory after the
+      // forward transform; pull its lines into L2 now
+      if (PROG == FP_IF4_B2 || PROG == FP_IF4_B3) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.g[0] + gbase + (t + T * r)));
+      }
     }
     cp_async_commit();
     issue(tile + (int)gridDim.x, ring[(it + 1) & 1]);
@@ -407,8 +414,9 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
   if ((program >= FP_IF4_START && program <= FP_IF4_B4 || program == FP_STR_START) && !a.u)
     return set_error(CGL_EINVAL, "fft_pass: program needs u");
   if ((program >= FP_IF4_B1 && program <= FP_IF4_B3) && !a.g_out) return set_error(CGL_EINVAL, "fft_pass: needs g_out");
-  if (program == FP_IF4_B4 && (!a.g[0] || !a.g[1] || !a.g[2] || !a.u_out))
-    return set_error(CGL_EINVAL, "fft_pass: B4 needs g1..g3 and u_out");
+  if ((program == FP_IF4_B2 || program == FP_IF4_B3) && !a.g[0])
+    return set_error(CGL_EINVAL, "fft_pass: B2 / B3 need the running combination g[0]");
+  if (program == FP_IF4_B4 && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: B4 needs u_out");
   if (program == FP_STR_A0 && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: needs u_out");
   if ((program >= FP_IF4_B1 && program <= FP_IF4_B4) || program == FP_STR_MID)
     for (int fr = 0; fr < 2; ++fr)

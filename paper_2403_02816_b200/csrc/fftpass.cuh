@@ -18,10 +18,10 @@ namespace fftp {
 enum Prog {
   FP_PLAIN = 0,     // transform only
   FP_IF4_START,     // contiguous, inverse: src = spectral state u
-  FP_IF4_B1,        // contiguous: g1 = F(src); u2 = E1/2 (u + t/2 g1); dst = F^-1 u2
-  FP_IF4_B2,        // g2 = F(src); u3 = E1/2 u + t/2 g2
-  FP_IF4_B3,        // g3 = F(src); u4 = t E1/2 g3 + E1 u
-  FP_IF4_B4,        // g4 = F(src); out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4 -> u; check;
+  FP_IF4_B1,        // contiguous: g1 = F(src); acc = E1 (u + t/6 g1) -> g_out; u2 = E1/2 (u + t/2 g1); dst = F^-1 u2
+  FP_IF4_B2,        // g2 = F(src); acc = g[0] + t/3 E1/2 g2 -> g_out; u3 = E1/2 u + t/2 g2
+  FP_IF4_B3,        // g3 = F(src); acc = g[0] + t/3 E1/2 g3 -> g_out; u4 = t E1/2 g3 + E1 u
+  FP_IF4_B4,        // g4 = F(src); out = u + t/6 g4 with u = acc -> u_out; check;
                     // dst = F^-1 out (the next step's first inverse pass) when dst != null
   FP_G,             // inverse, x scale, g(.), forward (any axis)
   FP_STR_START,     // strided, forward: src = physical u (x scale); v = flow(u, t/2) [seq 0]
@@ -346,32 +346,45 @@ __device__ __forceinline__ bool contig_program(double2 (&v)[8], const Args& a, b
     return true;
   }
   fft_pencil<L, true, false>(v, t, sbuf, lay, tw);  // v = g_i (spectral)
-  cp_async_wait<1>();                               // the stage operands (the prefetch may fly)
+  cp_async_wait<1>();                               // the stage operand (the prefetch may fly)
+  // The Lawson combination out = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4
+  // (integrators.py:205-215) is ACCUMULATED stage by stage in one field `acc`
+  // (B1 starts it, B2 and B3 add their term, B4 adds the last and checks), so
+  // no stage reads more than one extra operand and g1..g3 are never stored.
+  // E1 = E1/2 E1/2 is formed as the square of the E1/2 entry (semigroup property, the same
+  // few-ulp difference from a separately rounded E1 table as the FD path's quad form): the
+  // passes are LSU-bound and a second table walk per point costs more than four multiplies
   double2 rf[2];
-  rf[0] = valid ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
-  rf[1] = (valid && (PROG == FP_IF4_B3 || PROG == FP_IF4_B4)) ? row_factor(a, 1, row) : rf[0];
+  rf[0] = (valid && PROG != FP_IF4_B4) ? row_factor(a, 0, row) : make_double2(0.0, 0.0);
+  rf[1] = rf[0];
   if (valid) {
+    // B2 / B3: the running combination of this tile, loaded before the arithmetic needs it
+    double2 acc[8];
+    if (PROG == FP_IF4_B2 || PROG == FP_IF4_B3) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc[r] = ldg_s(a.g[0] + gbase + t + T * r);
+    }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int i = t + T * r;
       const int gi = gbase + i;
       const double2 gi_v = v[r];
-      const double2 u = aux[r * NT + tid];
+      const double2 u = aux[r * NT + tid];  // B1..B3: the state u; B4: the accumulated combination
       if (PROG == FP_IF4_B1) {
-        stg_s(a.g_out + gi, gi_v);
-        v[r] = cmul(efac(a, 0, rf, i), caxpy(0.5 * tau, gi_v, u));
+        const double2 eh = efac(a, 0, rf, i);
+        stg_s(a.g_out + gi, cmul(cmul(eh, eh), caxpy(tau / 6.0, gi_v, u)));
+        v[r] = cmul(eh, caxpy(0.5 * tau, gi_v, u));
       } else if (PROG == FP_IF4_B2) {
-        stg_s(a.g_out + gi, gi_v);
-        v[r] = caxpy(0.5 * tau, gi_v, cmul(efac(a, 0, rf, i), u));
+        const double2 eh = efac(a, 0, rf, i);
+        stg_s(a.g_out + gi, caxpy(tau / 3.0, cmul(eh, gi_v), acc[r]));
+        v[r] = caxpy(0.5 * tau, gi_v, cmul(eh, u));
       } else if (PROG == FP_IF4_B3) {
-        stg_s(a.g_out + gi, gi_v);
-        v[r] = caxpy(tau, cmul(efac(a, 0, rf, i), gi_v), cmul(efac(a, 1, rf, i), u));
+        const double2 eh = efac(a, 0, rf, i);
+        const double2 ehg = cmul(eh, gi_v);
+        stg_s(a.g_out + gi, caxpy(tau / 3.0, ehg, acc[r]));
+        v[r] = caxpy(tau, ehg, cmul(cmul(eh, eh), u));
       } else {
-        const double2 g1 = ldg_s(a.g[0] + gi), g2 = ldg_s(a.g[1] + gi), g3 = ldg_s(a.g[2] + gi);
-        const double2 out =
-            caxpy(tau / 6.0, gi_v,
-                  caxpy(tau / 3.0, cmul(efac(a, 0, rf, i), caxpy(1.0, g2, g3)),
-                        cmul(efac(a, 1, rf, i), caxpy(tau / 6.0, g1, u))));
+        const double2 out = caxpy(tau / 6.0, gi_v, u);
         if (!cfinite(out)) note(key, check_pos, CGL_NONFINITE_STATE);
         stg_s(a.u_out + gi, out);
         v[r] = out;

@@ -608,10 +608,11 @@ class PencilFourierPlan(FourierPlan):
     if4 (state u in coefficient space, scratch T, g1..g3):
       prologue  IF4_START  T = F2^-1 u
       eval i    G1^-1, G0 (F0^-1, /N, g, F0), G1      (2D: G0 only)
-                B_i: g_i = F2 T; next stage input q -> T = F2^-1 q
-                (B4: u = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4, checked;
-                T = F2^-1 u starts the next step)
-      16 passes per 3D step: 688 B/pt of HBM traffic (cuFFT + stage kernels: ~1.1 KB/pt).
+                B_i: g_i = F2 T; next stage input q -> T = F2^-1 q; the combination
+                u' = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4 accumulates term by term
+                in one field (B4 adds the last, checks, stores u; T = F2^-1 u starts the
+                next step)
+      16 passes per 3D step: 672 B/pt of HBM traffic (cuFFT + stage kernels: ~1.1 KB/pt).
     strang (state in physical space, ping-pong U; the reference's F^-1 F at
     each step boundary elided exactly as FourierPlan):
       prologue  STR_START  T = F0 flow(u0 / N, t/2)
@@ -637,7 +638,7 @@ class PencilFourierPlan(FourierPlan):
         self.T = mk()
         if scheme_name == "if4":
             self.U = [[mk()]]
-            self.G = [mk() for _ in range(3)]
+            self.G = [mk()]   # the accumulated Lawson combination (B1 starts it, B4 finishes it)
         else:
             self.U = [[mk()], [mk()]]
         self.graphs = {}
@@ -689,17 +690,19 @@ class PencilFourierPlan(FourierPlan):
         inv_n = 1.0 / self.n
         if self.scheme == "if4":
             u = self.U[0][0]
-            g1, g2, g3 = self.G
-            for prog, gout in (("if4_b1", g1), ("if4_b2", g2), ("if4_b3", g3), ("if4_b4", None)):
+            acc = self.G[0]
+            for prog in ("if4_b1", "if4_b2", "if4_b3", "if4_b4"):
                 if d == 3:
                     self._pass("plain", 1, T, T, tau, inverse=True)
                 self._pass("g", 0, T, T, tau, scale=inv_n)
                 if d == 3:
                     self._pass("plain", 1, T, T, tau)
-                if gout is not None:
-                    self._pass(prog, last, T, T, tau, u=u, g_out=gout)
+                if prog == "if4_b1":
+                    self._pass(prog, last, T, T, tau, u=u, g_out=acc)
+                elif prog == "if4_b4":
+                    self._pass(prog, last, T, T, tau, u=acc, u_out=u)
                 else:
-                    self._pass(prog, last, T, T, tau, u=u, u_out=u, g=(g1, g2, g3))
+                    self._pass(prog, last, T, T, tau, u=u, g=(acc, None, None), g_out=acc)
         else:
             out = self.U[k % 2][0]
             if d == 3:

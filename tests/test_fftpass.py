@@ -152,3 +152,37 @@ def test_pencil_plan_matches_cufft_plan(scheme):
         assert key == _lib.NO_DIVERGENCE
         outs.append(plan.result(w.steps)[0].clone())
     assert rel_l2(outs[0].cpu().numpy(), outs[1].cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 512), (64, 32, 256), (512, 16, 64)])
+def test_passes_are_deterministic_under_repetition(shape):
+    """Shared-memory hazards (the contiguous passes synchronise per pencil: a
+    64-thread named barrier at L = 512, a warp barrier below; the 512-point
+    strided G pass exchanges 32 points per thread) would show as run-to-run
+    differences: 30 repetitions of a 3D round trip and of the fused G and B1
+    programs give the same bits every time.  (compute-sanitizer is closed on
+    the GPU pool, so racecheck could not be run.)"""
+    from paper_2403_02816_b200 import _lib, fftpass
+    x = _rand(shape, 7)
+    u = _rand(shape, 8)
+    nl = _lib.Nonlinear()
+    nl.alpha3, nl.beta3, nl.kind = -1.0, 0.7, 0
+    tabs = [[torch.exp(-0.01 * fr * _rand((shape[d],), 10 + d).abs() ** 2 * (1 + 0.3j)) for d in range(3)]
+            for fr in (0.5, 1.0)]
+    flag = _lib.new_flag(0)
+
+    def once():
+        y = fftpass.fftn(x)
+        z = fftpass.fftn(y, inverse=True)
+        g = torch.empty_like(x)
+        fftpass.axis_pass(x, g, 0, program="g", ops=fftpass.make_ops(nl=nl, scale=0.05))
+        t, gout = x.clone(), torch.empty_like(x)
+        fftpass.axis_pass(t, t, 2, program="if4_b1",
+                          ops=fftpass.make_ops(u=u, g_out=gout, tables=tabs, tau=0.01, nl=nl, flag=flag,
+                                               pos=_lib.rel_pos(1)))
+        return [torch.view_as_real(a).clone() for a in (y, z, g, t, gout)]
+
+    ref = once()
+    for _ in range(30):
+        for a, b in zip(once(), ref):
+            assert torch.equal(a, b)

@@ -88,9 +88,10 @@ def main():
     T0.copy_(fftpass.fftn(0.1 * x))
     run("G axis 0 (inv, g, fwd)", lambda: plan._pass("g", 0, T, T, w.tau, scale=1.0 / N), 32, True)
     run("IF4_B1 axis 2", lambda: plan._pass("if4_b1", 2, T, T, w.tau, u=u, g_out=g[0]), 64, True)
-    run("IF4_B3 axis 2", lambda: plan._pass("if4_b3", 2, T, T, w.tau, u=u, g_out=g[2]), 64, True)
+    run("IF4_B3 axis 2", lambda: plan._pass("if4_b3", 2, T, T, w.tau, u=u, g=(g[0], None, None), g_out=g[0]), 80,
+        True)
     v = u.clone()
-    run("IF4_B4 axis 2", lambda: plan._pass("if4_b4", 2, T, T, w.tau, u=v, u_out=v, g=tuple(g)), 112, True)
+    run("IF4_B4 axis 2", lambda: plan._pass("if4_b4", 2, T, T, w.tau, u=g[0], u_out=v), 64, True)
     y = x.clone()
     run("STR_A0 axis 0", lambda: plan._pass("str_a0", 0, T, T, w.tau, u_out=y, scale=1.0 / N), 48, True)
     run("STR_MID axis 2", lambda: plan._pass("str_mid", 2, T, T, w.tau), 32, True)

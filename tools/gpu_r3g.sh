@@ -1,0 +1,5 @@
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/g3_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/g3_pytest.log
+tail -n 4 gpurun_out/g3_pytest.log
+timeout 300 python tools/fft_probe.py 512 > gpurun_out/g3_probe.log 2>&1; grep -E "IF4_B|G axis" gpurun_out/g3_probe.log | grep -v "^{"
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/g3_bench.log 2>&1; echo "rc=$?" >> gpurun_out/g3_bench.log
+cut -c1-330 gpurun_out/g3_bench.log
