@@ -251,20 +251,36 @@ class ShardedPlan(FusedPlan):
         return _lib.NO_DIVERGENCE
 
 
-def integrate_sharded(problem, scheme_name, local_fields, t_final, steps, layout, group=None):
+def integrate_sharded(problem, scheme_name, local_fields, t_final, steps, layout, group=None,
+                      snapshot_steps=(), snapshot_path=None, grids=None):
     """Slab-sharded counterpart of integrate() for FD problems built on the
     LOCAL slab's operator (the axis-0 factor is the global n0 x n0 matrix).
-    Returns (local result fields, diverged_at, reason, device_seconds)."""
+    Returns (local result fields, diverged_at, reason, device_seconds).
+    snapshot_steps + snapshot_path (a format string taking the step, e.g.
+    "run_{:05d}.cgls") + grids (global node coordinates per direction): every
+    rank stores its slab of those steps into the one snapshot file
+    (io.write_snapshot_sharded; no gather)."""
     from .integrators import SCHEMES
     if scheme_name not in ("if4", "strang", "split4", "if2"):
         raise ValueError(f"sharded path supports if4/strang/split4/if2, not {scheme_name!r}")
     tau = t_final / steps
     problem.prepare(tau, SCHEMES[scheme_name])
     plan = ShardedPlan(problem, scheme_name, list(local_fields), layout, group)
+    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
+    on_stop = None
+    if snapshot_path is not None and snapshot_steps:
+        if grids is None:
+            raise ValueError("snapshots need the global node coordinates (grids)")
+        from .io import write_snapshot_sharded
+        barrier = (lambda: dist.barrier(group)) if dist.is_available() and dist.is_initialized() else None
+
+        def on_stop(k, fields):
+            write_snapshot_sharded(snapshot_path.format(k), fields, k * tau, grids, layout.shape,
+                                   layout.bounds(rank), rank=rank, barrier=barrier)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record()
-    key = plan.run(list(local_fields), steps, tau)
+    key = plan.run(list(local_fields), steps, tau, stop_at=tuple(snapshot_steps), on_stop=on_stop)
     ev1.record()
     torch.cuda.synchronize()
     dev_s = ev0.elapsed_time(ev1) / 1e3

@@ -1,12 +1,18 @@
-"""Slab-sharded periodic (pseudospectral) path: distributed 3D cuFFT with the
+"""Slab-sharded periodic (pseudospectral) path: distributed 3D FFT with the
 spectral data kept in the transposed column-block layout.
 
 Global grid (n0, n1, n2), C order, split into axis-0 slabs of p0 = n0/P
 planes.  Forward transform of a slab set:
-  2D FFT over (x1, x2) of every local plane          (cuFFT, batched, in place)
+  transforms along x2 and x1 of every local plane    (one pencil pass each, in place)
   all-to-all: slab (p0, n1 n2) -> column block (n0, m), m = n1 n2 / P
-  1D FFT along x0 of the m columns                    (cuFFT, strided, in place)
-The inverse reverses the three stages.  Coefficients therefore live in
+  transform along x0 of the m columns                 (one strided pencil pass, in place)
+The inverse reverses the three stages.  The local transforms are the
+single-GPU plan's pencil passes (csrc/fftpass.cu, one HBM pass per axis) when
+the local extents are powers of two in 16..512, else batched cuFFT plans; with
+the passes, F g F^-1 of a stage input (integrators.py:99-101) takes the fused
+program along the contiguous axis (F_2^-1, 1/N, g, F_2 in one pass), so an
+evaluation is 5 local passes and 2 exchanges instead of cuFFT's ~7 passes plus
+a g kernel.  Coefficients therefore live in
 (n0 x m) column blocks; the separable exp(f tau symbol) multipliers and the
 Lawson stage combinations run there (cgl_stage_fourier_cols /
 cgl_separable_mul_cols map a local element (k0, c) to global flat index
@@ -74,7 +80,11 @@ class SlabExchange:
                 for ls, s in enumerate(self.ranks):
                     cols[ls][r * p0:(r + 1) * p0].copy_(src[:, s, :])
             return cols
-        self.send.copy_(slabs[0].reshape(p0, P, m).transpose(0, 1))
+        if slabs[0].is_cuda:   # row-permutation kernels (csrc/slab.cu) instead of a strided torch copy
+            _lib.check(_lib.load().cgl_slab_pack(_lib.stream(), P, p0, m, _lib.ptr(slabs[0]), _lib.ptr(self.send)),
+                       "cgl_slab_pack")
+        else:
+            self.send.copy_(slabs[0].reshape(p0, P, m).transpose(0, 1))
         dist.all_to_all_single(cols[0].view(-1), self.send.view(-1), group=self.group)
         return cols
 
@@ -87,7 +97,11 @@ class SlabExchange:
                     dst[:, s, :].copy_(cols[ls][r * p0:(r + 1) * p0])
             return slabs
         dist.all_to_all_single(self.recv.view(-1), cols[0].reshape(-1), group=self.group)
-        slabs[0].reshape(p0, P, m).copy_(self.recv.transpose(0, 1))
+        if slabs[0].is_cuda:
+            _lib.check(_lib.load().cgl_slab_unpack(_lib.stream(), P, p0, m, _lib.ptr(self.recv), _lib.ptr(slabs[0])),
+                       "cgl_slab_unpack")
+        else:
+            slabs[0].reshape(p0, P, m).copy_(self.recv.transpose(0, 1))
         return slabs
 
 
@@ -95,17 +109,38 @@ class SlabFFT:
     """Unnormalised distributed 3D FFT: slabs (p0, n1, n2) <-> column blocks (n0, m)."""
 
     def __init__(self, ex):
+        from . import fftpass
         n0, n1, n2 = ex.shape
         self.ex = ex
-        self.f2 = FftMany((n1, n2), ex.p0, 1, n1 * n2)   # planes of a slab
-        self.f1 = FftMany((n0,), ex.m, ex.m, 1)          # columns of a block (stride m)
+        # column block (n0, m) viewed as (n0, m / n2, n2): the pencil passes take 3D fields
+        self.cshape = (n0, ex.m // n2, n2) if ex.m % n2 == 0 else None
+        self.sshape = (ex.p0, n1, n2)
+        self.pencil = (self.cshape is not None and fftpass.supported(self.cshape) and fftpass.supported(self.sshape))
+        if not self.pencil:
+            self.f2 = FftMany((n1, n2), ex.p0, 1, n1 * n2)   # planes of a slab
+            self.f1 = FftMany((n0,), ex.m, ex.m, 1)          # columns of a block (stride m)
+
+    def slab_pass(self, x, axis, inverse=False, program="plain", ops=None):
+        from .fftpass import axis_pass
+        axis_pass(x, x, axis, inverse=inverse, program=program, ops=ops, shape=self.sshape)
+
+    def col_pass(self, y, inverse=False):
+        from .fftpass import axis_pass
+        axis_pass(y, y, 0, inverse=inverse, shape=self.cshape)
 
     def forward(self, slabs, cols):
         for x in slabs:
-            self.f2(x)
+            if self.pencil:
+                self.slab_pass(x, 2)
+                self.slab_pass(x, 1)
+            else:
+                self.f2(x)
         self.ex.to_cols(slabs, cols)
         for y in cols:
-            self.f1(y)
+            if self.pencil:
+                self.col_pass(y)
+            else:
+                self.f1(y)
         return cols
 
     def inverse(self, cols, slabs, cols_scratch=None):
@@ -117,11 +152,35 @@ class SlabFFT:
                 b.copy_(a)
             work = cols_scratch
         for y in work:
-            self.f1(y, inverse=True)
+            if self.pencil:
+                self.col_pass(y, inverse=True)
+            else:
+                self.f1(y, inverse=True)
         self.ex.to_slabs(work, slabs)
         for x in slabs:
-            self.f2(x, inverse=True)
+            if self.pencil:
+                self.slab_pass(x, 1, inverse=True)
+                self.slab_pass(x, 2, inverse=True)
+            else:
+                self.f2(x, inverse=True)
         return slabs
+
+    def g_of(self, work_cols, slabs, dst_cols, nl, scale, flag, pos):
+        """dst = F g(scale F^-1 work) with the contiguous-axis transforms and g
+        fused in one pass (pencil passes only); work_cols is clobbered."""
+        from .fftpass import make_ops
+        for y in work_cols:
+            self.col_pass(y, inverse=True)
+        self.ex.to_slabs(work_cols, slabs)
+        ops = make_ops(nl=nl, scale=scale, flag=flag, pos=pos)
+        for x in slabs:
+            self.slab_pass(x, 1, inverse=True)
+            self.slab_pass(x, 2, program="g", ops=ops)
+            self.slab_pass(x, 1)
+        self.ex.to_cols(slabs, dst_cols)
+        for y in dst_cols:
+            self.col_pass(y)
+        return dst_cols
 
 
 class ShardedFourierPlan:
@@ -185,9 +244,18 @@ class ShardedFourierPlan:
         if not self.ex.virtual:
             global_min_key(self.flag, self.group)
 
-    def _gspec(self, src_cols, dst_cols, pos):
-        """dst = F g(F^-1 src) (coefficients -> coefficients)."""
-        self.fft.inverse(src_cols, self.Qs, cols_scratch=self.Qc)
+    def _gspec(self, src_cols, dst_cols, pos, clobber=False):
+        """dst = F g(F^-1 src) (coefficients -> coefficients); src is preserved
+        unless clobber."""
+        if self.fft.pencil:
+            work = src_cols
+            if not clobber:
+                for a, b in zip(src_cols, self.Qc):
+                    b.copy_(a)
+                work = self.Qc
+            self.fft.g_of(work, self.Qs, dst_cols, self.nl, 1.0 / self.N, self.flag, pos)
+            return
+        self.fft.inverse(src_cols, self.Qs, cols_scratch=None if clobber else self.Qc)
         self._g(self.Qs, pos)
         self.fft.forward(self.Qs, dst_cols)
 
@@ -209,9 +277,7 @@ class ShardedFourierPlan:
                     for li in range(len(self.ranks)):
                         self._fstage(name, li, [self.U[li], gin[li]], [self.Qc[li]], tau, pos)
                     # Qc holds the next stage input: F g F^-1 Qc -> gout (Qc may be clobbered)
-                    self.fft.inverse(self.Qc, self.Qs)
-                    self._g(self.Qs, pos)
-                    self.fft.forward(self.Qs, gout)
+                    self._gspec(self.Qc, gout, pos, clobber=True)
                 self._reduce()
                 for li in range(len(self.ranks)):
                     self._fstage("fif4_s4", li, [self.U[li], G1[li], G2[li], G3[li], G4[li]], [self.U[li]], tau, pos)

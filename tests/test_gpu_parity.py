@@ -648,6 +648,54 @@ def test_slab_sharded_fourier_virtual_ranks(P, config_golden, nranks, scheme, ta
     assert rel_l2(got, arrays[f"{tag}_out"]) <= 1e-10
 
 
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+@pytest.mark.parametrize("scheme", ["if4", "strang"])
+def test_slab_sharded_fourier_on_pencil_passes(P, nranks, scheme):
+    """At 64^3 the sharded plan's local transforms are the pencil passes (g fused
+    into the contiguous-axis pass): P virtual ranks reproduce the single-GPU
+    plan's coefficients after 10 steps."""
+    from paper_2403_02816_b200 import SCHEMES, workloads as W
+    from paper_2403_02816_b200 import slabfourier as SF
+    from paper_2403_02816_b200.spectral import dft_forward, dft_inverse
+    w = W.CONFIGS["C3"].scaled(64, 10)
+    uhat = dft_forward(W.initial_state_device(w))
+    ref = torch.as_tensor(P.integrate(W.build_problem(w), scheme, (uhat,), w.t_final, w.steps).fields[0])
+    prob = W.build_problem(w)
+    prob.prepare(w.tau, SCHEMES[scheme])
+    plan = SF.ShardedFourierPlan(prob, scheme, w.extents, nranks, list(range(nranks)))
+    assert plan.fft.pencil
+    x = SF.split_global(uhat if scheme == "if4" else dft_inverse(uhat), nranks, "cols" if scheme == "if4" else "slabs")
+    assert plan.run(x, w.steps, w.tau) == (1 << 64) - 1
+    got = SF.gather_cols(plan.result_cols(w.steps), w.extents)
+    assert float(torch.linalg.vector_norm(got - ref) / torch.linalg.vector_norm(ref)) <= 1e-12
+
+
+def test_slab_sharded_fourier_real_rank_path_world1(P):
+    """One real rank with an NCCL process group of size 1: the non-virtual
+    exchange (cgl_slab_pack / all_to_all_single / cgl_slab_unpack) and the
+    cross-rank key reduction run as they do at P > 1."""
+    import torch.distributed as dist
+    from paper_2403_02816_b200 import SCHEMES, workloads as W
+    from paper_2403_02816_b200 import slabfourier as SF
+    from paper_2403_02816_b200.spectral import dft_forward
+    from test_multirank import _port
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        w = W.CONFIGS["C3"].scaled(64, 6)
+        uhat = dft_forward(W.initial_state_device(w))
+        ref = torch.as_tensor(P.integrate(W.build_problem(w), "if4", (uhat,), w.t_final, w.steps).fields[0])
+        prob = W.build_problem(w)
+        prob.prepare(w.tau, SCHEMES["if4"])
+        plan = SF.ShardedFourierPlan(prob, "if4", w.extents, 1, [0], dist.group.WORLD)
+        assert not plan.ex.virtual
+        assert plan.run(SF.split_global(uhat, 1, "cols"), w.steps, w.tau) == (1 << 64) - 1
+        got = SF.gather_cols(plan.result_cols(w.steps), w.extents)
+        assert float(torch.linalg.vector_norm(got - ref) / torch.linalg.vector_norm(ref)) <= 1e-12
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("nranks", [1, 2, 4, 8])
 def test_fd_slab_tucker_oz_virtual_ranks_bit_identical(P, nranks):
     """Slab-sharded Tucker chain on the INT8 tensor cores (column-block
@@ -683,6 +731,26 @@ def test_sharded_plan_world1_matches_unsharded(P, scheme):
                                                 D.SlabLayout(w.extents, 1))
     assert k_div == 0 and reason == ""
     assert (torch.linalg.vector_norm(out[0] - ref) / torch.linalg.vector_norm(ref)).item() <= 1e-13
+
+
+def test_sharded_run_writes_snapshots_without_gather(P, tmp_path):
+    """integrate_sharded stores the slab of each snapshot step into the one CGLS
+    file (io.write_snapshot_sharded): the same bytes as write_snapshot of the
+    single-GPU run's snapshot (io.py:35-59 of the reference)."""
+    from paper_2403_02816_b200 import distributed as D, io as cio, workloads as W
+    w = W.CONFIGS["C2"].scaled(32, 6)
+    x0 = W.initial_state_device(w)
+    grids = [np.linspace(-1.0, 1.0, n) for n in w.extents]
+    snaps = {}
+    P.integrate(W.build_problem(w), "if4", (x0,), w.t_final, w.steps, snapshot_steps=(3, 6),
+                on_snapshot=lambda k, t, f: snaps.__setitem__(k, (t, f[0].clone())))
+    D.integrate_sharded(W.build_problem(w), "if4", [x0.clone()], w.t_final, w.steps, D.SlabLayout(w.extents, 1),
+                        snapshot_steps=(3, 6), snapshot_path=str(tmp_path / "s_{:03d}.cgls"), grids=grids)
+    for k, (t, f) in snaps.items():
+        (got,), tt = cio.read_snapshot(tmp_path / f"s_{k:03d}.cgls")
+        assert tt == pytest.approx(t, abs=1e-15)
+        ref = f.cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-13
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
