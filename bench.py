@@ -325,8 +325,9 @@ def fourier_roofline(torch, w, scheme, step_seconds):
         dom = "g (axis 0: F^-1, g, F)"
     else:
         y = x.clone()
+        a0 = "str_a0f" if plan._fused_boundary() else "str_a0"
         progs = {"str_a0 (axis 0: F^-1, 2 flows, check, F)": (
-                     lambda: plan._pass("str_a0", 0, T, T, w.tau, u_out=y, scale=1.0 / n), 48, 1),
+                     lambda: plan._pass(a0, 0, T, T, w.tau, u_out=y, scale=1.0 / n), 48, 1),
                  "plain axis 1": (lambda: plan._pass("plain", 1, T, T, w.tau), 32, 2),
                  "str_mid (axis 2: F, E1, F^-1)": (lambda: plan._pass("str_mid", last, T, T, w.tau), 32, 1)}
         dom = "str_a0 (axis 0: F^-1, 2 flows, check, F)"

@@ -352,7 +352,11 @@ enum cgl_fft_program {
   CGL_FFT_STR_START = 7,  /* strided: dst = F flow(scale * u, t/2)  [step, seq 0]      */
   CGL_FFT_STR_A0 = 8,     /* strided: w = scale F^-1 src; u_out = flow(w, t/2) [seq 1],
                              checked; dst = F flow(u_out, t/2) [step + 1] unless NULL  */
-  CGL_FFT_STR_MID = 9     /* last axis: dst = F^-1 (E1 .* F src)                       */
+  CGL_FFT_STR_MID = 9,    /* last axis: dst = F^-1 (E1 .* F src)                       */
+  CGL_FFT_STR_A0F = 10    /* STR_A0 for the exact cubic flow (kind 0) with the two flows at the
+                             step boundary evaluated as one (semigroup; the reference's checks
+                             and positions kept): u_out = w = scale F^-1 src, the step's state
+                             being flow(u_out, t/2); dst = F flow(w, t) unless NULL          */
 };
 typedef struct {
   const double* u;           /* state operand (spectral for if4, physical for strang) */

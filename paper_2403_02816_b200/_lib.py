@@ -73,7 +73,7 @@ class FftOps(ctypes.Structure):
 
 
 FFT_PROGRAMS = {"plain": 0, "if4_start": 1, "if4_b1": 2, "if4_b2": 3, "if4_b3": 4, "if4_b4": 5, "g": 6,
-                "str_start": 7, "str_a0": 8, "str_mid": 9}
+                "str_start": 7, "str_a0": 8, "str_mid": 9, "str_a0f": 10}
 
 _SIGS = {
     "cgl_version": (ctypes.c_char_p, []),

@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
   // take the slots this grid's remaining CTAs need
   pdl_wait();
   const uint64_t step = resolve_pos(a.flag, a.pos) >> 24;
-  if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)(PROG == FP_STR_A0 ? a.fw : 0) << 8))) return;
+  if (a.flag && flag_skip(a.flag, (step << 24) | ((uint64_t)((PROG == FP_STR_A0 || PROG == FP_STR_A0F) ? a.fw : 0) << 8)))
+    return;
   const int tid = threadIdx.x;
   const TileMap<L, false, NT> map(tid);
   const int t = map.t;
@@ -252,12 +253,27 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
     }
     __syncthreads();
     fft_pencil<L, false, false>(v, t, sm, lay, tw);
+  } else if (PROG == FP_STR_A0F) {
+    fft_pencil<L, false, true>(v, t, sm, lay, tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double2 w = cscale(a.scale, v[r]);
+      if (valid) stg_s(a.u_out + gbase + (t + T * r) * gstride, w);
+      v[r] = cubic_boundary(a.nl, w, 0.5 * tau, step, a.fw, key);
+    }
+    if (a.dst == nullptr) {
+      raise_min(a.flag, valid ? key : ~0ull);
+      pdl_trigger();
+      return;
+    }
+    __syncthreads();
+    fft_pencil<L, false, false>(v, t, sm, lay, tw);
   }
   if (valid) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) stg_s(a.dst + gbase + (t + T * r) * gstride, v[r]);
   }
-  if (PROG == FP_STR_START || PROG == FP_STR_A0) raise_min(a.flag, valid ? key : ~0ull);
+  if (PROG == FP_STR_START || PROG == FP_STR_A0 || PROG == FP_STR_A0F) raise_min(a.flag, valid ? key : ~0ull);
   pdl_trigger();
 }
 
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(NT, Occ<PROG, NT, false>::MINB) fft_strided_ke
 //    two exact flows per point are FP64-latency-bound and want warps more
 //    than 128-byte chunks.
 static int threads_for(int L, bool contig, int prog) {
-  if (prog == FP_STR_A0 || prog == FP_STR_START) return 256;
+  if (prog == FP_STR_A0 || prog == FP_STR_A0F || prog == FP_STR_START) return 256;
   return (!contig && L == 512) ? 512 : 256;
 }
 
@@ -354,6 +370,7 @@ static int launch_L(int prog, bool contig, bool inv, const Args& a, cudaStream_t
     case FP_G: return launch_one<L, false, FP_G, false>(a, st);
     case FP_STR_START: return launch_one<L, false, FP_STR_START, false>(a, st);
     case FP_STR_A0: return launch_one<L, false, FP_STR_A0, false>(a, st);
+    case FP_STR_A0F: return launch_one<L, false, FP_STR_A0F, false>(a, st);
     default: return set_error(CGL_EINVAL, "fft_pass: program needs the contiguous axis");
   }
 }
@@ -409,7 +426,7 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
   // operand checks per program
   const bool need_src = !(program == FP_IF4_START || program == FP_STR_START);
   if (need_src && !src) return set_error(CGL_EINVAL, "fft_pass: null src");
-  const bool dst_optional = program == FP_IF4_B4 || program == FP_STR_A0;
+  const bool dst_optional = program == FP_IF4_B4 || program == FP_STR_A0 || program == FP_STR_A0F;
   if (!dst && !dst_optional) return set_error(CGL_EINVAL, "fft_pass: null dst");
   if ((program >= FP_IF4_START && program <= FP_IF4_B4 || program == FP_STR_START) && !a.u)
     return set_error(CGL_EINVAL, "fft_pass: program needs u");
@@ -417,7 +434,8 @@ int fft_pass_launch(cudaStream_t st, int program, int ndim, const int64_t* shape
   if ((program == FP_IF4_B2 || program == FP_IF4_B3) && !a.g[0])
     return set_error(CGL_EINVAL, "fft_pass: B2 / B3 need the running combination g[0]");
   if (program == FP_IF4_B4 && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: B4 needs u_out");
-  if (program == FP_STR_A0 && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: needs u_out");
+  if ((program == FP_STR_A0 || program == FP_STR_A0F) && !a.u_out) return set_error(CGL_EINVAL, "fft_pass: needs u_out");
+  if (program == FP_STR_A0F && a.nl.kind != 0) return set_error(CGL_EINVAL, "fft_pass: STR_A0F is for the exact cubic flow");
   if ((program >= FP_IF4_B1 && program <= FP_IF4_B4) || program == FP_STR_MID)
     for (int fr = 0; fr < 2; ++fr)
       for (int d = 0; d < ndim; ++d)

@@ -28,6 +28,8 @@ enum Prog {
   FP_STR_A0,        // strided: w = F^-1(src) x scale; out = flow(w, t/2) [seq w]; check; u_out = out;
                     // v = flow(out, t/2) [step + 1, seq 0]; dst = F(v) when dst != null
   FP_STR_MID,       // contiguous: F, x E1, F^-1
+  FP_STR_A0F,       // as STR_A0 for the exact cubic flow with the two boundary flows fused (cubic_boundary):
+                    // u_out = w (the step's state is flow(u_out, t/2), evaluated on demand); dst = F(flow(w, t))
   FP_NPROG
 };
 

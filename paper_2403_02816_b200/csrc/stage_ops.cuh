@@ -143,6 +143,38 @@ __device__ __forceinline__ V<NF> flow(const StageNL& p, const V<NF>& u, double t
   return r;
 }
 
+// Boundary of two Strang steps on the exact cubic flow (kind 0).  The reference evaluates
+//   out = flow(w, h) at (step, seq1), checks the state, then v = flow(out, h) at (step + 1, 0)
+// (integrators.py:161-164 at consecutive steps; flows.py:87-100).  By the semigroup property
+// v = flow(w, 2 h): one log1p, one sincos and one rsqrt instead of two of each.  With
+// y1 = 2 a3 |w|^2 h computed as the reference computes it, none of its four checks (blow-up
+// and non-finite output of either flow, non-finite state) can fire while w is finite and
+// y1 < 1/2 (then y2 = 2 a3 |out|^2 h = y1 / (1 - y1) < 1); a guard band of 1e-9 below that
+// threshold and every other case take the reference's own two evaluations, so the recorded
+// (step, seq, reason) is the reference's.  Returns v; the step's state is flow(w, h), which
+// the caller keeps as w and evaluates on demand.
+__device__ __forceinline__ double2 cubic_boundary(const StageNL& p, double2 w, double h, uint64_t step, int seq1,
+                                                  uint64_t& key) {
+  const double m = cabs2(w);
+  const double y1 = 2.0 * p.a3 * m * h;
+  const bool phase_only = fabs(p.a3) < 1e-14;
+  if (cfinite(w) && (phase_only || y1 < 0.5 - 1e-9)) {
+    double sn, cs;
+    if (phase_only) {
+      sincos(p.b3 * m * (2.0 * h), &sn, &cs);
+      return cmul(w, make_double2(cs, sn));
+    }
+    const double y = 2.0 * y1;  // 2 a3 |w|^2 (2 h)
+    const double L = log1p(-y);
+    sincos((-p.b3 / (2.0 * p.a3)) * L, &sn, &cs);
+    const double r = rsqrt(1.0 - y);
+    return cmul(w, make_double2(__dmul_rn(r, cs), __dmul_rn(r, sn)));
+  }
+  const double2 out = cubic_exact(p, w, h, (step << 24) | ((uint64_t)seq1 << 8), key);
+  if (!cfinite(out)) note(key, (step << 24) | (255ull << 8), CGL_NONFINITE_STATE);
+  return cubic_exact(p, out, h, (step + 1) << 24, key);
+}
+
 template <int NF>
 __device__ __forceinline__ bool finite_all(const V<NF>& v) {
   bool ok = true;

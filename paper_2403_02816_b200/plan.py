@@ -619,7 +619,10 @@ class PencilFourierPlan(FourierPlan):
       step k    F1, STR_MID (F2, E1, F2^-1), F1^-1,
                 STR_A0: w = F0^-1 T / N; u_k = flow(w, t/2) (checked, stored);
                 T = F0 flow(u_k, t/2) of step k + 1
-      4 passes per 3D step: 144 B/pt.
+      4 passes per 3D step: 144 B/pt.  For the exact cubic flow the two flows at a step
+      boundary are one flow(., t) by the semigroup property (STR_A0F: one log1p / sincos /
+      rsqrt per point instead of two; the reference's checks decided as it decides them):
+      the stored field is then w, and the state flow(w, t/2) is formed when it is asked for.
     Divergence keys and positions are those of the stage kernels (same
     programs, same flag record), so diverged_at / reason are unchanged.
     """
@@ -670,6 +673,7 @@ class PencilFourierPlan(FourierPlan):
         d = len(self.shape)
         self._tab_keep = tabs
         self._tabs = [tabs[0:d], tabs[d:2 * d]]
+        self._tau = float(tau)
         if self.scheme == "if4":
             self.U[0][0].copy_(u0[0])
         else:
@@ -711,13 +715,26 @@ class PencilFourierPlan(FourierPlan):
             if d == 3:
                 self._pass("plain", 1, T, T, tau, inverse=True)
             self._before_end(flag)
-            self._pass("str_a0", 0, T, T, tau, u_out=out, scale=inv_n)
+            self._pass("str_a0f" if self._fused_boundary() else "str_a0", 0, T, T, tau, u_out=out, scale=inv_n)
+
+    def _fused_boundary(self):
+        return self.nl.kind == 0
 
     def result(self, k):
         from .fftpass import fftn
         if self.scheme == "if4":
             return self.U[0]
-        return [fftn(self.U[k % 2][0])]
+        state = self.U[k % 2][0]
+        if k == 0:
+            return [fftn(state) * (1.0 / self.n)]   # load_state left N x the physical input in U[0]
+        if self._fused_boundary():
+            # U holds w of step k: the state is flow(w, t/2) (same device function as the
+            # step kernels; no divergence bookkeeping: step k's checks ran in its pass)
+            w, state = state, torch.empty_like(state)
+            _lib.check(_lib.load().cgl_stage(_lib.stream(), _lib.STAGE["flow1"], 1, w.numel(),
+                                             _lib.ctypes.byref(self.nl), self._tau, 1.0, _lib.ptr_array([w]),
+                                             _lib.ptr_array([state]), None, 0), "cgl_stage(flow1)")
+        return [fftn(state)]
 
 
 def half_bandwidth(m):

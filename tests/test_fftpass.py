@@ -186,3 +186,40 @@ def test_passes_are_deterministic_under_repetition(shape):
     for _ in range(30):
         for a, b in zip(once(), ref):
             assert torch.equal(a, b)
+
+
+def _oracle_fourier_problem(extents, params, kind):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN), "..", "oracle"))
+    import cgl_oracle as O
+    p = O.Params(**params)
+    intervals = tuple((-8.0, 8.0) for _ in extents)
+    return O, O.Prob([O.FourierOp(O.symbol(extents, intervals, p))], kind, p), intervals
+
+
+@pytest.mark.parametrize("extents", [(16, 16, 16), (32, 16)])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4, 5, 6, 7])
+def test_strang_blow_up_step_matches_oracle(extents, seed):
+    """Self-focusing cubic term (alpha3 > 0): the exact cubic flow blows up in
+    finite time.  The fused plan evaluates the two flows at a step boundary as
+    one (STR_A0F) and decides the reference's checks from y1; the diverged
+    step, the reason and the returned (last complete) state must be the
+    oracle's for every seed and amplitude (blow-ups at steps 2..21 and runs that
+    stay smooth)."""
+    import paper_2403_02816_b200 as P
+    from paper_2403_02816_b200 import CglParameters, FourierGrid, NonlinearSpec, Problem, build_periodic_operator
+    from paper_2403_02816_b200.plan import PencilFourierPlan
+    params = dict(alpha1=1.0, beta1=0.5, alpha2=0.5, alpha3=1.0, beta3=-0.7)
+    O, oprob, intervals = _oracle_fourier_problem(extents, params, "cubic")
+    rng = np.random.default_rng(seed)
+    amp = 0.55 + 0.6 * rng.random()
+    u0 = amp * (rng.standard_normal(extents) + 1j * rng.standard_normal(extents))
+    steps, t_final = 24, 0.6
+    want = O.integrate(oprob, "strang", (np.fft.fftn(u0),), t_final, steps)
+    p = CglParameters(**params)
+    prob = Problem(build_periodic_operator(FourierGrid(tuple(extents), intervals), p), NonlinearSpec("cubic", p))
+    got = P.integrate(prob, "strang", (np.fft.fftn(u0),), t_final, steps)
+    assert any(isinstance(pl, PencilFourierPlan) and pl._fused_boundary() for pl in prob._plans.values())
+    assert (got.diverged, got.diverged_at, got.reason) == (want.diverged, want.diverged_at, want.reason)
+    a, b = got.fields[0], want.fields[0]
+    assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)

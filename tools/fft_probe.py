@@ -94,6 +94,7 @@ def main():
     run("IF4_B4 axis 2", lambda: plan._pass("if4_b4", 2, T, T, w.tau, u=g[0], u_out=v), 64, True)
     y = x.clone()
     run("STR_A0 axis 0", lambda: plan._pass("str_a0", 0, T, T, w.tau, u_out=y, scale=1.0 / N), 48, True)
+    run("STR_A0F axis 0 (fused flows)", lambda: plan._pass("str_a0f", 0, T, T, w.tau, u_out=y, scale=1.0 / N), 48, True)
     run("STR_MID axis 2", lambda: plan._pass("str_mid", 2, T, T, w.tau), 32, True)
     run("cuFFT Z2Z 3D fwd", lambda: spectral.fft_dev(T, inverse=False, out=T), 32)
     if not eager:
