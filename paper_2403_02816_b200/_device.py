@@ -22,11 +22,12 @@ def to_device(x):
 
 
 def to_host(t):
-    """Device tensor -> numpy.  Fields of 1 MiB and more land in page-locked
+    """Device tensor -> numpy.  Fields of 1 MiB .. 4 GiB land in page-locked
     memory from torch's caching host allocator (a pageable .cpu() copy of a
     2 GiB state runs at a few GB/s; the pinned block is reused once the
-    returned array is dropped)."""
-    if t.numel() * t.element_size() < (1 << 20):
+    returned array is dropped); larger ones (1024^3: 17 GB) are not pinned."""
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (1 << 20) or nbytes > (4 << 30):
         return t.cpu().numpy()
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     h.copy_(t, non_blocking=True)
