@@ -29,7 +29,10 @@ def to_host(t):
     nbytes = t.numel() * t.element_size()
     if nbytes < (1 << 20) or nbytes > (4 << 30):
         return t.cpu().numpy()
-    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    try:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    except RuntimeError:   # no page-locked memory to be had: pageable copy
+        return t.cpu().numpy()
     h.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return h.numpy()
