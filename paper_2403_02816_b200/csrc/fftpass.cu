@@ -337,8 +337,29 @@ static int launch_r32(const Args& a, cudaStream_t st) {
   return check_launch("fft_r32_kernel");
 }
 
+template <int PROG>
+static int launch_c32(const Args& a, cudaStream_t st) {
+  auto kern = fft_c32_kernel<PROG>;
+  const int smem = 4096 * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "fft_c32 attribute");
+    attr = true;
+  }
+  const int64_t tiles = (a.O + 7) / 8;
+  if (tiles <= 0) return 0;
+  cudaError_t e = launch_k(kern, dim3((unsigned)tiles), dim3(128), (size_t)smem, st, dim3(1), a, (int)tiles);
+  if (e != cudaSuccess) return set_cuda_error(e, "fft_c32 launch");
+  return check_launch("fft_c32_kernel");
+}
+
 template <int L, bool CONTIG, int PROG, bool INV>
 static int launch_one(const Args& a, cudaStream_t st) {
+  if constexpr (L == 512 && CONTIG && (PROG == FP_G || PROG == FP_STR_MID)) {
+    static const int c32 = [] { const char* e = getenv("CGL_FFT_C32"); return e ? atoi(e) : 1; }();
+    if (c32) return launch_c32<PROG>(a, st);
+  }
   // the two-transform G pass is bound by the shared-memory data pipe: 32 points per thread
   // (one exchange per transform) take 1.15 ms at 512^3 against 1.50 ms for the radix-8 plan;
   // the single-transform passes are HBM/latency-bound and keep the 8-point kernel (0.76-0.87

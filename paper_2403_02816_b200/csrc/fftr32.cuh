@@ -134,7 +134,17 @@ __device__ __forceinline__ void dft16(double2* a) {
 // v[r] = x[t + 16 r], on exit v[r] = X[t + 16 r].  sm: the chunk's exchange
 // buffer [512][8] (conflict-free: a quarter-warp = the 8 pencils of one
 // (q, t) position = one 128-byte line); all 128 threads of the chunk call it.
-template <bool INV>
+// Exchange slot of position (q, t) of pencil `pp`.  Strided passes (SW = false): the 8
+// pencils of a chunk interleaved, [(q, t)][pp]; contiguous passes (SW = true): a pencil
+// (= row) owns 512 consecutive slots and t is XOR-swizzled with q, so that both the
+// writes (fixed q, t = 0..7 per quarter-warp) and the reads (fixed t, q = 0..7) hit 8
+// distinct 16-byte bank groups.
+template <bool SW>
+__device__ __forceinline__ int r32_slot(int q, int t, int pp) {
+  return SW ? pp * 512 + q * 16 + (t ^ (q & 15)) : (q * 16 + t) * 8 + pp;
+}
+
+template <bool INV, bool SW = false>
 __device__ __forceinline__ void fft512_r32(double2 (&v)[32], int t, int pp, double2* sm) {
   dft32<INV>(v);  // Y[m + 4 k] in v[k + 8 m]
 #pragma unroll
@@ -147,17 +157,17 @@ __device__ __forceinline__ void fft512_r32(double2 (&v)[32], int t, int pp, doub
         const double2 w = __ldg(&g_fft_tw512[t * q]);
         y = cmul(y, INV ? make_double2(w.x, -w.y) : w);
       }
-      sm[(q * 16 + t) * 8 + pp] = y;
+      sm[r32_slot<SW>(q, t, pp)] = y;
     }
   }
-  __syncthreads();
+  if (SW) __syncwarp(); else __syncthreads();  // contiguous: a row's 16 threads share a warp and own their region
   double2 c[32];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
 #pragma unroll
-    for (int tt = 0; tt < 16; ++tt) c[16 * s + tt] = sm[((t + 16 * s) * 16 + tt) * 8 + pp];
+    for (int tt = 0; tt < 16; ++tt) c[16 * s + tt] = sm[r32_slot<SW>(t + 16 * s, tt, pp)];
   }
-  __syncthreads();
+  if (SW) __syncwarp(); else __syncthreads();
   dft16<INV>(c);       // Z_0[m + 4 k] in c[k + 4 m]
   dft16<INV>(c + 16);  // Z_1
 #pragma unroll
@@ -208,6 +218,49 @@ __global__ void __launch_bounds__(128, 2) fft_r32_kernel(const Args a, const int
   }
 #pragma unroll
   for (int r = 0; r < 32; ++r) stg_s(a.dst + gbase + r * gstride, v[r]);
+  pdl_trigger();
+}
+
+// Contiguous-axis two-transform programs with 32 points per thread (L = 512): G (inverse,
+// x scale, g, forward: the slab-sharded plan's fused evaluation) and STR_MID (forward, x E1,
+// inverse: strang).  8 rows per 128-thread CTA, 16 threads per row; a half-warp reads 256
+// contiguous bytes per load.
+template <int PROG>
+__global__ void __launch_bounds__(128, 2) fft_c32_kernel(const Args a, const int ntiles) {
+  extern __shared__ double2 sm[];
+  pdl_wait();
+  const uint64_t step = resolve_pos(a.flag, a.pos) >> 24;
+  if (a.flag && flag_skip(a.flag, step << 24)) return;
+  const int tid = threadIdx.x;
+  const int t = tid & 15, pp = tid >> 4;
+  const int row = blockIdx.x * 8 + pp;
+  const bool valid = blockIdx.x < ntiles && row < (int)a.O;
+  const int gbase = row * 512 + t;
+  double2 v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = valid ? ldg_s(a.src + gbase + 16 * r) : make_double2(0.0, 0.0);
+  if (PROG == FP_G) {
+    fft512_r32<true, true>(v, t, pp, sm);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      V<1> x;
+      x.c[0] = cscale(a.scale, v[r]);
+      v[r] = gfun<1>(a.nl, x).c[0];
+    }
+    fft512_r32<false, true>(v, t, pp, sm);
+  } else {  // FP_STR_MID
+    fft512_r32<false, true>(v, t, pp, sm);
+    double2 rf[2];
+    rf[1] = valid ? row_factor(a, 1, row) : make_double2(0.0, 0.0);
+    rf[0] = rf[1];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = cmul(efac(a, 1, rf, t + 16 * r), v[r]);
+    fft512_r32<true, true>(v, t, pp, sm);
+  }
+  if (valid) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) stg_s(a.dst + gbase + 16 * r, v[r]);
+  }
   pdl_trigger();
 }
 

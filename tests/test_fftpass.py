@@ -65,11 +65,13 @@ def test_single_axis_passes(shape):
             assert _relmax(y, ref) <= 1e-14
 
 
-@pytest.mark.parametrize("shape,axis", [((512, 16, 16), 0), ((32, 512, 16), 1), ((64, 16, 32), 0), ((16, 256), 1)])
+@pytest.mark.parametrize("shape,axis", [((512, 16, 16), 0), ((32, 512, 16), 1), ((64, 16, 32), 0), ((16, 256), 1),
+                                        ((16, 16, 512), 2), ((32, 512), 1)])
 def test_fused_g_pass(shape, axis):
     """program g = F g(scale F^-1 .) along one axis (integrators.py:99-101 on one
-    axis) against torch; 512-point strided pencils take the 32-points-per-thread
-    kernel (csrc/fftr32.cuh), the others the radix-8 plan."""
+    axis) against torch; 512-point pencils take the 32-points-per-thread kernels
+    (csrc/fftr32.cuh: strided fft_r32_kernel, contiguous fft_c32_kernel), the
+    others the radix-8 plan."""
     from paper_2403_02816_b200 import _lib, fftpass
     x = _rand(shape, 2)
     nl = _lib.Nonlinear()
@@ -83,6 +85,30 @@ def test_fused_g_pass(shape, axis):
     z = x.clone()   # in place
     fftpass.axis_pass(z, z, axis, program="g", ops=fftpass.make_ops(nl=nl, scale=scale))
     assert torch.equal(torch.view_as_real(z), torch.view_as_real(got))
+
+
+@pytest.mark.parametrize("shape", [(16, 16, 512), (32, 512), (16, 32, 128)])
+def test_strang_mid_pass(shape):
+    """program str_mid = F^-1 (E1 .* F .) along the contiguous axis (the linear
+    half of a Strang step, integrators.py:161-164 with spectral.py:116-129)
+    against torch, 30 repetitions bit-identical (the 512-point form exchanges
+    within half-warps behind warp barriers only)."""
+    from paper_2403_02816_b200 import fftpass
+    x = _rand(shape, 5)
+    d = len(shape)
+    tabs = [[torch.exp(-0.01 * fr * _rand((shape[a],), 20 + a).abs() ** 2 * (1 + 0.3j)) for a in range(d)]
+            for fr in (0.5, 1.0)]
+    e1 = tabs[1][0]
+    for a in range(1, d):
+        e1 = e1.unsqueeze(-1) * tabs[1][a]
+    want = torch.fft.ifft(e1 * torch.fft.fft(x, dim=d - 1), dim=d - 1) * shape[-1]
+    got = torch.empty_like(x)
+    fftpass.axis_pass(x, got, d - 1, program="str_mid", ops=fftpass.make_ops(tables=tabs))
+    assert _relmax(got, want) <= 1e-13
+    for _ in range(30):
+        again = torch.empty_like(x)
+        fftpass.axis_pass(x, again, d - 1, program="str_mid", ops=fftpass.make_ops(tables=tabs))
+        assert torch.equal(torch.view_as_real(again), torch.view_as_real(got))
 
 
 def test_unsupported_shapes_are_rejected():
