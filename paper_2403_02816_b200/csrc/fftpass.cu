@@ -356,10 +356,9 @@ static int launch_c32(const Args& a, cudaStream_t st) {
 
 template <int L, bool CONTIG, int PROG, bool INV>
 static int launch_one(const Args& a, cudaStream_t st) {
-  if constexpr (L == 512 && CONTIG && (PROG == FP_G || PROG == FP_STR_MID)) {
-    static const int c32 = [] { const char* e = getenv("CGL_FFT_C32"); return e ? atoi(e) : 1; }();
-    if (c32) return launch_c32<PROG>(a, st);
-  }
+  // two-transform programs at 512 points: 32 points per thread, one exchange per transform
+  // (contiguous: STR_MID 1131 vs 1413 us with the radix-8 ring kernel, profiles/r02j_fft_probe.txt)
+  if constexpr (L == 512 && CONTIG && (PROG == FP_G || PROG == FP_STR_MID)) return launch_c32<PROG>(a, st);
   // the two-transform G pass is bound by the shared-memory data pipe: 32 points per thread
   // (one exchange per transform) take 1.15 ms at 512^3 against 1.50 ms for the radix-8 plan;
   // the single-transform passes are HBM/latency-bound and keep the 8-point kernel (0.76-0.87
