@@ -27,7 +27,9 @@
 extern "C" {
 #endif
 
-#define CGL_ABI_VERSION 1
+/* 2: cgl_oz_gemm_fused removed; cgl_rk_stage, CGL_FFT_STR_A0F, nonlinearity kind 3 added; the
+ * IF4_B1..B4 pass programs accumulate the Lawson combination in one field */
+#define CGL_ABI_VERSION 2
 
 #define CGL_EINVAL (-1)
 #define CGL_ESHAPE (-2)

@@ -42,7 +42,7 @@ def test_library_is_sm100a():
 def test_version_and_abi():
     from paper_2403_02816_b200 import _lib
     lib = _lib.load()
-    assert lib.cgl_abi_version() == 1
+    assert lib.cgl_abi_version() == 2
     assert b"sm_100a" in lib.cgl_version()
 
 
