@@ -15,9 +15,12 @@
 //   * the Lawson stage combinations (integrators.py:205-215) and the
 //     separable exp(f tau symbol) multipliers run between the forward pass of
 //     g_i and the inverse pass of the next stage input along the contiguous
-//     axis (one kernel: forward -> g_i -> stage -> inverse);
+//     axis (one kernel: forward -> g_i -> stage -> inverse); the combination
+//     u' = E1 (u + t/6 g1) + t/3 E1/2 (g2 + g3) + t/6 g4 accumulates term by
+//     term in one field, so a stage reads at most one extra operand;
 //   * strang: the end-of-step flow, the finiteness check, the next step's
-//     first flow and the forward pass share one kernel along the slowest axis;
+//     first flow and the forward pass share one kernel along the slowest axis
+//     (for the exact cubic flow the two flows are evaluated as one, STR_A0F);
 //     E1 rides between the forward and inverse passes of the contiguous axis.
 // Per-pass layout:
 //   contiguous axis (stride 1): a CTA owns 4096/L whole rows; thread t of a
@@ -33,6 +36,9 @@
 // two shared-memory exchanges per 512-point pencil.  Twiddles come from one
 // correctly rounded 512-entry table (fft_twiddles.h).  Unnormalised both
 // ways (the 1/N of ifftn is applied by the program that consumes the inverse).
+// The two-transform programs at 512 points (G; STR_MID) are bound by the
+// shared-memory data pipe: they run with 32 points per thread, radix-32 x
+// radix-16 and ONE exchange per transform (fftr32.cuh).
 #include "fftpass.cuh"
 #include "fftr32.cuh"
 

@@ -16,9 +16,13 @@ keeps what a size-independent comparison needs (as make_golden_c2_full.py):
 
     python tests/golden/make_golden_full.py C3 512 strang,if4
     python tests/golden/make_golden_full.py C4 64 if4
+    python tests/golden/make_golden_full.py C4 512 if4 4     # the FIRST 4 steps only
 
 -> tests/golden/full_<C>_<n>.npz (one file per config and grid; the keys of
-each scheme are prefixed "<scheme>_"; an existing file is extended).
+each scheme are prefixed "<scheme>_"; an existing file is extended), or, with
+a step count, tests/golden/steps_<C>_<n>.npz (the reference's 512^3 C4 run takes
+~8 min per step on this container: the first steps pin the 512^3 code path, the
+full 50 steps are pinned at 256^3 and 64^3).
 """
 import json
 import os
@@ -80,8 +84,10 @@ def main():
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else None
     base = W.CONFIGS[cfg]
     w = base if n == base.extents[0] else base.scaled(n)
+    if steps is not None:
+        w = w.scaled(n, steps)
     n_steps = steps or w.steps
-    path = os.path.join(HERE, f"full_{cfg}_{n}.npz")
+    path = os.path.join(HERE, f"full_{cfg}_{n}.npz" if steps is None else f"steps_{cfg}_{n}.npz")
     arrays, metas = {}, []
     if os.path.exists(path) and steps is None:
         with np.load(path) as z:
@@ -107,8 +113,8 @@ def main():
             arrays[f"{scheme}_{k}"] = v
         metas.append(meta)
         del out, res
-        if steps is None:   # checkpoint after every scheme (the 512^3 runs take hours)
-            np.savez_compressed(path, meta=np.array(json.dumps(metas)), **arrays)
+        # checkpoint after every scheme (the 512^3 runs take hours)
+        np.savez_compressed(path, meta=np.array(json.dumps(metas)), **arrays)
 
 
 if __name__ == "__main__":

@@ -35,7 +35,7 @@ RESULTS = os.environ.get("CGL_FULLRUN_LOG")  # optional JSON-lines record of the
 
 def _cases():
     out = []
-    for path in sorted(glob.glob(os.path.join(GOLDEN, "full_*.npz"))):
+    for path in sorted(glob.glob(os.path.join(GOLDEN, "full_*.npz")) + glob.glob(os.path.join(GOLDEN, "steps_*.npz"))):
         with np.load(path) as z:
             for m in json.loads(str(z["meta"])):
                 out.append((os.path.basename(path), m["scheme"]))
@@ -51,6 +51,8 @@ def test_full_run_against_reference(fname, scheme):
     base = W.CONFIGS[meta["config"]]
     n = meta["extents"][0]
     w = base if n == base.extents[0] else base.scaled(n)
+    if fname.startswith("steps_"):   # the first meta["steps"] steps of the run (512^3 C4: ~8 min of reference per step)
+        w = w.scaled(n, meta["steps"])
     assert list(w.extents) == meta["extents"] and meta["steps"] == w.steps and meta["tau"] == w.tau
     prob = W.build_problem(w)
     x0 = W.state_for_problem(w, W.initial_state_device(w))
