@@ -16,12 +16,12 @@ keeps what a size-independent comparison needs (as make_golden_c2_full.py):
 
     python tests/golden/make_golden_full.py C3 512 strang,if4
     python tests/golden/make_golden_full.py C4 64 if4
-    python tests/golden/make_golden_full.py C4 512 if4 4     # the FIRST 4 steps only
+    python tests/golden/make_golden_full.py C4 512 if4 16    # the FIRST 16 steps only
 
 -> tests/golden/full_<C>_<n>.npz (one file per config and grid; the keys of
 each scheme are prefixed "<scheme>_"; an existing file is extended), or, with
 a step count, tests/golden/steps_<C>_<n>.npz (the reference's 512^3 C4 run takes
-~8 min per step on this container: the first steps pin the 512^3 code path, the
+~4 min per step on this container: the first steps pin the 512^3 code path, the
 full 50 steps are pinned at 256^3 and 64^3).
 """
 import json

@@ -14,8 +14,8 @@ the band's largest |u_ref| (`band_rel`), and relative to the global peak
 C3 (512^3 Fourier) and C4 (FD Dirichlet) run at their full step counts; C4's
 1024^3 grid needs ~210 GB of host RAM for the reference, so its full 50 steps
 are pinned at 64^3 and 256^3 on the identical code path (the
-reference takes 26 min at 256^3 and would take ~4 h at 512^3, where its first
-steps are pinned: steps_C4_512.npz).
+reference takes 26 min at 256^3 and would take ~3.4 h at 512^3, where its
+first 16 steps are pinned: steps_C4_512.npz, 64 min of reference time).
 """
 
 import glob
